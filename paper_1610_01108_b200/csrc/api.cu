@@ -1,0 +1,282 @@
+// C-ABI of the B200 decoder (include/amun_b200.h): device model handle,
+// length-bucketed batched beam-search decode, and the per-step parity hooks.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/amun_b200.h"
+#include "common.cuh"
+#include "decode.cuh"
+#include "gemm_simt.cuh"
+#include "kernels.cuh"
+
+using namespace amun;
+
+static thread_local std::string g_last_error;
+
+#define AMUN_API_BEGIN try {
+#define AMUN_API_END                                  \
+  }                                                   \
+  catch (const ::amun::Error &e) {                    \
+    g_last_error = e.what();                          \
+    return e.code;                                    \
+  }                                                   \
+  catch (const std::exception &e) {                   \
+    g_last_error = e.what();                          \
+    return AMUN_ERR_CUDA;                             \
+  }                                                   \
+  return AMUN_OK;
+
+static void invalid(const std::string &m) { throw Error(AMUN_ERR_INVALID, m); }
+
+extern "C" const char *amun_last_error(void) { return g_last_error.c_str(); }
+extern "C" int amun_version(void) { return 1; }
+
+extern "C" int amun_device_count(int32_t *n) {
+  AMUN_API_BEGIN
+  int c = 0;
+  AMUN_CUDA(cudaGetDeviceCount(&c));
+  *n = c;
+  AMUN_API_END
+}
+
+// ------------------------------------------------------------------ model
+
+namespace {
+
+// schema order (model.py:94-117)
+enum {
+  T_E_SRC = 0, T_E_TRG = 1,
+  T_ENC_FWD = 2, T_ENC_BWD = 11, T_DEC = 20,  // + {W_z W_r W_h U_z U_r U_h b_z b_r b_h}
+  T_W_INIT = 29, T_B_INIT, T_W_ATT_S, T_W_ATT_H, T_V_ATT, T_W_OUT_S, T_W_OUT_Y, T_W_OUT_C, T_B_OUT,
+  T_W_LOGIT, T_B_LOGIT, T_COUNT
+};
+enum { G_WZ = 0, G_WR, G_WH, G_UZ, G_UR, G_UH, G_BZ, G_BR, G_BH };
+
+}  // namespace
+
+static float *upload(amun_model *m, const std::vector<float> &h) {
+  float *d = nullptr;
+  AMUN_CUDA(cudaMalloc(&d, h.size() * sizeof(float)));
+  m->allocs.push_back(d);
+  AMUN_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  m->bytes += (int64_t)(h.size() * sizeof(float));
+  return d;
+}
+
+extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const float *const *t,
+                                 int32_t n_tensors, amun_model **out) {
+  amun_model *m = nullptr;
+  AMUN_API_BEGIN
+  if (!dims || !t || !out) invalid("null argument");
+  if (n_tensors != T_COUNT) invalid("expected 40 tensors in schema order, got " + std::to_string(n_tensors));
+  if (dims->d_emb < 1 || dims->d_h < 1 || dims->d_att < 1 || dims->v_src < 2 || dims->v_trg < 2)
+    invalid("invalid model dimensions");
+  for (int i = 0; i < T_COUNT; ++i)
+    if (!t[i]) invalid("null tensor pointer " + std::to_string(i));
+  int ndev = 0;
+  AMUN_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) invalid("device " + std::to_string(device) + " out of range");
+  AMUN_CUDA(cudaSetDevice(device));
+  m = new amun_model();
+  m->device = device;
+  m->d = *dims;
+  const int de = dims->d_emb, dh = dims->d_h, da = dims->d_att, V = dims->v_trg, Vs = dims->v_src;
+  const int din = de + 2 * dh;  // decoder GRU input [y ; c]
+  m->xs_w = de + 3 * dh;
+  auto cp = [&](int idx, size_t n) { return std::vector<float>(t[idx], t[idx] + n); };
+
+  m->E_src = upload(m, cp(T_E_SRC, (size_t)Vs * de));
+  m->E_trg = upload(m, cp(T_E_TRG, (size_t)V * de));
+  {  // encoder input projection, both directions: [de, 6dh] = [fwd z r h | bwd z r h]
+    std::vector<float> W((size_t)de * 6 * dh), b(6 * dh);
+    for (int dir = 0; dir < 2; ++dir) {
+      int base = dir ? T_ENC_BWD : T_ENC_FWD;
+      for (int g = 0; g < 3; ++g) {
+        const float *src = t[base + G_WZ + g];
+        for (int i = 0; i < de; ++i)
+          std::memcpy(&W[(size_t)i * 6 * dh + (dir * 3 + g) * dh], src + (size_t)i * dh, dh * sizeof(float));
+        std::memcpy(&b[(dir * 3 + g) * dh], t[base + G_BZ + g], dh * sizeof(float));
+      }
+    }
+    m->Wenc = upload(m, W);
+    m->benc = upload(m, b);
+  }
+  {  // encoder recurrent weights: Uzr [2][dh][2dh], Uh [2][dh][dh]
+    std::vector<float> Uzr((size_t)2 * dh * 2 * dh), Uh((size_t)2 * dh * dh);
+    for (int dir = 0; dir < 2; ++dir) {
+      int base = dir ? T_ENC_BWD : T_ENC_FWD;
+      for (int i = 0; i < dh; ++i) {
+        std::memcpy(&Uzr[((size_t)dir * dh + i) * 2 * dh], t[base + G_UZ] + (size_t)i * dh, dh * sizeof(float));
+        std::memcpy(&Uzr[((size_t)dir * dh + i) * 2 * dh + dh], t[base + G_UR] + (size_t)i * dh, dh * sizeof(float));
+      }
+      std::memcpy(&Uh[(size_t)dir * dh * dh], t[base + G_UH], (size_t)dh * dh * sizeof(float));
+    }
+    m->Uzr = upload(m, Uzr);
+    m->Uh = upload(m, Uh);
+  }
+  m->W_att_h = upload(m, cp(T_W_ATT_H, (size_t)2 * dh * da));
+  m->W_init = upload(m, cp(T_W_INIT, (size_t)2 * dh * dh));
+  m->b_init = upload(m, cp(T_B_INIT, dh));
+  m->W_att_s = upload(m, cp(T_W_ATT_S, (size_t)dh * da));
+  m->v_att = upload(m, cp(T_V_ATT, da));
+  {  // decoder gates: rows [y ; c ; s] (= XS columns), cols [z | r | h];
+     // the h block of the s rows is zero (reset-before-matmul: s enters h~
+     // only through (r*s) U_h, applied in phase B).
+    std::vector<float> Wg((size_t)(din + dh) * 3 * dh, 0.f), bg(3 * dh);
+    for (int g = 0; g < 3; ++g) {
+      const float *W = t[T_DEC + G_WZ + g];
+      for (int i = 0; i < din; ++i)
+        std::memcpy(&Wg[(size_t)i * 3 * dh + g * dh], W + (size_t)i * dh, dh * sizeof(float));
+      if (g < 2) {
+        const float *U = t[T_DEC + G_UZ + g];
+        for (int i = 0; i < dh; ++i)
+          std::memcpy(&Wg[(size_t)(din + i) * 3 * dh + g * dh], U + (size_t)i * dh, dh * sizeof(float));
+      }
+      std::memcpy(&bg[g * dh], t[T_DEC + G_BZ + g], dh * sizeof(float));
+    }
+    m->Wg = upload(m, Wg);
+    m->bg = upload(m, bg);
+    m->Uh_dec = upload(m, cp(T_DEC + G_UH, (size_t)dh * dh));
+  }
+  {  // deep output: rows [y ; c ; s'] = [W_out_y ; W_out_c ; W_out_s]
+    std::vector<float> Wo((size_t)(de + 3 * dh) * de);
+    std::memcpy(&Wo[0], t[T_W_OUT_Y], (size_t)de * de * sizeof(float));
+    std::memcpy(&Wo[(size_t)de * de], t[T_W_OUT_C], (size_t)2 * dh * de * sizeof(float));
+    std::memcpy(&Wo[(size_t)(de + 2 * dh) * de], t[T_W_OUT_S], (size_t)dh * de * sizeof(float));
+    m->Wout = upload(m, Wo);
+    m->b_out = upload(m, cp(T_B_OUT, de));
+  }
+  m->W_logit = upload(m, cp(T_W_LOGIT, (size_t)de * V));
+  m->b_logit = upload(m, cp(T_B_LOGIT, V));
+  AMUN_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  *out = m;
+  m = nullptr;
+  }
+  catch (const ::amun::Error &e) {
+    g_last_error = e.what();
+    if (m) amun_model_destroy(m);
+    return e.code;
+  }
+  catch (const std::exception &e) {
+    g_last_error = e.what();
+    if (m) amun_model_destroy(m);
+    return AMUN_ERR_CUDA;
+  }
+  return AMUN_OK;
+}
+
+extern "C" int amun_model_destroy(amun_model *m) {
+  if (!m) return AMUN_OK;
+  cudaSetDevice(m->device);
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  for (void *p : m->allocs) cudaFree(p);
+  if (m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+  return AMUN_OK;
+}
+
+extern "C" int amun_model_device_bytes(const amun_model *m, int64_t *bytes) {
+  AMUN_API_BEGIN
+  if (!m || !bytes) invalid("null argument");
+  *bytes = m->bytes;
+  AMUN_API_END
+}
+
+// ------------------------------------------------------------------ decode
+
+extern "C" int amun_decode(amun_model *const *models, int32_t n_models, const int32_t *src_ids,
+                           const int32_t *src_len, int32_t n_sent, const int32_t *sl_ids,
+                           const int32_t *sl_len, const amun_decode_opts *opts, amun_result **out) {
+  AMUN_API_BEGIN
+  if (!models || n_models < 1) invalid("at least one model is required");
+  if (!opts || !out || (n_sent > 0 && (!src_ids || !src_len))) invalid("null argument");
+  *out = nullptr;
+  std::vector<amun_model *> ms(models, models + n_models);
+  for (auto *m : ms) {
+    if (!m) invalid("null model handle");
+    if (m->device != ms[0]->device) invalid("ensemble members must live on the same device");
+    if (m->d.v_src != ms[0]->d.v_src || m->d.v_trg != ms[0]->d.v_trg)
+      invalid("model vocabulary mismatch");
+  }
+  *out = decode_run(ms, src_ids, src_len, n_sent, sl_ids, sl_len, *opts);
+  AMUN_API_END
+}
+
+extern "C" int amun_result_free(amun_result *r) {
+  if (!r) return AMUN_OK;
+  free(r->hyp_offsets);
+  free(r->scores);
+  free(r->finished);
+  free(r->tok_offsets);
+  free(r->tokens);
+  free(r->states);
+  free(r);
+  return AMUN_OK;
+}
+
+// ------------------------------------------------------------------ hooks
+
+extern "C" int amun_encode(amun_model *m, const int32_t *ids, int32_t J, float *h_out, float *p_out,
+                           float *s0_out) {
+  AMUN_API_BEGIN
+  if (!m || !ids) invalid("null argument");
+  if (J < 1) invalid("cannot encode an empty source sentence");
+  for (int j = 0; j < J; ++j)
+    if (ids[j] < 0 || ids[j] >= m->d.v_src)
+      invalid("source id " + std::to_string(ids[j]) + " at position " + std::to_string(j) +
+              " out of range for v_src=" + std::to_string(m->d.v_src));
+  hook_encode(m, ids, J, h_out, p_out, s0_out);
+  AMUN_API_END
+}
+
+extern "C" int amun_attention(amun_model *m, const float *s, int32_t R, const float *h, const float *p,
+                              int32_t J, float *alpha_out, float *ctx_out) {
+  AMUN_API_BEGIN
+  if (!m || !s || !h || !p) invalid("null argument");
+  if (R < 1 || J < 1) invalid("attention needs at least one state row and one source position");
+  hook_step(m, s, nullptr, R, h, p, J, nullptr, 0, nullptr, nullptr, alpha_out, ctx_out);
+  AMUN_API_END
+}
+
+extern "C" int amun_decoder_step(amun_model *m, const float *s, const int32_t *y_prev, int32_t R,
+                                 const float *h, const float *p, int32_t J, const int32_t *sl, int32_t n_sl,
+                                 float *s_out, double *logp_out, float *alpha_out) {
+  AMUN_API_BEGIN
+  if (!m || !s || !y_prev || !h || !p) invalid("null argument");
+  if (R < 1 || J < 1) invalid("decoder step needs at least one state row and one source position");
+  for (int r = 0; r < R; ++r)
+    if (y_prev[r] < 0 || y_prev[r] >= m->d.v_trg)
+      invalid("previous token id " + std::to_string(y_prev[r]) + " out of range for v_trg=" +
+              std::to_string(m->d.v_trg));
+  if (sl) {
+    if (n_sl < 1) invalid("shortlist must be non-empty");
+    for (int i = 0; i < n_sl; ++i)
+      if (sl[i] < 0 || sl[i] >= m->d.v_trg)
+        invalid("shortlist id " + std::to_string(sl[i]) + " out of range for v_trg=" + std::to_string(m->d.v_trg));
+  }
+  hook_step(m, s, y_prev, R, h, p, J, sl, n_sl, s_out, logp_out, alpha_out, nullptr);
+  AMUN_API_END
+}
+
+extern "C" int amun_init_state(amun_model *m, const float *h, int32_t J, float *s0_out) {
+  AMUN_API_BEGIN
+  if (!m || !h || !s0_out) invalid("null argument");
+  if (J < 1) invalid("annotations must have at least one source position");
+  hook_init_state(m, h, J, s0_out);
+  AMUN_API_END
+}
+
+extern "C" int amun_gru_cell(int32_t device, int32_t d_in, int32_t d_h, const float *const *W,
+                             const float *const *U, const float *const *b, int32_t R, const float *x,
+                             const float *h, float *h_out) {
+  AMUN_API_BEGIN
+  if (!W || !U || !b || !x || !h || !h_out) invalid("null argument");
+  for (int i = 0; i < 3; ++i)
+    if (!W[i] || !U[i] || !b[i]) invalid("null weight pointer");
+  if (d_in < 1 || d_h < 1 || R < 1) invalid("invalid GRU cell dimensions");
+  hook_gru_cell(device, d_in, d_h, W, U, b, R, x, h, h_out);
+  AMUN_API_END
+}

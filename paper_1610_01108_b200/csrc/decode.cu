@@ -1,0 +1,767 @@
+// Decode driver: length buckets -> batched encoder -> device-resident beam
+// search loop (all bookkeeping on the device) -> host back-pointer walk and
+// final ranking.  Mirrors search.py:116-216 for a batch of sentences, the
+// way engine.py:181-221 fans sentences out — but as one device batch.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "decode.cuh"
+#include "gemm_simt.cuh"
+#include "kernels.cuh"
+
+namespace amun {
+
+namespace {
+
+struct Carver {  // bump allocator; base == nullptr -> sizing pass
+  char *base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T *take(size_t n) {
+    size_t a = (off + 255) & ~size_t(255);
+    off = a + n * sizeof(T);
+    return base ? reinterpret_cast<T *>(base + a) : nullptr;
+  }
+};
+
+struct DevMem {  // owning stream-ordered device allocation
+  void *p = nullptr;
+  cudaStream_t st = nullptr;
+  DevMem() = default;
+  DevMem(const DevMem &) = delete;
+  DevMem &operator=(const DevMem &) = delete;
+  void alloc(size_t n, cudaStream_t s) {
+    st = s;
+    AMUN_CUDA(cudaMallocAsync(&p, std::max<size_t>(n, 256), s));
+  }
+  ~DevMem() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+// Launch context: stream, launch counter, byte counters, and (when
+// profiling) CUDA-event pairs around every launch, bucketed by kernel class.
+struct Ctx {
+  cudaStream_t st;
+  int64_t launches = 0;
+  int64_t h2d = 0, d2h = 0;
+  bool prof = false;
+  int cls = AMUN_K_ENCODER;
+  std::vector<cudaEvent_t> pool;
+  std::vector<int> rec_cls;
+  size_t used = 0;
+  double kms[AMUN_K_CLASSES] = {0};
+  int64_t kcount[AMUN_K_CLASSES] = {0};
+  explicit Ctx(cudaStream_t s) : st(s) {}
+  ~Ctx() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+  cudaEvent_t next_event() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      AMUN_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  template <class F>
+  void run(int k, F &&f) {
+    ++launches;
+    if (!prof) {
+      f();
+      return;
+    }
+    AMUN_CUDA(cudaEventRecord(next_event(), st));
+    f();
+    AMUN_CUDA(cudaEventRecord(next_event(), st));
+    rec_cls.push_back(k);
+  }
+  // call after the stream is synchronised: fold recorded pairs into totals
+  void collect() {
+    for (size_t i = 0; i < rec_cls.size(); ++i) {
+      float ms = 0.f;
+      AMUN_CUDA(cudaEventElapsedTime(&ms, pool[2 * i], pool[2 * i + 1]));
+      kms[rec_cls[i]] += ms;
+      kcount[rec_cls[i]] += 1;
+    }
+    rec_cls.clear();
+    used = 0;
+  }
+};
+
+GemmArgs ga(int M, int N, const float *a0, int lda0, int k0, const float *B, int ldb) {
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.a0 = a0;
+  g.lda0 = lda0;
+  g.k0 = k0;
+  g.rows0 = nullptr;
+  g.a1 = nullptr;
+  g.lda1 = 0;
+  g.k1 = 0;
+  g.B = B;
+  g.ldb = ldb;
+  g.n_split = INT_MAX;
+  g.k_limit = INT_MAX;
+  g.a_zs = 0;
+  g.b_zs = 0;
+  return g;
+}
+
+template <class Epi>
+void gemm(Ctx &c, const GemmArgs &g, const Epi &e, int nz = 1) {
+  c.run(c.cls, [&] { launch_gemm_simt(g, e, nz, c.st); });
+}
+
+// Encoder buffers of one model for a bucket of B sentences, jmax positions.
+struct EncBufs {
+  float *XP, *Hann, *P, *Hs, *Zs, *RHs, *Hmean, *S0;
+};
+// Decoder row buffers of one model for R hypothesis rows.
+struct DecBufs {
+  float *XS, *Sn, *Q, *Z, *RH, *XH, *T, *L;
+};
+
+void carve_enc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
+  const int dh = m->d.d_h, da = m->d.d_att;
+  e.XP = cv.take<float>((size_t)B * jmax * 6 * dh);
+  e.Hann = cv.take<float>((size_t)B * jmax * 2 * dh);
+  e.P = cv.take<float>((size_t)B * jmax * da);
+  e.Hs = cv.take<float>((size_t)2 * B * dh);
+  e.Zs = cv.take<float>((size_t)2 * B * dh);
+  e.RHs = cv.take<float>((size_t)2 * B * dh);
+  e.Hmean = cv.take<float>((size_t)B * 2 * dh);
+  e.S0 = cv.take<float>((size_t)B * dh);
+}
+
+void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, bool full_logits) {
+  const int dh = m->d.d_h, da = m->d.d_att, de = m->d.d_emb;
+  d.XS = cv.take<float>((size_t)R * m->xs_w);
+  d.Sn = cv.take<float>((size_t)R * dh);
+  d.Q = cv.take<float>((size_t)R * da);
+  d.Z = cv.take<float>((size_t)R * dh);
+  d.RH = cv.take<float>((size_t)R * dh);
+  d.XH = cv.take<float>((size_t)R * dh);
+  d.T = cv.take<float>((size_t)R * de);
+  d.L = full_logits ? cv.take<float>((size_t)R * m->d.v_trg) : nullptr;
+}
+
+// nnet.py:110-130 for B padded sentences: input projection (embedding
+// gather fused into the A-load), the bi-GRU recurrence (both directions per
+// launch), precomp_att, masked mean and the initial decoder state.
+void encode_bucket(Ctx &c, const amun_model *m, const EncBufs &e, const int *d_ids, const int *d_len, int B,
+                   int jmax) {
+  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att;
+  c.cls = AMUN_K_ENCODER;
+  {
+    GemmArgs g = ga(B * jmax, 6 * dh, m->E_src, de, de, m->Wenc, 6 * dh);
+    g.rows0 = d_ids;
+    gemm(c, g, EpiStore{e.XP, 6 * dh, m->benc, 0, 0});
+  }
+  AMUN_CUDA(cudaMemsetAsync(e.Hs, 0, sizeof(float) * 2 * B * dh, c.st));
+  AMUN_CUDA(cudaMemsetAsync(e.Hann, 0, sizeof(float) * (size_t)B * jmax * 2 * dh, c.st));
+  for (int t = 0; t < jmax; ++t) {
+    GemmArgs a = ga(B, 2 * dh, e.Hs, dh, dh, m->Uzr, 2 * dh);
+    a.a_zs = (long long)B * dh;
+    a.b_zs = (long long)dh * 2 * dh;
+    gemm(c, a, EpiEncA{e.XP, e.Hs, d_len, jmax, dh, t, B, e.Zs, e.RHs}, 2);
+    GemmArgs b = ga(B, dh, e.RHs, dh, dh, m->Uh, dh);
+    b.a_zs = (long long)B * dh;
+    b.b_zs = (long long)dh * dh;
+    gemm(c, b, EpiEncB{e.XP, e.Hs, d_len, jmax, dh, t, B, e.Zs, e.Hann}, 2);
+  }
+  gemm(c, ga(B * jmax, da, e.Hann, 2 * dh, 2 * dh, m->W_att_h, da), EpiStore{e.P, da, nullptr, 0, 0});
+  c.run(AMUN_K_ENCODER, [&] { launch_masked_mean(e.Hann, d_len, B, jmax, 2 * dh, e.Hmean, c.st); });
+  gemm(c, ga(B, dh, e.Hmean, 2 * dh, 2 * dh, m->W_init, dh), EpiStore{e.S0, dh, m->b_init, 1, 0});
+}
+
+// nnet.py:143-161 for R rows: query, attention (-> ctx into XS), GRU phase
+// A/B, deep output, logits (fused top-k partials or full logits).
+struct LogitOut {
+  bool fused;
+  int kk, ntiles;
+  float *pmax, *psum, *cval;
+  int *ctok;
+};
+
+void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
+               int R, int rows_per_sent, const int *n_act, const int *done, float *alpha, const LogitOut &lo) {
+  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
+  const int s_off = de + 2 * dh;
+  c.cls = AMUN_K_QUERY;
+  gemm(c, ga(R, da, d.XS + s_off, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
+  AttnArgs aa{d.Q, da, e.P, e.Hann, m->v_att, d_len, jmax, da, 2 * dh, rows_per_sent, n_act, done,
+              d.XS + de, xs, alpha};
+  c.run(AMUN_K_ATTN, [&] { launch_attention(aa, R, c.st); });
+  c.cls = AMUN_K_GRU_A;
+  {
+    GemmArgs g = ga(R, 3 * dh, d.XS, xs, xs, m->Wg, 3 * dh);
+    g.n_split = 2 * dh;
+    g.k_limit = de + 2 * dh;
+    gemm(c, g, EpiGruA{m->bg, d.XS + s_off, xs, dh, d.Z, d.RH, d.XH});
+  }
+  c.cls = AMUN_K_GRU_B;
+  gemm(c, ga(R, dh, d.RH, dh, dh, m->Uh_dec, dh), EpiGruB{d.XS + s_off, xs, dh, d.Z, d.XH, d.Sn});
+  c.cls = AMUN_K_OUT;
+  {
+    GemmArgs g = ga(R, de, d.XS, xs, de + 2 * dh, m->Wout, de);
+    g.a1 = d.Sn;
+    g.lda1 = dh;
+    g.k1 = dh;
+    gemm(c, g, EpiStore{d.T, de, m->b_out, 1, 0});
+  }
+  c.cls = AMUN_K_LOGIT;
+  GemmArgs g = ga(R, V, d.T, de, de, m->W_logit, V);
+  if (lo.fused)
+    gemm(c, g, EpiLogitTopK{m->b_logit, lo.kk, lo.ntiles, lo.pmax, lo.psum, lo.cval, lo.ctok});
+  else
+    gemm(c, g, EpiStore{d.L, V, m->b_logit, 0, 0});
+}
+
+__global__ void build_rows_kernel(float *XS, int ldxs, const float *E, const int *y, const float *s, int de, int dh,
+                                  int s_off) {
+  const int r = blockIdx.x;
+  float *row = XS + (long long)r * ldxs;
+  for (int c = threadIdx.x; c < de; c += blockDim.x) row[c] = y ? E[(long long)y[r] * de + c] : 0.f;
+  for (int c = threadIdx.x; c < dh; c += blockDim.x) row[s_off + c] = s[(long long)r * dh + c];
+}
+
+struct HostHyp {
+  double score;
+  int finished;
+  std::vector<int> toks;
+  std::vector<float> state;  // n_models * dh (optional)
+};
+
+template <class T>
+void h2d(Ctx &c, T *dst, const T *src, size_t n) {
+  if (n) AMUN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, c.st));
+  c.h2d += (int64_t)(n * sizeof(T));
+}
+template <class T>
+void d2h(Ctx &c, T *dst, const T *src, size_t n) {
+  if (n) AMUN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, c.st));
+  c.d2h += (int64_t)(n * sizeof(T));
+}
+
+}  // namespace
+
+// ====================================================================== decode
+
+amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_ids, const int32_t *src_len,
+                        int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o) {
+  amun_model *m0 = ms[0];
+  AMUN_CUDA(cudaSetDevice(m0->device));
+  const int n_models = (int)ms.size();
+  const int k = o.beam_size;
+  if (k < 1) throw Error(AMUN_ERR_INVALID, "beam_size must be >= 1, got " + std::to_string(k));
+  if (o.n_best < 1) throw Error(AMUN_ERR_INVALID, "n_best must be >= 1, got " + std::to_string(o.n_best));
+  const int V = m0->d.v_trg, Vs = m0->d.v_src, dh = m0->d.d_h;
+  std::vector<long long> off(n_sent + 1, 0), sl_offs(n_sent + 1, 0);
+  for (int i = 0; i < n_sent; ++i) {
+    if (src_len[i] < 1) throw Error(AMUN_ERR_INVALID, "cannot decode an empty source sentence");
+    long long cap = (long long)o.max_len_factor * src_len[i] + o.max_len_offset;
+    if (cap < 1) throw Error(AMUN_ERR_INVALID, "length cap " + std::to_string(cap) + " must be >= 1");
+    off[i + 1] = off[i] + src_len[i];
+    if (sl_ids) {
+      if (sl_len[i] < 1) throw Error(AMUN_ERR_INVALID, "shortlist must be non-empty");
+      sl_offs[i + 1] = sl_offs[i] + sl_len[i];
+    }
+  }
+  for (long long j = 0; j < off[n_sent]; ++j)
+    if (src_ids[j] < 0 || src_ids[j] >= Vs)
+      throw Error(AMUN_ERR_INVALID, "source id " + std::to_string(src_ids[j]) + " out of range for v_src=" +
+                                        std::to_string(Vs));
+  if (sl_ids)
+    for (long long j = 0; j < sl_offs[n_sent]; ++j)
+      if (sl_ids[j] < 0 || sl_ids[j] >= V)
+        throw Error(AMUN_ERR_INVALID, "shortlist id " + std::to_string(sl_ids[j]) + " out of range for v_trg=" +
+                                          std::to_string(V));
+
+  const int Bmax_opt = o.max_batch > 0 ? o.max_batch : 64;
+  const bool fused = n_models == 1 && !sl_ids && k <= kMaxRowCand && !o.force_full_logits;
+  const int kk = std::min(k, V);
+  const int ntiles = ceil_div(V, kBN);
+
+  // length buckets: stable sort by source length, cut every Bmax sentences
+  std::vector<int> order(n_sent);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return src_len[a] < src_len[b]; });
+  struct Bucket {
+    int first, count, jmax, cap_max;
+  };
+  std::vector<Bucket> buckets;
+  int Bmax = 0, jmax_all = 0, cap_all = 0, sl_max = 0;
+  for (int s = 0; s < n_sent; s += Bmax_opt) {
+    Bucket bk{s, std::min(Bmax_opt, n_sent - s), 0, 0};
+    for (int i = bk.first; i < bk.first + bk.count; ++i) {
+      int L = src_len[order[i]];
+      bk.jmax = std::max(bk.jmax, L);
+      bk.cap_max = std::max(bk.cap_max, o.max_len_factor * L + o.max_len_offset);
+    }
+    Bmax = std::max(Bmax, bk.count);
+    jmax_all = std::max(jmax_all, bk.jmax);
+    cap_all = std::max(cap_all, bk.cap_max);
+    if (sl_ids) {
+      int tot = 0;
+      for (int i = bk.first; i < bk.first + bk.count; ++i) tot += sl_len[order[i]];
+      sl_max = std::max(sl_max, tot);
+    }
+    buckets.push_back(bk);
+  }
+  const int Rmax = Bmax * k;
+  const int fin_cap = k * cap_all;
+
+  // ---- workspace
+  std::vector<EncBufs> eb(n_models);
+  std::vector<DecBufs> db(n_models);
+  std::vector<float *> fin_states(n_models, nullptr);
+  int *d_ids, *d_len, *d_cap, *d_sl, *d_sl_off, *d_sl_len;
+  float *pmax, *psum, *cval;
+  int *ctok, *cand_tok;
+  double *cand_lp;
+  BeamState bs{};
+  float **p_XS;
+  const float **p_Sn, **p_E, **p_S0, **p_L;
+  float **p_fin;
+  DevMem mem;
+  for (int pass = 0; pass < 2; ++pass) {
+    Carver cv;
+    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
+    for (int m = 0; m < n_models; ++m) {
+      carve_enc(cv, eb[m], ms[m], Bmax, jmax_all);
+      carve_dec(cv, db[m], ms[m], Rmax, !fused);
+      fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * dh) : nullptr;
+    }
+    d_ids = cv.take<int>((size_t)Bmax * jmax_all);
+    d_len = cv.take<int>(Bmax);
+    d_cap = cv.take<int>(Bmax);
+    d_sl = cv.take<int>(std::max(sl_max, 1));
+    d_sl_off = cv.take<int>(Bmax);
+    d_sl_len = cv.take<int>(Bmax);
+    pmax = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
+    psum = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
+    cval = cv.take<float>(fused ? (size_t)Rmax * ntiles * kk : 1);
+    ctok = cv.take<int>(fused ? (size_t)Rmax * ntiles * kk : 1);
+    cand_lp = cv.take<double>((size_t)Rmax * kk);
+    cand_tok = cv.take<int>((size_t)Rmax * kk);
+    bs.n_act = cv.take<int>(Bmax);
+    bs.score = cv.take<double>(Rmax);
+    bs.tok = cv.take<int>(Rmax);
+    bs.done = cv.take<int>(Bmax);
+    bs.steps = cv.take<int>(Bmax);
+    bs.cap = d_cap;
+    bs.fin_n = cv.take<int>(Bmax);
+    bs.fin_score = cv.take<double>((size_t)Bmax * fin_cap);
+    bs.fin_t = cv.take<int>((size_t)Bmax * fin_cap);
+    bs.fin_par = cv.take<int>((size_t)Bmax * fin_cap);
+    bs.best_fin = cv.take<double>(Bmax);
+    bs.bp_tok = cv.take<int>((size_t)Bmax * cap_all * k);
+    bs.bp_par = cv.take<int>((size_t)Bmax * cap_all * k);
+    bs.n_done = cv.take<int>(1);
+    p_XS = cv.take<float *>(n_models);
+    p_Sn = cv.take<const float *>(n_models);
+    p_E = cv.take<const float *>(n_models);
+    p_S0 = cv.take<const float *>(n_models);
+    p_L = cv.take<const float *>(n_models);
+    p_fin = cv.take<float *>(n_models);
+    if (!pass) mem.alloc(cv.off, m0->stream);
+  }
+  Ctx c(m0->stream);
+  c.prof = o.profile != 0;
+  cudaStream_t st = c.st;
+  {
+    std::vector<const void *> hx(n_models), hs(n_models), he(n_models), h0(n_models), hl(n_models), hf(n_models);
+    for (int m = 0; m < n_models; ++m) {
+      hx[m] = db[m].XS;
+      hs[m] = db[m].Sn;
+      he[m] = ms[m]->E_trg;
+      h0[m] = eb[m].S0;
+      hl[m] = db[m].L;
+      hf[m] = fin_states[m];
+    }
+    h2d(c, (const void **)p_XS, hx.data(), n_models);
+    h2d(c, (const void **)p_Sn, hs.data(), n_models);
+    h2d(c, (const void **)p_E, he.data(), n_models);
+    h2d(c, (const void **)p_S0, h0.data(), n_models);
+    h2d(c, (const void **)p_L, hl.data(), n_models);
+    h2d(c, (const void **)p_fin, hf.data(), n_models);
+  }
+  int *h_ndone = nullptr;
+  AMUN_CUDA(cudaMallocHost(&h_ndone, sizeof(int)));
+  struct PinnedFree {
+    int *p;
+    ~PinnedFree() { cudaFreeHost(p); }
+  } pf{h_ndone};
+
+  cudaEvent_t ev0, ev1;
+  AMUN_CUDA(cudaEventCreate(&ev0));
+  AMUN_CUDA(cudaEventCreate(&ev1));
+  AMUN_CUDA(cudaEventRecord(ev0, st));
+
+  std::vector<std::vector<HostHyp>> out_hyps(n_sent);
+  int64_t total_steps = 0;
+  const int xs = m0->xs_w;
+  const int de = m0->d.d_emb;
+
+  for (const Bucket &bk : buckets) {
+    const int B = bk.count, jmax = bk.jmax, capm = bk.cap_max, R = B * k;
+    std::vector<int> ids((size_t)B * jmax, 0), lens(B), caps(B), slo(B), sll(B), slv;
+    for (int i = 0; i < B; ++i) {
+      int s = order[bk.first + i];
+      lens[i] = src_len[s];
+      caps[i] = o.max_len_factor * src_len[s] + o.max_len_offset;
+      std::copy(src_ids + off[s], src_ids + off[s + 1], ids.begin() + (size_t)i * jmax);
+      if (sl_ids) {
+        slo[i] = (int)slv.size();
+        sll[i] = sl_len[s];
+        slv.insert(slv.end(), sl_ids + sl_offs[s], sl_ids + sl_offs[s + 1]);
+      }
+    }
+    h2d(c, d_ids, ids.data(), ids.size());
+    h2d(c, d_len, lens.data(), B);
+    h2d(c, d_cap, caps.data(), B);
+    if (sl_ids) {
+      h2d(c, d_sl, slv.data(), slv.size());
+      h2d(c, d_sl_off, slo.data(), B);
+      h2d(c, d_sl_len, sll.data(), B);
+    }
+    for (int m = 0; m < n_models; ++m) encode_bucket(c, ms[m], eb[m], d_ids, d_len, B, jmax);
+
+    bs.B = B;
+    bs.k = k;
+    bs.cap_max = capm;
+    bs.fin_cap = fin_cap;
+    ModelRows mr{p_XS, p_Sn, p_E, o.want_states ? p_fin : nullptr, xs, de, dh, de + 2 * dh, n_models};
+    c.run(AMUN_K_SELECT, [&] { launch_init_beam(bs, mr, p_S0, st); });
+    LogitOut lo{fused, kk, ntiles, pmax, psum, cval, ctok};
+    SelectArgs sa{};
+    sa.kk = kk;
+    sa.fused = fused;
+    sa.V = V;
+    sa.pmax = pmax;
+    sa.psum = psum;
+    sa.cval = cval;
+    sa.ctok = ctok;
+    sa.ntiles = ntiles;
+    sa.M = R;
+    sa.L = p_L;
+    sa.ldl = V;
+    sa.sl_ids = sl_ids ? d_sl : nullptr;
+    sa.sl_off = d_sl_off;
+    sa.sl_len = d_sl_len;
+    sa.cand_lp = cand_lp;
+    sa.cand_tok = cand_tok;
+    int steps_run = 0;
+    for (int t = 0; t < capm; ++t) {
+      for (int m = 0; m < n_models; ++m)
+        step_rows(c, ms[m], db[m], eb[m], d_len, jmax, R, k, bs.n_act, bs.done, nullptr, lo);
+      sa.t = t;
+      c.run(AMUN_K_SELECT, [&] { launch_select(sa, bs, mr, st); });
+      ++steps_run;
+      if ((t & 7) == 7 && t + 1 < capm) {  // cheap early-exit probe
+        d2h(c, h_ndone, bs.n_done, 1);
+        AMUN_CUDA(cudaStreamSynchronize(st));
+        if (*h_ndone >= B) break;
+      }
+    }
+    total_steps += steps_run;
+
+    // ---- read back beam state and walk back-pointers (search.py:200-216)
+    std::vector<int> n_act(B), steps(B), fin_n(B), fin_t((size_t)B * fin_cap), fin_par((size_t)B * fin_cap);
+    std::vector<int> bp_tok((size_t)B * capm * k), bp_par((size_t)B * capm * k);
+    std::vector<double> score(R), fin_score((size_t)B * fin_cap);
+    d2h(c, n_act.data(), bs.n_act, B);
+    d2h(c, steps.data(), bs.steps, B);
+    d2h(c, fin_n.data(), bs.fin_n, B);
+    d2h(c, score.data(), bs.score, R);
+    d2h(c, fin_score.data(), bs.fin_score, (size_t)B * fin_cap);
+    d2h(c, fin_t.data(), bs.fin_t, (size_t)B * fin_cap);
+    d2h(c, fin_par.data(), bs.fin_par, (size_t)B * fin_cap);
+    d2h(c, bp_tok.data(), bs.bp_tok, (size_t)B * capm * k);
+    d2h(c, bp_par.data(), bs.bp_par, (size_t)B * capm * k);
+    std::vector<float> act_states, fin_st;
+    if (o.want_states) {
+      act_states.resize((size_t)n_models * R * dh);
+      fin_st.resize((size_t)n_models * B * fin_cap * dh);
+      for (int m = 0; m < n_models; ++m) {
+        AMUN_CUDA(cudaMemcpy2DAsync(act_states.data() + (size_t)m * R * dh, dh * sizeof(float),
+                                    db[m].XS + de + 2 * dh, xs * sizeof(float), dh * sizeof(float), R,
+                                    cudaMemcpyDeviceToHost, st));
+        d2h(c, fin_st.data() + (size_t)m * B * fin_cap * dh, fin_states[m], (size_t)B * fin_cap * dh);
+      }
+    }
+    AMUN_CUDA(cudaStreamSynchronize(st));
+    c.collect();
+    auto walk = [&](int i, int tt, int slot) {
+      std::vector<int> seq;
+      for (; tt >= 0; --tt) {
+        size_t o2 = ((size_t)i * capm + tt) * k + slot;
+        seq.push_back(bp_tok[o2]);
+        slot = bp_par[o2];
+      }
+      std::reverse(seq.begin(), seq.end());
+      return seq;
+    };
+    for (int i = 0; i < B; ++i) {
+      const int s = order[bk.first + i];
+      std::vector<HostHyp> hyps;
+      if (fin_n[i] > 0) {
+        for (int f = 0; f < fin_n[i]; ++f) {
+          size_t fo = (size_t)i * fin_cap + f;
+          HostHyp h{fin_score[fo], 1, walk(i, fin_t[fo] - 1, fin_par[fo]), {}};
+          h.toks.push_back(0);
+          if (o.want_states)
+            for (int m = 0; m < n_models; ++m) {
+              const float *p = fin_st.data() + ((size_t)m * B * fin_cap + fo) * dh;
+              h.state.insert(h.state.end(), p, p + dh);
+            }
+          hyps.push_back(std::move(h));
+        }
+      } else {
+        for (int a = 0; a < n_act[i]; ++a) {
+          HostHyp h{score[(size_t)i * k + a], 0, walk(i, steps[i] - 1, a), {}};
+          if (o.want_states)
+            for (int m = 0; m < n_models; ++m) {
+              const float *p = act_states.data() + ((size_t)m * R + (size_t)i * k + a) * dh;
+              h.state.insert(h.state.end(), p, p + dh);
+            }
+          hyps.push_back(std::move(h));
+        }
+      }
+      auto rank = [&](const HostHyp &h) {
+        return (o.length_normalize && !h.toks.empty()) ? h.score / (double)h.toks.size() : h.score;
+      };
+      std::stable_sort(hyps.begin(), hyps.end(), [&](const HostHyp &a, const HostHyp &b) {
+        double ra = rank(a), rb = rank(b);
+        if (ra != rb) return ra > rb;
+        return a.toks < b.toks;
+      });
+      if ((int)hyps.size() > o.n_best) hyps.resize(o.n_best);
+      out_hyps[s] = std::move(hyps);
+    }
+  }
+  AMUN_CUDA(cudaEventRecord(ev1, st));
+  AMUN_CUDA(cudaEventSynchronize(ev1));
+  float ms_elapsed = 0.f;
+  AMUN_CUDA(cudaEventElapsedTime(&ms_elapsed, ev0, ev1));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+
+  // ---- assemble the flat result
+  amun_result *r = static_cast<amun_result *>(calloc(1, sizeof(amun_result)));
+  r->n_sent = n_sent;
+  r->n_models = n_models;
+  r->d_h = dh;
+  int64_t nh = 0, nt = 0;
+  for (auto &v : out_hyps)
+    for (auto &h : v) {
+      ++nh;
+      nt += (int64_t)h.toks.size();
+    }
+  r->n_hyp = nh;
+  r->hyp_offsets = static_cast<int32_t *>(malloc(sizeof(int32_t) * (n_sent + 1)));
+  r->scores = static_cast<double *>(malloc(sizeof(double) * std::max<int64_t>(nh, 1)));
+  r->finished = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nh, 1)));
+  r->tok_offsets = static_cast<int64_t *>(malloc(sizeof(int64_t) * (nh + 1)));
+  r->tokens = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nt, 1)));
+  r->states = o.want_states ? static_cast<float *>(malloc(sizeof(float) * std::max<int64_t>(nh * n_models * dh, 1)))
+                            : nullptr;
+  int64_t hi = 0, ti = 0;
+  r->tok_offsets[0] = 0;
+  for (int s = 0; s < n_sent; ++s) {
+    r->hyp_offsets[s] = (int32_t)hi;
+    for (auto &h : out_hyps[s]) {
+      r->scores[hi] = h.score;
+      r->finished[hi] = h.finished;
+      std::copy(h.toks.begin(), h.toks.end(), r->tokens + ti);
+      ti += (int64_t)h.toks.size();
+      r->tok_offsets[hi + 1] = ti;
+      if (r->states) std::copy(h.state.begin(), h.state.end(), r->states + hi * n_models * dh);
+      ++hi;
+    }
+  }
+  r->hyp_offsets[n_sent] = (int32_t)hi;
+  r->decoder_steps = total_steps;
+  r->kernel_launches = c.launches;
+  r->device_ms = ms_elapsed;
+  r->h2d_bytes = c.h2d;
+  r->d2h_bytes = c.d2h;
+  for (int i = 0; i < AMUN_K_CLASSES; ++i) {
+    r->kernel_ms[i] = c.kms[i];
+    r->kernel_count[i] = c.kcount[i];
+  }
+  return r;
+}
+
+// ====================================================================== hooks
+
+void hook_encode(amun_model *m, const int32_t *ids, int J, float *h_out, float *p_out, float *s0_out) {
+  AMUN_CUDA(cudaSetDevice(m->device));
+  Ctx c(m->stream);
+  EncBufs e{};
+  int *d_ids, *d_len;
+  DevMem mem;
+  for (int pass = 0; pass < 2; ++pass) {
+    Carver cv;
+    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
+    carve_enc(cv, e, m, 1, J);
+    d_ids = cv.take<int>(J);
+    d_len = cv.take<int>(1);
+    if (!pass) mem.alloc(cv.off, c.st);
+  }
+  h2d(c, d_ids, ids, J);
+  h2d(c, d_len, &J, 1);
+  encode_bucket(c, m, e, d_ids, d_len, 1, J);
+  const int dh = m->d.d_h, da = m->d.d_att;
+  if (h_out) d2h(c, h_out, e.Hann, (size_t)J * 2 * dh);
+  if (p_out) d2h(c, p_out, e.P, (size_t)J * da);
+  if (s0_out) d2h(c, s0_out, e.S0, dh);
+  AMUN_CUDA(cudaStreamSynchronize(c.st));
+}
+
+void hook_step(amun_model *m, const float *s, const int32_t *y_prev, int R, const float *h, const float *p, int J,
+               const int32_t *sl, int n_sl, float *s_out, double *logp_out, float *alpha_out, float *ctx_out) {
+  AMUN_CUDA(cudaSetDevice(m->device));
+  Ctx c(m->stream);
+  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
+  EncBufs e{};
+  DecBufs d{};
+  int *d_len, *d_y, *d_sl;
+  float *d_s, *d_alpha;
+  double *d_logp;
+  const int n_out = sl ? n_sl : V;
+  DevMem mem;
+  for (int pass = 0; pass < 2; ++pass) {
+    Carver cv;
+    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
+    e.Hann = cv.take<float>((size_t)J * 2 * dh);
+    e.P = cv.take<float>((size_t)J * da);
+    carve_dec(cv, d, m, R, true);
+    d_len = cv.take<int>(1);
+    d_y = cv.take<int>(R);
+    d_sl = cv.take<int>(std::max(n_sl, 1));
+    d_s = cv.take<float>((size_t)R * dh);
+    d_alpha = cv.take<float>((size_t)R * J);
+    d_logp = cv.take<double>((size_t)R * n_out);
+    if (!pass) mem.alloc(cv.off, c.st);
+  }
+  h2d(c, e.Hann, h, (size_t)J * 2 * dh);
+  h2d(c, e.P, p, (size_t)J * da);
+  h2d(c, d_len, &J, 1);
+  h2d(c, d_s, s, (size_t)R * dh);
+  if (y_prev) h2d(c, d_y, y_prev, R);
+  if (sl) h2d(c, d_sl, sl, n_sl);
+  AMUN_CUDA(cudaMemsetAsync(d.XS, 0, sizeof(float) * (size_t)R * xs, c.st));
+  build_rows_kernel<<<R, 256, 0, c.st>>>(d.XS, xs, m->E_trg, y_prev ? d_y : nullptr, d_s, de, dh, de + 2 * dh);
+  AMUN_CHECK_LAUNCH();
+  if (!y_prev) {  // attention only (nnet.py:132-141)
+    gemm(c, ga(R, da, d.XS + de + 2 * dh, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
+    AttnArgs aa{d.Q, da, e.P, e.Hann, m->v_att, d_len, J, da, 2 * dh, R, nullptr, nullptr, d.XS + de, xs, d_alpha};
+    launch_attention(aa, R, c.st);
+  } else {
+    LogitOut lo{false, 0, 0, nullptr, nullptr, nullptr, nullptr};
+    step_rows(c, m, d, e, d_len, J, R, R, nullptr, nullptr, d_alpha, lo);
+    launch_logp_rows(d.L, V, R, V, sl ? d_sl : nullptr, n_sl, d_logp, c.st);
+  }
+  if (alpha_out) d2h(c, alpha_out, d_alpha, (size_t)R * J);
+  if (ctx_out)
+    AMUN_CUDA(cudaMemcpy2DAsync(ctx_out, 2 * dh * sizeof(float), d.XS + de, xs * sizeof(float),
+                                2 * dh * sizeof(float), R, cudaMemcpyDeviceToHost, c.st));
+  if (s_out) d2h(c, s_out, d.Sn, (size_t)R * dh);
+  if (logp_out && y_prev) d2h(c, logp_out, d_logp, (size_t)R * n_out);
+  AMUN_CUDA(cudaStreamSynchronize(c.st));
+}
+
+}  // namespace amun
+
+namespace amun {
+
+void hook_init_state(amun_model *m, const float *h, int J, float *s0_out) {
+  AMUN_CUDA(cudaSetDevice(m->device));
+  Ctx c(m->stream);
+  const int dh = m->d.d_h;
+  float *d_h, *d_mean, *d_s0;
+  int *d_len;
+  DevMem mem;
+  for (int pass = 0; pass < 2; ++pass) {
+    Carver cv;
+    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
+    d_h = cv.take<float>((size_t)J * 2 * dh);
+    d_mean = cv.take<float>(2 * dh);
+    d_s0 = cv.take<float>(dh);
+    d_len = cv.take<int>(1);
+    if (!pass) mem.alloc(cv.off, c.st);
+  }
+  h2d(c, d_h, h, (size_t)J * 2 * dh);
+  h2d(c, d_len, &J, 1);
+  launch_masked_mean(d_h, d_len, 1, J, 2 * dh, d_mean, c.st);
+  gemm(c, ga(1, dh, d_mean, 2 * dh, 2 * dh, m->W_init, dh), EpiStore{d_s0, dh, m->b_init, 1, 0});
+  d2h(c, s0_out, d_s0, dh);
+  AMUN_CUDA(cudaStreamSynchronize(c.st));
+}
+
+// Standalone GRU cell (nnet.py:177-185): same phase A / phase B kernels as
+// the decoder, with rows [x | h] and fused weights [[W_z W_r W_h];[U_z U_r 0]].
+void hook_gru_cell(int device, int d_in, int dh, const float *const *W, const float *const *U,
+                   const float *const *b, int R, const float *x, const float *h, float *h_out) {
+  AMUN_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  AMUN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } sg{st};
+  Ctx c(st);
+  const int w = d_in + dh;
+  std::vector<float> Wg((size_t)w * 3 * dh, 0.f), bg(3 * dh), rows((size_t)R * w);
+  for (int g = 0; g < 3; ++g) {
+    for (int i = 0; i < d_in; ++i)
+      std::memcpy(&Wg[(size_t)i * 3 * dh + g * dh], W[g] + (size_t)i * dh, dh * sizeof(float));
+    if (g < 2)
+      for (int i = 0; i < dh; ++i)
+        std::memcpy(&Wg[(size_t)(d_in + i) * 3 * dh + g * dh], U[g] + (size_t)i * dh, dh * sizeof(float));
+    std::memcpy(&bg[g * dh], b[g], dh * sizeof(float));
+  }
+  for (int r = 0; r < R; ++r) {
+    std::memcpy(&rows[(size_t)r * w], x + (size_t)r * d_in, d_in * sizeof(float));
+    std::memcpy(&rows[(size_t)r * w + d_in], h + (size_t)r * dh, dh * sizeof(float));
+  }
+  float *d_W, *d_b, *d_Uh, *d_rows, *d_Z, *d_RH, *d_XH, *d_out;
+  DevMem mem;
+  for (int pass = 0; pass < 2; ++pass) {
+    Carver cv;
+    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
+    d_W = cv.take<float>(Wg.size());
+    d_b = cv.take<float>(bg.size());
+    d_Uh = cv.take<float>((size_t)dh * dh);
+    d_rows = cv.take<float>(rows.size());
+    d_Z = cv.take<float>((size_t)R * dh);
+    d_RH = cv.take<float>((size_t)R * dh);
+    d_XH = cv.take<float>((size_t)R * dh);
+    d_out = cv.take<float>((size_t)R * dh);
+    if (!pass) mem.alloc(cv.off, st);
+  }
+  h2d(c, d_W, Wg.data(), Wg.size());
+  h2d(c, d_b, bg.data(), bg.size());
+  h2d(c, d_Uh, U[2], (size_t)dh * dh);
+  h2d(c, d_rows, rows.data(), rows.size());
+  GemmArgs g = ga(R, 3 * dh, d_rows, w, w, d_W, 3 * dh);
+  g.n_split = 2 * dh;
+  g.k_limit = d_in;
+  gemm(c, g, EpiGruA{d_b, d_rows + d_in, w, dh, d_Z, d_RH, d_XH});
+  gemm(c, ga(R, dh, d_RH, dh, dh, d_Uh, dh), EpiGruB{d_rows + d_in, w, dh, d_Z, d_XH, d_out});
+  d2h(c, h_out, d_out, (size_t)R * dh);
+  AMUN_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace amun

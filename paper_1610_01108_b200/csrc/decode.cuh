@@ -1,0 +1,45 @@
+// Device model handle and the decode / hook drivers behind the C ABI.
+#pragma once
+
+#include <vector>
+
+#include "../../include/amun_b200.h"
+#include "common.cuh"
+
+// Device-resident model in the fused layouts the kernels consume.  All
+// fp32, row-major, K rows x N cols ("B" operands of C = A * B).
+struct amun_model {
+  int device = 0;
+  amun_dims d{};
+  int xs_w = 0;  // decoder row width [y | c | s] = d_emb + 3 d_h
+  float *E_src = nullptr, *E_trg = nullptr;
+  float *Wenc = nullptr, *benc = nullptr;  // [de, 6dh], [6dh]  (fwd z r h | bwd z r h)
+  float *Uzr = nullptr, *Uh = nullptr;     // [2][dh][2dh], [2][dh][dh]
+  float *W_att_h = nullptr, *W_init = nullptr, *b_init = nullptr, *W_att_s = nullptr, *v_att = nullptr;
+  float *Wg = nullptr, *bg = nullptr;      // [de+3dh, 3dh], [3dh]
+  float *Uh_dec = nullptr;                 // [dh, dh]
+  float *Wout = nullptr, *b_out = nullptr; // [de+3dh, de], [de]
+  float *W_logit = nullptr, *b_logit = nullptr;  // [de, V], [V]
+  int64_t bytes = 0;
+  std::vector<void *> allocs;
+  cudaStream_t stream = nullptr;
+};
+
+namespace amun {
+
+amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_ids, const int32_t *src_len,
+                        int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o);
+
+void hook_encode(amun_model *m, const int32_t *ids, int J, float *h_out, float *p_out, float *s0_out);
+
+void hook_init_state(amun_model *m, const float *h, int J, float *s0_out);
+
+void hook_gru_cell(int device, int d_in, int d_h, const float *const *W, const float *const *U,
+                   const float *const *b, int R, const float *x, const float *h, float *h_out);
+
+// y_prev == nullptr -> attention only (alpha_out, ctx_out)
+void hook_step(amun_model *m, const float *s, const int32_t *y_prev, int R, const float *h, const float *p,
+               int J, const int32_t *sl, int n_sl, float *s_out, double *logp_out, float *alpha_out,
+               float *ctx_out);
+
+}  // namespace amun

@@ -1,0 +1,323 @@
+// FP32 CUDA-core GEMM with fused epilogues (the exact-FP32 baseline path and
+// the path for shapes the tensor-core kernel does not take: tiny test
+// models, the encoder recurrence at small batch, the hooks).
+//
+//   C[M, N] = A[M, K] * B[K, N]     (B row-major, N contiguous)
+//
+// A may be given as two row-major segments concatenated along K
+// ([a0 | a1], e.g. [y ; c ; s] and s' for the deep output), and segment 0 may
+// be row-gathered through an index array (embedding lookup fused into the
+// GEMM A-load, nnet.py:113 / :155).  blockIdx.z selects one of several
+// independent problems (the two encoder directions) via element strides.
+#pragma once
+
+#include "common.cuh"
+
+namespace amun {
+
+struct GemmArgs {
+  int M, N;
+  const float *a0;
+  int lda0, k0;
+  const int *rows0;  // optional row gather for segment 0
+  const float *a1;
+  int lda1, k1;
+  const float *B;
+  int ldb;
+  int n_split, k_limit;        // tiles with n0 >= n_split only use K <= k_limit
+  long long a_zs, b_zs;        // per-blockIdx.z element strides of a0 and B
+};
+
+constexpr int kBM = 64, kBN = 128, kBK = 16, kThreads = 256;
+constexpr int kApad = 4;
+constexpr int kSmemFloats =
+    (2 * kBK * (kBM + kApad) + 2 * kBK * kBN) > (kBM * (kBN + 1)) ? (2 * kBK * (kBM + kApad) + 2 * kBK * kBN)
+                                                                   : (kBM * (kBN + 1));
+
+// Elementwise epilogue interface: operator()(m, n, acc, z) for m < M, n < N.
+// Tile epilogues (kTile == true) instead get the full BM x BN tile staged in
+// shared memory (row stride kBN + 1) and run with all 256 threads.
+
+template <class Epi>
+__global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmArgs g, Epi epi) {
+  __shared__ __align__(16) float smem[kSmemFloats];
+  float *As = smem;                               // [2][BK][BM + pad]
+  float *Bs = smem + 2 * kBK * (kBM + kApad);     // [2][BK][BN]
+  const int tid = threadIdx.x;
+  const int z = blockIdx.z;
+  const float *a0 = g.a0 + z * g.a_zs;
+  const float *Bp = g.B + z * g.b_zs;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  int K = g.k0 + g.k1;
+  if (n0 >= g.n_split && g.k_limit < K) K = g.k_limit;
+  const int nk = ceil_div(K, kBK);
+
+  // Per-thread A rows (4 rows, fixed over k): pointer bases for segment 0/1.
+  const float *arow0[4];
+  const float *arow1[4];
+  bool arow_ok[4];
+  const int a_kk = tid % kBK;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int r = tid / kBK + i * (kThreads / kBK);
+    int m = m0 + r;
+    arow_ok[i] = m < g.M;
+    int src = arow_ok[i] ? (g.rows0 ? g.rows0[m] : m) : 0;
+    arow0[i] = a0 + (long long)src * g.lda0;
+    arow1[i] = g.a1 ? g.a1 + (long long)(arow_ok[i] ? m : 0) * g.lda1 : nullptr;
+  }
+  const int b_n = tid % kBN;
+  const bool b_ok = (n0 + b_n) < g.N;
+
+  float ra[4], rb[8];
+  auto load = [&](int kt) {
+    const int kbase = kt * kBK;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int k = kbase + a_kk;
+      float v = 0.f;
+      if (arow_ok[i] && k < K) v = (k < g.k0) ? arow0[i][k] : arow1[i][k - g.k0];
+      ra[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int k = kbase + tid / kBN + i * (kThreads / kBN);
+      rb[i] = (b_ok && k < K) ? Bp[(long long)k * g.ldb + n0 + b_n] : 0.f;
+    }
+  };
+  auto store = [&](int buf) {
+    float *as = As + buf * kBK * (kBM + kApad);
+    float *bs = Bs + buf * kBK * kBN;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) as[a_kk * (kBM + kApad) + tid / kBK + i * (kThreads / kBK)] = ra[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bs[(tid / kBN + i * (kThreads / kBN)) * kBN + b_n] = rb[i];
+  };
+
+  const int ty = tid / 16, tx = tid % 16;
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  if (nk > 0) {
+    load(0);
+    store(0);
+  }
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    if (kt + 1 < nk) load(kt + 1);
+    const float *as = As + (kt & 1) * kBK * (kBM + kApad);
+    const float *bs = Bs + (kt & 1) * kBK * kBN;
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      float4 a = *reinterpret_cast<const float4 *>(as + kk * (kBM + kApad) + ty * 4);
+      float4 b0 = *reinterpret_cast<const float4 *>(bs + kk * kBN + tx * 4);
+      float4 b1 = *reinterpret_cast<const float4 *>(bs + kk * kBN + 64 + tx * 4);
+      float av[4] = {a.x, a.y, a.z, a.w};
+      float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) store((kt + 1) & 1);
+    __syncthreads();
+  }
+
+  if constexpr (Epi::kTile) {
+    float *Ct = smem;  // [BM][BN + 1]; all threads passed the last barrier
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int c = (j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+        Ct[(ty * 4 + i) * (kBN + 1) + c] = acc[i][j];
+      }
+    __syncthreads();
+    epi.tile(Ct, m0, n0, g.M, g.N, z);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int m = m0 + ty * 4 + i;
+      if (m >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int n = n0 + ((j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+        if (n < g.N) epi(m, n, acc[i][j], z);
+      }
+    }
+  }
+}
+
+template <class Epi>
+inline void launch_gemm_simt(const GemmArgs &g, const Epi &epi, int nz, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  dim3 grid(ceil_div(g.N, kBN), ceil_div(g.M, kBM), nz);
+  gemm_simt_kernel<Epi><<<grid, kThreads, 0, st>>>(g, epi);
+  AMUN_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------ epilogues
+
+// C = act(acc + bias)    act: 0 identity, 1 tanh
+struct EpiStore {
+  static constexpr bool kTile = false;
+  float *C;
+  int ldc;
+  const float *bias;
+  int act;
+  long long c_zs;
+  __device__ void operator()(int m, int n, float v, int z) const {
+    if (bias) v += bias[n];
+    if (act == 1) v = tanhf(v);
+    C[z * c_zs + (long long)m * ldc + n] = v;
+  }
+};
+
+// Decoder GRU phase A (nnet.py:66-69): columns [0,dh) -> z, [dh,2dh) -> r
+// (stored as r*h), [2dh,3dh) -> x W_h + b_h (the input half of h~).
+struct EpiGruA {
+  static constexpr bool kTile = false;
+  const float *bias;  // [3 dh]
+  const float *S;     // current state rows, stride lds
+  int lds, dh;
+  float *Z, *RH, *XH;  // [M, dh] each
+  __device__ void operator()(int m, int n, float v, int) const {
+    v += bias[n];
+    if (n < dh) {
+      Z[(long long)m * dh + n] = sigmoid_acc(v);
+    } else if (n < 2 * dh) {
+      int j = n - dh;
+      RH[(long long)m * dh + j] = sigmoid_acc(v) * S[(long long)m * lds + j];
+    } else {
+      XH[(long long)m * dh + n - 2 * dh] = v;
+    }
+  }
+};
+
+// Decoder GRU phase B (nnet.py:69-70): h~ = tanh(xW_h + b_h + (r*h)U_h),
+// s' = (1-z) s + z h~.
+struct EpiGruB {
+  static constexpr bool kTile = false;
+  const float *S;
+  int lds, dh;
+  const float *Z, *XH;
+  float *Sn;
+  __device__ void operator()(int m, int n, float v, int) const {
+    long long o = (long long)m * dh + n;
+    float ht = tanhf(v + XH[o]);
+    float zz = Z[o];
+    float s = S[(long long)m * lds + n];
+    Sn[o] = (1.0f - zz) * s + zz * ht;
+  }
+};
+
+// Encoder recurrence phase A, both directions (blockIdx.z = dir).
+// XP holds x W + b for all positions: [B*Jmax, 6 dh] = [fwd z r h | bwd z r h].
+struct EpiEncA {
+  static constexpr bool kTile = false;
+  const float *XP;
+  const float *Hs;  // [2][B][dh] states
+  const int *len;
+  int jmax, dh, t, B;
+  float *Z, *RH;  // [2][B][dh]
+  __device__ void operator()(int b, int n, float v, int dir) const {
+    int L = len[b];
+    if (t >= L) return;
+    int pos = dir == 0 ? t : L - 1 - t;
+    v += XP[((long long)b * jmax + pos) * 6 * dh + dir * 3 * dh + n];
+    long long o = ((long long)dir * B + b) * dh;
+    if (n < dh) {
+      Z[o + n] = sigmoid_acc(v);
+    } else {
+      int j = n - dh;
+      RH[o + j] = sigmoid_acc(v) * Hs[o + j];
+    }
+  }
+};
+
+struct EpiEncB {
+  static constexpr bool kTile = false;
+  const float *XP;
+  float *Hs;
+  const int *len;
+  int jmax, dh, t, B;
+  const float *Z;
+  float *Hann;  // [B][jmax][2 dh]
+  __device__ void operator()(int b, int n, float v, int dir) const {
+    int L = len[b];
+    if (t >= L) return;
+    int pos = dir == 0 ? t : L - 1 - t;
+    long long o = ((long long)dir * B + b) * dh + n;
+    float ht = tanhf(v + XP[((long long)b * jmax + pos) * 6 * dh + dir * 3 * dh + 2 * dh + n]);
+    float zz = Z[o];
+    float h = (1.0f - zz) * Hs[o] + zz * ht;
+    Hs[o] = h;
+    Hann[((long long)b * jmax + pos) * 2 * dh + dir * dh + n] = h;
+  }
+};
+
+// Logit epilogue, fused mode: per (row, N-tile) partial log-sum-exp and the
+// tile's top-kk (logit desc, token asc).  Full logits never reach HBM.
+//   pmax/psum: [ntiles][M]   cval/ctok: [M][ntiles][kk]
+struct EpiLogitTopK {
+  static constexpr bool kTile = true;
+  const float *bias;
+  int kk, ntiles;
+  float *pmax, *psum, *cval;
+  int *ctok;
+  __device__ void tile(const float *Ct, int m0, int n0, int M, int N, int) const {
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nt = n0 / kBN;
+    for (int r = warp; r < kBM; r += kThreads / 32) {
+      int m = m0 + r;
+      if (m >= M) break;
+      float v[4];
+      bool ok[4];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int c = lane + 32 * q;
+        ok[q] = (n0 + c) < N;
+        v[q] = ok[q] ? Ct[r * (kBN + 1) + c] + bias[n0 + c] : -INFINITY;
+        mx = fmaxf(mx, v[q]);
+      }
+      mx = warp_max(mx);
+      float se = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (ok[q]) se += expf(v[q] - mx);
+      se = warp_sum(se);
+      if (lane == 0) {
+        pmax[(long long)nt * M + m] = mx;
+        psum[(long long)nt * M + m] = se;
+      }
+      // kk passes of "best key strictly below the previous pick"
+      double lv = INFINITY;
+      int lt = -1;
+      long long base = ((long long)m * ntiles + nt) * kk;
+      for (int p = 0; p < kk; ++p) {
+        Key best{-INFINITY, 0x7fffffff, 0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!ok[q]) continue;
+          int tok = n0 + lane + 32 * q;
+          double x = v[q];
+          bool below = (x < lv) || (x == lv && tok > lt);
+          if (below && key_better(x, tok, 0, best.v, best.tok, 0)) best = Key{x, tok, 0};
+        }
+        best = warp_best(best);
+        if (lane == 0) {
+          cval[base + p] = best.tok == 0x7fffffff ? -INFINITY : (float)best.v;
+          ctok[base + p] = best.tok == 0x7fffffff ? -1 : best.tok;
+        }
+        lv = best.v;
+        lt = best.tok;
+      }
+    }
+  }
+};
+
+}  // namespace amun

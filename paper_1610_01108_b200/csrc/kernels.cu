@@ -1,0 +1,384 @@
+// Non-GEMM kernels of the decode path (see kernels.cuh).
+#include "kernels.cuh"
+
+namespace amun {
+
+// ================================================================ attention
+
+__global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
+  extern __shared__ float sm[];
+  float *q = sm;              // [da]
+  float *e = sm + a.da;       // [jmax]
+  __shared__ float s_red[2];
+  const int r = blockIdx.x;
+  const int b = r / a.rows_per_sent;
+  if (a.n_act) {
+    int slot = r % a.rows_per_sent;
+    if (a.done[b] || slot >= a.n_act[b]) return;
+  }
+  const int J = a.len[b];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int i = threadIdx.x; i < a.da; i += blockDim.x) q[i] = a.Q[(long long)r * a.ldq + i];
+  __syncthreads();
+  const float *Pb = a.P + (long long)b * a.jmax * a.da;
+  for (int j = warp; j < J; j += nw) {
+    const float *pj = Pb + (long long)j * a.da;
+    float acc = 0.f;
+    for (int i = lane; i < a.da; i += 32) acc = fmaf(a.v[i], tanhf(pj[i] + q[i]), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) e[j] = acc;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float mx = -INFINITY;
+    for (int j = lane; j < J; j += 32) mx = fmaxf(mx, e[j]);
+    mx = warp_max(mx);
+    float s = 0.f;
+    for (int j = lane; j < J; j += 32) {
+      float w = expf(e[j] - mx);
+      e[j] = w;
+      s += w;
+    }
+    s = warp_sum(s);
+    if (lane == 0) s_red[0] = s;
+  }
+  __syncthreads();
+  const float inv = 1.0f / s_red[0];
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    float al = e[j] * inv;
+    e[j] = al;
+    if (a.alpha) a.alpha[(long long)r * a.jmax + j] = al;
+  }
+  __syncthreads();
+  const float *Hb = a.H + (long long)b * a.jmax * a.dh2;
+  for (int c = threadIdx.x; c < a.dh2; c += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < J; ++j) acc = fmaf(e[j], Hb[(long long)j * a.dh2 + c], acc);
+    a.ctx[(long long)r * a.ldctx + c] = acc;
+  }
+}
+
+void launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
+  if (R <= 0) return;
+  size_t smem = sizeof(float) * (a.da + a.jmax);
+  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  attention_kernel<<<R, 256, smem, st>>>(a);
+  AMUN_CHECK_LAUNCH();
+}
+
+// ================================================================ encoder
+
+__global__ void masked_mean_kernel(const float *Hann, const int *len, int jmax, int dh2, float *out) {
+  const int b = blockIdx.x;
+  const int L = len[b];
+  const float *Hb = Hann + (long long)b * jmax * dh2;
+  for (int c = threadIdx.x; c < dh2; c += blockDim.x) {
+    float s = 0.f;
+    for (int j = 0; j < L; ++j) s += Hb[(long long)j * dh2 + c];
+    out[(long long)b * dh2 + c] = s / (float)L;
+  }
+}
+
+void launch_masked_mean(const float *Hann, const int *len, int B, int jmax, int dh2, float *out,
+                        cudaStream_t st) {
+  masked_mean_kernel<<<B, 256, 0, st>>>(Hann, len, jmax, dh2, out);
+  AMUN_CHECK_LAUNCH();
+}
+
+// ================================================================ beam init
+
+__global__ void init_beam_kernel(BeamState bs, ModelRows mr, const float *const *S0) {
+  const int b = blockIdx.x;
+  const int k = bs.k;
+  if (threadIdx.x == 0) {
+    bs.n_act[b] = 1;
+    bs.done[b] = 0;
+    bs.steps[b] = 0;
+    bs.fin_n[b] = 0;
+    bs.best_fin[b] = -INFINITY;
+    for (int i = 0; i < k; ++i) {
+      bs.score[b * k + i] = 0.0;
+      bs.tok[b * k + i] = 0;
+    }
+    if (b == 0) *bs.n_done = 0;
+  }
+  for (int m = 0; m < mr.n_models; ++m) {
+    float *XS = mr.XS[m];
+    const float *E = mr.E_trg[m];
+    for (int i = 0; i < k; ++i) {
+      float *row = XS + (long long)(b * k + i) * mr.ldxs;
+      for (int c = threadIdx.x; c < mr.ldxs; c += blockDim.x) {
+        float v = 0.f;
+        if (i == 0) {
+          if (c < mr.de) v = E[c];  // E_trg[EOS_ID]
+          else if (c >= mr.s_off && c < mr.s_off + mr.dh) v = S0[m][(long long)b * mr.dh + (c - mr.s_off)];
+        }
+        row[c] = v;
+      }
+    }
+  }
+}
+
+void launch_init_beam(const BeamState &bs, const ModelRows &mr, const float *const *S0, cudaStream_t st) {
+  init_beam_kernel<<<bs.B, 256, 0, st>>>(bs, mr, S0);
+  AMUN_CHECK_LAUNCH();
+}
+
+// ================================================================ select
+
+constexpr int kMaxModels = 8;
+
+__device__ __forceinline__ double combine_models(double l0, const double *lm, int n) {
+  // search.py:67-72 mean about the first member: first + mean(stack - first)
+  if (n == 1) return l0;
+  double acc = 0.0;
+  for (int m = 0; m < n; ++m) acc += (lm[m] - l0);
+  return l0 + acc / (double)n;
+}
+
+__global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs, ModelRows mr) {
+  extern __shared__ unsigned char smraw[];
+  const int k = bs.k;
+  double *ch_v = reinterpret_cast<double *>(smraw);     // [k]
+  int *ch_tok = reinterpret_cast<int *>(ch_v + k);      // [k]
+  int *ch_par = ch_tok + k;                             // [k]
+  int *fin_par = ch_par + k;                            // [k] finished this step: parent
+  int *fin_idx = fin_par + k;                           // [k]
+  __shared__ int s_nch, s_newna, s_nfin;
+
+  const int b = blockIdx.x;
+  if (bs.done[b]) return;
+  const int t = sa.t;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int na = bs.n_act[b];
+  const int kk = sa.kk;
+  const int n_models = mr.n_models;
+
+  // ---- phase 1: per active row, log-sum-exp and top-kk candidates
+  for (int i = warp; i < na; i += nw) {
+    const int r = b * k + i;
+    double *out_lp = sa.cand_lp + ((long long)b * k + i) * kk;
+    int *out_tok = sa.cand_tok + ((long long)b * k + i) * kk;
+    if (sa.fused) {
+      float mx = -INFINITY;
+      for (int tt = lane; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, sa.pmax[(long long)tt * sa.M + r]);
+      mx = warp_max(mx);
+      double s = 0.0;
+      for (int tt = lane; tt < sa.ntiles; tt += 32) {
+        long long o = (long long)tt * sa.M + r;
+        s += (double)sa.psum[o] * exp((double)sa.pmax[o] - (double)mx);
+      }
+      s = warp_sum_d(s);
+      const double lse = (double)mx + log(s);
+      const int n = sa.ntiles * kk;
+      const float *cv = sa.cval + (long long)r * n;
+      const int *ct = sa.ctok + (long long)r * n;
+      double lv = INFINITY;
+      int lt = -1;
+      for (int p = 0; p < kk; ++p) {
+        Key best{-INFINITY, 0x7fffffff, 0};
+        for (int e = lane; e < n; e += 32) {
+          int tok = ct[e];
+          if (tok < 0) continue;
+          double x = cv[e];
+          bool below = (x < lv) || (x == lv && tok > lt);
+          if (below && key_better(x, tok, 0, best.v, best.tok, 0)) best = Key{x, tok, 0};
+        }
+        best = warp_best(best);
+        if (lane == 0) {
+          bool none = best.tok == 0x7fffffff;
+          out_lp[p] = none ? -INFINITY : best.v - lse;
+          out_tok[p] = none ? -1 : best.tok;
+        }
+        lv = best.v;
+        lt = best.tok;
+      }
+    } else {
+      const int *ids = sa.sl_ids ? sa.sl_ids + sa.sl_off[b] : nullptr;
+      const int ncols = sa.sl_ids ? sa.sl_len[b] : sa.V;
+      double lse[kMaxModels];
+      for (int m = 0; m < n_models; ++m) {
+        const float *Lr = sa.L[m] + (long long)r * sa.ldl;
+        float mx = -INFINITY;
+        for (int c = lane; c < ncols; c += 32) mx = fmaxf(mx, Lr[ids ? ids[c] : c]);
+        mx = warp_max(mx);
+        double s = 0.0;
+        for (int c = lane; c < ncols; c += 32) s += exp((double)Lr[ids ? ids[c] : c] - (double)mx);
+        s = warp_sum_d(s);
+        lse[m] = (double)mx + log(s);
+      }
+      double lv = INFINITY;
+      int lt = -1;
+      for (int p = 0; p < kk; ++p) {
+        Key best{-INFINITY, 0x7fffffff, 0};
+        for (int c = lane; c < ncols; c += 32) {
+          int g = ids ? ids[c] : c;
+          double lm[kMaxModels];
+          for (int m = 0; m < n_models; ++m) lm[m] = (double)sa.L[m][(long long)r * sa.ldl + g] - lse[m];
+          double x = combine_models(lm[0], lm, n_models);
+          bool below = (x < lv) || (x == lv && g > lt);
+          if (below && key_better(x, g, 0, best.v, best.tok, 0)) best = Key{x, g, 0};
+        }
+        best = warp_best(best);
+        if (lane == 0) {
+          bool none = best.tok == 0x7fffffff;
+          out_lp[p] = none ? -INFINITY : best.v;
+          out_tok[p] = none ? -1 : best.tok;
+        }
+        lv = best.v;
+        lt = best.tok;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: sentence top-k over na*kk candidates, key (score desc,
+  // token asc, parent asc) with f64 scores (search.py:169-170, :75-91)
+  if (warp == 0) {
+    const int n = na * kk;
+    const double *clp = sa.cand_lp + (long long)b * k * kk;
+    const int *ctk = sa.cand_tok + (long long)b * k * kk;
+    double lv = INFINITY;
+    int lt = -1, lp_ = -1;
+    int nch = 0;
+    for (int p = 0; p < k; ++p) {
+      Key best{-INFINITY, 0x7fffffff, 0x7fffffff};
+      for (int e = lane; e < n; e += 32) {
+        int tok = ctk[e];
+        if (tok < 0) continue;
+        int par = e / kk;
+        double x = bs.score[b * k + par] + clp[e];
+        bool below = key_better(lv, lt, lp_, x, tok, par);
+        if (below && key_better(x, tok, par, best.v, best.tok, best.par)) best = Key{x, tok, par};
+      }
+      best = warp_best(best);
+      if (best.tok == 0x7fffffff) break;
+      if (lane == 0) {
+        ch_v[p] = best.v;
+        ch_tok[p] = best.tok;
+        ch_par[p] = best.par;
+      }
+      nch = p + 1;
+      lv = best.v;
+      lt = best.tok;
+      lp_ = best.par;
+    }
+    if (lane == 0) s_nch = nch;
+  }
+  __syncthreads();
+
+  // ---- phase 3: beam update (search.py:172-198)
+  if (threadIdx.x == 0) {
+    const int nch = s_nch;
+    int newna = 0, nfin = 0;
+    double best_new = -INFINITY;
+    const int rowbase = (b * bs.cap_max + t) * k;
+    for (int j = 0; j < nch; ++j) {
+      if (ch_tok[j] == 0) {  // EOS_ID -> finished list (unbounded in the reference)
+        int idx = bs.fin_n[b]++;
+        long long fo = (long long)b * bs.fin_cap + idx;
+        bs.fin_score[fo] = ch_v[j];
+        bs.fin_t[fo] = t;
+        bs.fin_par[fo] = ch_par[j];
+        if (ch_v[j] > bs.best_fin[b]) bs.best_fin[b] = ch_v[j];
+        fin_par[nfin] = ch_par[j];
+        fin_idx[nfin] = idx;
+        ++nfin;
+      } else {
+        int slot = newna++;
+        bs.bp_tok[rowbase + slot] = ch_tok[j];
+        bs.bp_par[rowbase + slot] = ch_par[j];
+        if (ch_v[j] > best_new) best_new = ch_v[j];
+        // reuse ch_* arrays in place: slot <= j always
+        ch_v[slot] = ch_v[j];
+        ch_tok[slot] = ch_tok[j];
+        ch_par[slot] = ch_par[j];
+      }
+    }
+    bs.steps[b] = t + 1;
+    int done = 0;
+    if (newna == 0) {
+      done = 1;  // search.py:186-187 (beam left as it was)
+    } else {
+      bs.n_act[b] = newna;
+      for (int i = 0; i < newna; ++i) {
+        bs.score[b * k + i] = ch_v[i];
+        bs.tok[b * k + i] = ch_tok[i];
+      }
+      if (bs.fin_n[b] > 0 && best_new <= bs.best_fin[b]) done = 1;  // search.py:195-198
+    }
+    if (t + 1 >= bs.cap[b]) done = 1;
+    if (done) {
+      bs.done[b] = 1;
+      atomicAdd(bs.n_done, 1);
+    }
+    s_newna = newna;
+    s_nfin = nfin;
+  }
+  __syncthreads();
+
+  // ---- phase 4: gather next-step decoder rows [E_trg[y] | . | s'_parent]
+  const int newna = s_newna, nfin = s_nfin;
+  for (int m = 0; m < n_models; ++m) {
+    float *XS = mr.XS[m];
+    const float *Sn = mr.Sn[m];
+    const float *E = mr.E_trg[m];
+    for (int i = 0; i < newna; ++i) {
+      float *row = XS + (long long)(b * k + i) * mr.ldxs;
+      const float *ey = E + (long long)ch_tok[i] * mr.de;
+      const float *sp = Sn + (long long)(b * k + ch_par[i]) * mr.dh;
+      for (int c = threadIdx.x; c < mr.de; c += blockDim.x) row[c] = ey[c];
+      for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) row[mr.s_off + c] = sp[c];
+    }
+    if (mr.fin_states) {
+      for (int i = 0; i < nfin; ++i) {
+        float *dst = mr.fin_states[m] + ((long long)b * bs.fin_cap + fin_idx[i]) * mr.dh;
+        const float *sp = Sn + (long long)(b * k + fin_par[i]) * mr.dh;
+        for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) dst[c] = sp[c];
+      }
+    }
+  }
+}
+
+void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, cudaStream_t st) {
+  if (mr.n_models > kMaxModels) throw Error(4, "at most 8 ensemble members are supported on the device path");
+  size_t smem = (size_t)bs.k * (sizeof(double) + 4 * sizeof(int));
+  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  select_kernel<<<bs.B, 256, smem, st>>>(sa, bs, mr);
+  AMUN_CHECK_LAUNCH();
+}
+
+// ================================================================ hook logp
+
+__global__ void logp_rows_kernel(const float *L, int ldl, int V, const int *sl, int n_sl, double *logp) {
+  const int r = blockIdx.x;
+  const int n = sl ? n_sl : V;
+  const float *Lr = L + (long long)r * ldl;
+  __shared__ float s_mx[32];
+  __shared__ double s_sum[32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) mx = fmaxf(mx, Lr[sl ? sl[c] : c]);
+  mx = warp_max(mx);
+  if (lane == 0) s_mx[warp] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int w = 0; w < nw; ++w) mx = fmaxf(mx, s_mx[w]);
+  double s = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) s += exp((double)Lr[sl ? sl[c] : c] - (double)mx);
+  s = warp_sum_d(s);
+  if (lane == 0) s_sum[warp] = s;
+  __syncthreads();
+  s = 0.0;
+  for (int w = 0; w < nw; ++w) s += s_sum[w];
+  const double lse = (double)mx + log(s);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) logp[(long long)r * n + c] = (double)Lr[sl ? sl[c] : c] - lse;
+}
+
+void launch_logp_rows(const float *L, int ldl, int R, int V, const int *sl, int n_sl, double *logp,
+                      cudaStream_t st) {
+  logp_rows_kernel<<<R, 256, 0, st>>>(L, ldl, V, sl, n_sl, logp);
+  AMUN_CHECK_LAUNCH();
+}
+
+}  // namespace amun

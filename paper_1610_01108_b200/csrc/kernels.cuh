@@ -1,0 +1,84 @@
+// Non-GEMM kernels of the decode path: MLP attention, encoder helpers,
+// beam initialisation, and the fused select / beam-update / state-gather.
+#pragma once
+
+#include "common.cuh"
+
+namespace amun {
+
+// ---------------------------------------------------------------- attention
+// nnet.py:132-141 for a batch of hypothesis rows.  One CTA per row r
+// (sentence b = r / rows_per_sent): e_j = v . tanh(P_bj + q_r) with one warp
+// per source position, masked softmax over j < len[b], ctx = sum_j a_j H_bj
+// written straight into the decoder input buffer.
+struct AttnArgs {
+  const float *Q;  // [R, ldq]
+  int ldq;
+  const float *P;  // [B][jmax][da]
+  const float *H;  // [B][jmax][2 dh]
+  const float *v;  // [da]
+  const int *len;
+  int jmax, da, dh2, rows_per_sent;
+  const int *n_act, *done;  // optional beam masks
+  float *ctx;
+  int ldctx;
+  float *alpha;  // optional [R][jmax]
+};
+void launch_attention(const AttnArgs &a, int R, cudaStream_t st);
+
+// ---------------------------------------------------------------- encoder
+// masked mean over real positions: out[b] = sum_{j < len_b} Hann[b, j] / len_b
+void launch_masked_mean(const float *Hann, const int *len, int B, int jmax, int dh2, float *out,
+                        cudaStream_t st);
+
+// ---------------------------------------------------------------- beam state
+struct BeamState {
+  int B, k, cap_max, fin_cap;
+  int *n_act;        // [B]
+  double *score;     // [B*k]
+  int *tok;          // [B*k] last emitted token per slot
+  int *done;         // [B]
+  int *steps;        // [B]
+  const int *cap;    // [B]
+  int *fin_n;        // [B]
+  double *fin_score; // [B*fin_cap]
+  int *fin_t, *fin_par;
+  double *best_fin;  // [B]
+  int *bp_tok, *bp_par;  // [B][cap_max][k]
+  int *n_done;       // [1] sentences finished so far
+};
+
+struct ModelRows {  // per-model decoder row buffers (device arrays of pointers)
+  float *const *XS;       // [R][ldxs] = [y | c | s]
+  const float *const *Sn; // [R][dh]   s' of this step
+  const float *const *E_trg;
+  float *const *fin_states;  // optional [B][fin_cap][dh]
+  int ldxs, de, dh, s_off, n_models;
+};
+
+// XS rows of every sentence: slot 0 <- [E_trg[EOS] | 0 | s0_b], others 0;
+// beam: one hypothesis, score 0, prev token EOS (search.py:153-158).
+void launch_init_beam(const BeamState &bs, const ModelRows &mr, const float *const *S0, cudaStream_t st);
+
+struct SelectArgs {
+  int t, kk, fused, V;
+  // fused-mode inputs (single model): per (row, N-tile) partial lse + top-kk
+  const float *pmax, *psum, *cval;
+  const int *ctok;
+  int ntiles, M;
+  // full-mode inputs: logits per model [R][ldl]
+  const float *const *L;
+  int ldl;
+  const int *sl_ids, *sl_off, *sl_len;  // optional per-sentence shortlists
+  double *cand_lp;  // scratch [B*k*kk]
+  int *cand_tok;
+};
+// search.py:161-198 for one step of every sentence of the bucket.
+void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, cudaStream_t st);
+
+// hook helpers (full logits): lse over (optionally shortlisted) columns and
+// logp[r, i] = L[r, id_i] - lse_r
+void launch_logp_rows(const float *L, int ldl, int R, int V, const int *sl, int n_sl, double *logp,
+                      cudaStream_t st);
+
+}  // namespace amun

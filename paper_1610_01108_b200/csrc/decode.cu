@@ -57,9 +57,19 @@ struct Ctx {
   size_t used = 0;
   double kms[AMUN_K_CLASSES] = {0};
   int64_t kcount[AMUN_K_CLASSES] = {0};
+  float *ws = nullptr;  // split-K partials (stream-ordered, grown on demand)
+  size_t ws_floats = 0;
   explicit Ctx(cudaStream_t s) : st(s) {}
   ~Ctx() {
     for (auto e : pool) cudaEventDestroy(e);
+    if (ws) cudaFreeAsync(ws, st);
+  }
+  void ensure_ws(size_t n) {
+    if (n <= ws_floats) return;
+    if (ws) AMUN_CUDA(cudaFreeAsync(ws, st));
+    ws = nullptr;
+    AMUN_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&ws), n * sizeof(float), st));
+    ws_floats = n;
   }
   cudaEvent_t next_event() {
     if (used == pool.size()) {
@@ -111,12 +121,21 @@ GemmArgs ga(int M, int N, const float *a0, int lda0, int k0, const float *B, int
   g.k_limit = INT_MAX;
   g.a_zs = 0;
   g.b_zs = 0;
+  g.splits = 1;
+  g.kchunk = 0;
   return g;
 }
 
+// GEMM with split-K when the output has too few tiles to fill 148 SMs.
+// allow_split = false for the large-M encoder GEMMs (enough tiles already).
 template <class Epi>
-void gemm(Ctx &c, const GemmArgs &g, const Epi &e, int nz = 1) {
-  c.run(c.cls, [&] { launch_gemm_simt(g, e, nz, c.st); });
+void gemm(Ctx &c, const GemmArgs &g, const Epi &e, int nz = 1, bool allow_split = true) {
+  const int K = g.k0 + g.k1;
+  int splits = (allow_split && !Epi::kTile) ? effective_splits(K, choose_splits(g.N, K, nz)) : 1;
+  if (splits > 1) c.ensure_ws((size_t)splits * nz * g.M * g.N);
+  int n = 1;
+  c.run(c.cls, [&] { n = launch_gemm_simt(g, e, nz, splits, c.st, c.ws); });
+  c.launches += n - 1;
 }
 
 // Encoder buffers of one model for a bucket of B sentences, jmax positions.
@@ -162,7 +181,7 @@ void encode_bucket(Ctx &c, const amun_model *m, const EncBufs &e, const int *d_i
   {
     GemmArgs g = ga(B * jmax, 6 * dh, m->E_src, de, de, m->Wenc, 6 * dh);
     g.rows0 = d_ids;
-    gemm(c, g, EpiStore{e.XP, 6 * dh, m->benc, 0, 0});
+    gemm(c, g, EpiStore{e.XP, 6 * dh, m->benc, 0, 0}, 1, false);
   }
   AMUN_CUDA(cudaMemsetAsync(e.Hs, 0, sizeof(float) * 2 * B * dh, c.st));
   AMUN_CUDA(cudaMemsetAsync(e.Hann, 0, sizeof(float) * (size_t)B * jmax * 2 * dh, c.st));
@@ -176,7 +195,7 @@ void encode_bucket(Ctx &c, const amun_model *m, const EncBufs &e, const int *d_i
     b.b_zs = (long long)dh * dh;
     gemm(c, b, EpiEncB{e.XP, e.Hs, d_len, jmax, dh, t, B, e.Zs, e.Hann}, 2);
   }
-  gemm(c, ga(B * jmax, da, e.Hann, 2 * dh, 2 * dh, m->W_att_h, da), EpiStore{e.P, da, nullptr, 0, 0});
+  gemm(c, ga(B * jmax, da, e.Hann, 2 * dh, 2 * dh, m->W_att_h, da), EpiStore{e.P, da, nullptr, 0, 0}, 1, false);
   c.run(AMUN_K_ENCODER, [&] { launch_masked_mean(e.Hann, d_len, B, jmax, 2 * dh, e.Hmean, c.st); });
   gemm(c, ga(B, dh, e.Hmean, 2 * dh, 2 * dh, m->W_init, dh), EpiStore{e.S0, dh, m->b_init, 1, 0});
 }

@@ -25,7 +25,8 @@ struct GemmArgs {
   const float *B;
   int ldb;
   int n_split, k_limit;        // tiles with n0 >= n_split only use K <= k_limit
-  long long a_zs, b_zs;        // per-blockIdx.z element strides of a0 and B
+  long long a_zs, b_zs;        // per-problem element strides of a0 and B
+  int splits, kchunk;          // split-K: blockIdx.z = problem * splits + split
 };
 
 constexpr int kBM = 64, kBN = 128, kBK = 16, kThreads = 256;
@@ -45,12 +46,15 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmArgs g, Epi epi
   float *Bs = smem + 2 * kBK * (kBM + kApad);     // [2][BK][BN]
   const int tid = threadIdx.x;
   const int z = blockIdx.z;
-  const float *a0 = g.a0 + z * g.a_zs;
-  const float *Bp = g.B + z * g.b_zs;
+  const int zp = z / g.splits, zs = z % g.splits;
+  const float *a0 = g.a0 + zp * g.a_zs;
+  const float *Bp = g.B + zp * g.b_zs;
   const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
   int K = g.k0 + g.k1;
   if (n0 >= g.n_split && g.k_limit < K) K = g.k_limit;
-  const int nk = ceil_div(K, kBK);
+  const int kbeg = zs * g.kchunk;
+  const int kend = min(K, kbeg + g.kchunk);
+  const int nk = kend > kbeg ? ceil_div(kend - kbeg, kBK) : 0;
 
   // Per-thread A rows (4 rows, fixed over k): pointer bases for segment 0/1.
   const float *arow0[4];
@@ -71,18 +75,18 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmArgs g, Epi epi
 
   float ra[4], rb[8];
   auto load = [&](int kt) {
-    const int kbase = kt * kBK;
+    const int kbase = kbeg + kt * kBK;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       int k = kbase + a_kk;
       float v = 0.f;
-      if (arow_ok[i] && k < K) v = (k < g.k0) ? arow0[i][k] : arow1[i][k - g.k0];
+      if (arow_ok[i] && k < kend) v = (k < g.k0) ? arow0[i][k] : arow1[i][k - g.k0];
       ra[i] = v;
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       int k = kbase + tid / kBN + i * (kThreads / kBN);
-      rb[i] = (b_ok && k < K) ? Bp[(long long)k * g.ldb + n0 + b_n] : 0.f;
+      rb[i] = (b_ok && k < kend) ? Bp[(long long)k * g.ldb + n0 + b_n] : 0.f;
     }
   };
   auto store = [&](int buf) {
@@ -151,12 +155,71 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmArgs g, Epi epi
   }
 }
 
+// Split-K partial store: P[(problem * splits + split)][M][N].
+struct EpiPartial {
+  static constexpr bool kTile = false;
+  float *P;
+  int M, N;
+  __device__ void operator()(int m, int n, float v, int z) const { P[((long long)z * M + m) * N + n] = v; }
+};
+
+// Sum the split partials in a fixed order (deterministic), then apply the
+// elementwise epilogue.
 template <class Epi>
-inline void launch_gemm_simt(const GemmArgs &g, const Epi &epi, int nz, cudaStream_t st) {
-  if (g.M <= 0 || g.N <= 0) return;
-  dim3 grid(ceil_div(g.N, kBN), ceil_div(g.M, kBM), nz);
-  gemm_simt_kernel<Epi><<<grid, kThreads, 0, st>>>(g, epi);
-  AMUN_CHECK_LAUNCH();
+__global__ void splitk_reduce_kernel(const float *P, int M, int N, int splits, long long total, Epi epi) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const long long mn = (long long)M * N;
+  const int p = (int)(i / mn);
+  const long long rem = i - p * mn;
+  const int m = (int)(rem / N), n = (int)(rem % N);
+  const float *src = P + (long long)p * splits * mn + rem;
+  float v = 0.f;
+  for (int s = 0; s < splits; ++s) v += src[s * mn];
+  epi(m, n, v, p);
+}
+
+// Split count depends only on (N, K, problems) — never on M — so a row's
+// result is independent of how many rows share the launch (batch
+// invariance: identical output for any bucket size or GPU count).
+inline int choose_splits(int N, int K, int nz) {
+  const int tiles_n = ceil_div(N, kBN) * nz;
+  int s = ceil_div(128, tiles_n);
+  s = std::min(s, std::max(1, K / 128));
+  return std::max(1, s);
+}
+
+inline int effective_splits(int K, int splits) {
+  if (splits <= 1) return 1;
+  int kchunk = ceil_div(ceil_div(K, splits), kBK) * kBK;
+  return ceil_div(K, kchunk);
+}
+
+// Returns the number of kernel launches issued.  `splits` > 1 needs a
+// workspace of effective_splits(K, splits) * nz * M * N floats.
+template <class Epi>
+inline int launch_gemm_simt(GemmArgs g, const Epi &epi, int nz, int splits, cudaStream_t st, float *ws) {
+  if (g.M <= 0 || g.N <= 0) return 0;
+  const int Kfull = g.k0 + g.k1;
+  if (Epi::kTile) splits = 1;
+  int kchunk = splits > 1 ? ceil_div(ceil_div(Kfull, splits), kBK) * kBK : Kfull + kBK;
+  if (splits > 1) splits = ceil_div(Kfull, kchunk);
+  g.splits = splits;
+  g.kchunk = kchunk;
+  dim3 grid(ceil_div(g.N, kBN), ceil_div(g.M, kBM), nz * splits);
+  if (splits == 1) {
+    gemm_simt_kernel<Epi><<<grid, kThreads, 0, st>>>(g, epi);
+    AMUN_CHECK_LAUNCH();
+    return 1;
+  }
+  if constexpr (!Epi::kTile) {
+    gemm_simt_kernel<EpiPartial><<<grid, kThreads, 0, st>>>(g, EpiPartial{ws, g.M, g.N});
+    AMUN_CHECK_LAUNCH();
+    long long total = (long long)nz * g.M * g.N;
+    splitk_reduce_kernel<Epi><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(ws, g.M, g.N, splits, total, epi);
+    AMUN_CHECK_LAUNCH();
+  }
+  return 2;
 }
 
 // ------------------------------------------------------------------ epilogues

@@ -136,6 +136,85 @@ __device__ __forceinline__ double combine_models(double l0, const double *lm, in
   return l0 + acc / (double)n;
 }
 
+constexpr int kNoTok = 0x7fffffff;
+constexpr int kLaneList = 16;
+
+// A lane's sorted (best-first) list of up to kLaneList candidate keys.
+struct LaneList {
+  double v[kLaneList];
+  int t[kLaneList], p[kLaneList];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int i = 0; i < kLaneList; ++i) {
+      v[i] = -INFINITY;
+      t[i] = kNoTok;
+      p[i] = kNoTok;
+    }
+  }
+  // insertion by compare-exchange down the list (registers only)
+  __device__ __forceinline__ void push(Key c, int kk) {
+#pragma unroll
+    for (int i = 0; i < kLaneList; ++i) {
+      if (i < kk && key_better(c.v, c.tok, c.par, v[i], t[i], p[i])) {
+        double tv = v[i];
+        int tt = t[i], tp = p[i];
+        v[i] = c.v;
+        t[i] = c.tok;
+        p[i] = c.par;
+        c = Key{tv, tt, tp};
+      }
+    }
+  }
+  __device__ __forceinline__ Key get(int h) const {
+    Key k{-INFINITY, kNoTok, kNoTok};
+#pragma unroll
+    for (int i = 0; i < kLaneList; ++i)
+      if (i == h) k = Key{v[i], t[i], p[i]};
+    return k;
+  }
+};
+
+// Warp-cooperative exact top-kk of candidates get(0..n-1) (entries with
+// tok < 0 are skipped) in (value desc, tok asc, par asc) order; out(j, key)
+// is called by every lane with the warp-uniform j-th key (tok == kNoTok when
+// fewer than kk candidates exist).  (tok, par) pairs must be unique.
+template <class Get, class Out>
+__device__ __forceinline__ void warp_topk(int n, int kk, Get get, Out out) {
+  const int lane = threadIdx.x % 32;
+  if (kk <= kLaneList) {
+    LaneList L;
+    L.init();
+#pragma unroll 4
+    for (int e = lane; e < n; e += 32) {
+      Key c = get(e);
+      if (c.tok >= 0) L.push(c, kk);
+    }
+    int h = 0;
+    for (int j = 0; j < kk; ++j) {
+      Key mine = L.get(h);
+      Key best = warp_best(mine);
+      if (best.tok != kNoTok && mine.tok == best.tok && mine.par == best.par) ++h;
+      out(j, best);
+    }
+    return;
+  }
+  // general path (kk > 16): kk passes of "best key strictly below the last"
+  Key last{INFINITY, -1, -1};
+  for (int j = 0; j < kk; ++j) {
+    Key best{-INFINITY, kNoTok, kNoTok};
+    for (int e = lane; e < n; e += 32) {
+      Key c = get(e);
+      if (c.tok < 0) continue;
+      if (key_better(last.v, last.tok, last.par, c.v, c.tok, c.par) &&
+          key_better(c.v, c.tok, c.par, best.v, best.tok, best.par))
+        best = c;
+    }
+    best = warp_best(best);
+    out(j, best);
+    last = best;
+  }
+}
+
 __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs, ModelRows mr) {
   extern __shared__ unsigned char smraw[];
   const int k = bs.k;
@@ -173,26 +252,16 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       const int n = sa.ntiles * kk;
       const float *cv = sa.cval + (long long)r * n;
       const int *ct = sa.ctok + (long long)r * n;
-      double lv = INFINITY;
-      int lt = -1;
-      for (int p = 0; p < kk; ++p) {
-        Key best{-INFINITY, 0x7fffffff, 0};
-        for (int e = lane; e < n; e += 32) {
-          int tok = ct[e];
-          if (tok < 0) continue;
-          double x = cv[e];
-          bool below = (x < lv) || (x == lv && tok > lt);
-          if (below && key_better(x, tok, 0, best.v, best.tok, 0)) best = Key{x, tok, 0};
-        }
-        best = warp_best(best);
-        if (lane == 0) {
-          bool none = best.tok == 0x7fffffff;
-          out_lp[p] = none ? -INFINITY : best.v - lse;
-          out_tok[p] = none ? -1 : best.tok;
-        }
-        lv = best.v;
-        lt = best.tok;
-      }
+      // ordering by raw logit == ordering by logit - lse within a row
+      warp_topk(
+          n, kk, [&](int e) { return Key{(double)cv[e], ct[e], 0}; },
+          [&](int j, const Key &bk) {
+            if (lane == 0) {
+              bool none = bk.tok == kNoTok;
+              out_lp[j] = none ? -INFINITY : bk.v - lse;
+              out_tok[j] = none ? -1 : bk.tok;
+            }
+          });
     } else {
       const int *ids = sa.sl_ids ? sa.sl_ids + sa.sl_off[b] : nullptr;
       const int ncols = sa.sl_ids ? sa.sl_len[b] : sa.V;
@@ -207,27 +276,21 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         s = warp_sum_d(s);
         lse[m] = (double)mx + log(s);
       }
-      double lv = INFINITY;
-      int lt = -1;
-      for (int p = 0; p < kk; ++p) {
-        Key best{-INFINITY, 0x7fffffff, 0};
-        for (int c = lane; c < ncols; c += 32) {
-          int g = ids ? ids[c] : c;
-          double lm[kMaxModels];
-          for (int m = 0; m < n_models; ++m) lm[m] = (double)sa.L[m][(long long)r * sa.ldl + g] - lse[m];
-          double x = combine_models(lm[0], lm, n_models);
-          bool below = (x < lv) || (x == lv && g > lt);
-          if (below && key_better(x, g, 0, best.v, best.tok, 0)) best = Key{x, g, 0};
-        }
-        best = warp_best(best);
-        if (lane == 0) {
-          bool none = best.tok == 0x7fffffff;
-          out_lp[p] = none ? -INFINITY : best.v;
-          out_tok[p] = none ? -1 : best.tok;
-        }
-        lv = best.v;
-        lt = best.tok;
-      }
+      warp_topk(
+          ncols, kk,
+          [&](int c) {
+            int g = ids ? ids[c] : c;
+            double lm[kMaxModels];
+            for (int m = 0; m < n_models; ++m) lm[m] = (double)sa.L[m][(long long)r * sa.ldl + g] - lse[m];
+            return Key{combine_models(lm[0], lm, n_models), g, 0};
+          },
+          [&](int j, const Key &bk) {
+            if (lane == 0) {
+              bool none = bk.tok == kNoTok;
+              out_lp[j] = none ? -INFINITY : bk.v;
+              out_tok[j] = none ? -1 : bk.tok;
+            }
+          });
     }
   }
   __syncthreads();
@@ -238,31 +301,22 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     const int n = na * kk;
     const double *clp = sa.cand_lp + (long long)b * k * kk;
     const int *ctk = sa.cand_tok + (long long)b * k * kk;
-    double lv = INFINITY;
-    int lt = -1, lp_ = -1;
     int nch = 0;
-    for (int p = 0; p < k; ++p) {
-      Key best{-INFINITY, 0x7fffffff, 0x7fffffff};
-      for (int e = lane; e < n; e += 32) {
-        int tok = ctk[e];
-        if (tok < 0) continue;
-        int par = e / kk;
-        double x = bs.score[b * k + par] + clp[e];
-        bool below = key_better(lv, lt, lp_, x, tok, par);
-        if (below && key_better(x, tok, par, best.v, best.tok, best.par)) best = Key{x, tok, par};
-      }
-      best = warp_best(best);
-      if (best.tok == 0x7fffffff) break;
-      if (lane == 0) {
-        ch_v[p] = best.v;
-        ch_tok[p] = best.tok;
-        ch_par[p] = best.par;
-      }
-      nch = p + 1;
-      lv = best.v;
-      lt = best.tok;
-      lp_ = best.par;
-    }
+    warp_topk(
+        n, k,
+        [&](int e) {
+          int par = e / kk;
+          return Key{bs.score[b * k + par] + clp[e], ctk[e], par};
+        },
+        [&](int j, const Key &bk) {
+          if (bk.tok == kNoTok) return;
+          if (lane == 0) {
+            ch_v[j] = bk.v;
+            ch_tok[j] = bk.tok;
+            ch_par[j] = bk.par;
+          }
+          nch = j + 1;
+        });
     if (lane == 0) s_nch = nch;
   }
   __syncthreads();

@@ -17,6 +17,11 @@ from pathlib import Path
 
 import numpy as np
 import pytest
+from threadpoolctl import threadpool_limits
+
+# numpy may already have been imported (by a pytest plugin) before the env
+# vars above took effect: pin BLAS to one thread at runtime as well.
+_BLAS_LIMIT = threadpool_limits(limits=1)
 
 REPO = Path(__file__).resolve().parent.parent
 GOLDEN = REPO / "tests" / "golden"

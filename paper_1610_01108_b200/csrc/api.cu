@@ -151,6 +151,23 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
   }
   m->W_logit = upload(m, cp(T_W_LOGIT, (size_t)de * V));
   m->b_logit = upload(m, cp(T_B_LOGIT, V));
+  if (de % 4 == 0) {  // TMA needs 16-byte row pitch: logit rows [V, de] hi/lo
+    std::vector<float> hi((size_t)V * de), lo((size_t)V * de);
+    const float *W = t[T_W_LOGIT];
+    for (int k = 0; k < de; ++k)
+      for (int v = 0; v < V; ++v) {
+        float x = W[(size_t)k * V + v];
+        uint32_t u;
+        std::memcpy(&u, &x, 4);
+        u &= 0xFFFFE000u;
+        float h;
+        std::memcpy(&h, &u, 4);
+        hi[(size_t)v * de + k] = h;
+        lo[(size_t)v * de + k] = x - h;
+      }
+    m->Wl_hi = upload(m, hi);
+    m->Wl_lo = upload(m, lo);
+  }
   AMUN_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
   *out = m;
   m = nullptr;

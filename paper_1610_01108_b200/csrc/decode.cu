@@ -13,6 +13,7 @@
 #include "decode.cuh"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
+#include "logits_tc.cuh"
 
 namespace amun {
 
@@ -145,6 +146,7 @@ struct EncBufs {
 // Decoder row buffers of one model for R hypothesis rows.
 struct DecBufs {
   float *XS, *Sn, *Q, *Z, *RH, *XH, *T, *L;
+  float *T_hi = nullptr, *T_lo = nullptr;  // 3xTF32 split of t (tensor-core logits)
 };
 
 void carve_enc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
@@ -169,6 +171,10 @@ void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, bool full_log
   d.XH = cv.take<float>((size_t)R * dh);
   d.T = cv.take<float>((size_t)R * de);
   d.L = full_logits ? cv.take<float>((size_t)R * m->d.v_trg) : nullptr;
+  if (!full_logits && m->Wl_hi) {
+    d.T_hi = cv.take<float>((size_t)R * de);
+    d.T_lo = cv.take<float>((size_t)R * de);
+  }
 }
 
 // nnet.py:110-130 for B padded sentences: input projection (embedding
@@ -207,6 +213,7 @@ struct LogitOut {
   int kk, ntiles;
   float *pmax, *psum, *cval;
   int *ctok;
+  const LogitTcMaps *tc = nullptr;  // tensor-core path when set
 };
 
 void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
@@ -233,9 +240,19 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     g.a1 = d.Sn;
     g.lda1 = dh;
     g.k1 = dh;
-    gemm(c, g, EpiStore{d.T, de, m->b_out, 1, 0});
+    EpiStore e{lo.tc ? nullptr : d.T, de, m->b_out, 1, 0};
+    if (lo.tc) {
+      e.hi = d.T_hi;
+      e.lo = d.T_lo;
+    }
+    gemm(c, g, e);
   }
   c.cls = AMUN_K_LOGIT;
+  if (lo.tc) {
+    LogitTcArgs ta{R, V, de, m->b_logit, lo.kk, lo.ntiles, lo.pmax, lo.psum, lo.cval, lo.ctok};
+    c.run(AMUN_K_LOGIT, [&] { launch_logits_tc(*lo.tc, ta, c.st); });
+    return;
+  }
   GemmArgs g = ga(R, V, d.T, de, de, m->W_logit, V);
   if (lo.fused)
     gemm(c, g, EpiLogitTopK{m->b_logit, lo.kk, lo.ntiles, lo.pmax, lo.psum, lo.cval, lo.ctok});
@@ -305,6 +322,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
 
   const int Bmax_opt = o.max_batch > 0 ? o.max_batch : 64;
   const bool fused = n_models == 1 && !sl_ids && k <= kMaxRowCand && !o.force_full_logits;
+  const char *no_tc = getenv("AMUN_NO_TC");
+  const bool use_tc = fused && m0->Wl_hi && !(no_tc && no_tc[0] == '1');
   const int kk = std::min(k, V);
   const int ntiles = ceil_div(V, kBN);
 
@@ -356,6 +375,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     for (int m = 0; m < n_models; ++m) {
       carve_enc(cv, eb[m], ms[m], Bmax, jmax_all);
       carve_dec(cv, db[m], ms[m], Rmax, !fused);
+      if (!use_tc) db[m].T_hi = db[m].T_lo = nullptr;
       fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * dh) : nullptr;
     }
     d_ids = cv.take<int>((size_t)Bmax * jmax_all);
@@ -394,6 +414,12 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   }
   Ctx c(m0->stream);
   c.prof = o.profile != 0;
+  LogitTcMaps tc_maps{};
+  if (use_tc) {
+    static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
+    if (logits_tc_tile_n() != kBN) throw Error(AMUN_ERR_UNSUPPORTED, "logit tile width mismatch");
+    tc_maps = make_logit_maps(db[0].T_hi, db[0].T_lo, Rmax, m0->d.d_emb, m0->d.d_emb, m0->Wl_hi, m0->Wl_lo, V);
+  }
   cudaStream_t st = c.st;
   {
     std::vector<const void *> hx(n_models), hs(n_models), he(n_models), h0(n_models), hl(n_models), hf(n_models);
@@ -460,6 +486,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     ModelRows mr{p_XS, p_Sn, p_E, o.want_states ? p_fin : nullptr, xs, de, dh, de + 2 * dh, n_models};
     c.run(AMUN_K_SELECT, [&] { launch_init_beam(bs, mr, p_S0, st); });
     LogitOut lo{fused, kk, ntiles, pmax, psum, cval, ctok};
+    if (use_tc) lo.tc = &tc_maps;
     SelectArgs sa{};
     sa.kk = kk;
     sa.fused = fused;

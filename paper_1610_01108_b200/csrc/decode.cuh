@@ -20,6 +20,9 @@ struct amun_model {
   float *Uh_dec = nullptr;                 // [dh, dh]
   float *Wout = nullptr, *b_out = nullptr; // [de+3dh, de], [de]
   float *W_logit = nullptr, *b_logit = nullptr;  // [de, V], [V]
+  // tensor-core copies of the output projection: logit rows [V, de] split
+  // into tf32-exact hi and residual lo (3xTF32); null when de % 4 != 0
+  float *Wl_hi = nullptr, *Wl_lo = nullptr;
   int64_t bytes = 0;
   std::vector<void *> allocs;
   cudaStream_t stream = nullptr;

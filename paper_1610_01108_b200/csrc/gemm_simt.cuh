@@ -232,10 +232,16 @@ struct EpiStore {
   const float *bias;
   int act;
   long long c_zs;
+  float *hi = nullptr, *lo = nullptr;  // optional 3xTF32 split copies (ldc, no z)
   __device__ void operator()(int m, int n, float v, int z) const {
     if (bias) v += bias[n];
     if (act == 1) v = tanhf(v);
-    C[z * c_zs + (long long)m * ldc + n] = v;
+    if (C) C[z * c_zs + (long long)m * ldc + n] = v;
+    if (hi) {
+      const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      hi[(long long)m * ldc + n] = h;
+      lo[(long long)m * ldc + n] = v - h;
+    }
   }
 };
 

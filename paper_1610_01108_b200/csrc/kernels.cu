@@ -137,15 +137,15 @@ __device__ __forceinline__ double combine_models(double l0, const double *lm, in
 }
 
 constexpr int kNoTok = 0x7fffffff;
-constexpr int kLaneList = 16;
 
-// A lane's sorted (best-first) list of up to kLaneList candidate keys.
+// A lane's sorted (best-first) list of up to KMAX candidate keys.
+template <int KMAX>
 struct LaneList {
-  double v[kLaneList];
-  int t[kLaneList], p[kLaneList];
+  double v[KMAX];
+  int t[KMAX], p[KMAX];
   __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int i = 0; i < kLaneList; ++i) {
+    for (int i = 0; i < KMAX; ++i) {
       v[i] = -INFINITY;
       t[i] = kNoTok;
       p[i] = kNoTok;
@@ -154,7 +154,7 @@ struct LaneList {
   // insertion by compare-exchange down the list (registers only)
   __device__ __forceinline__ void push(Key c, int kk) {
 #pragma unroll
-    for (int i = 0; i < kLaneList; ++i) {
+    for (int i = 0; i < KMAX; ++i) {
       if (i < kk && key_better(c.v, c.tok, c.par, v[i], t[i], p[i])) {
         double tv = v[i];
         int tt = t[i], tp = p[i];
@@ -168,7 +168,7 @@ struct LaneList {
   __device__ __forceinline__ Key get(int h) const {
     Key k{-INFINITY, kNoTok, kNoTok};
 #pragma unroll
-    for (int i = 0; i < kLaneList; ++i)
+    for (int i = 0; i < KMAX; ++i)
       if (i == h) k = Key{v[i], t[i], p[i]};
     return k;
   }
@@ -178,13 +178,14 @@ struct LaneList {
 // tok < 0 are skipped) in (value desc, tok asc, par asc) order; out(j, key)
 // is called by every lane with the warp-uniform j-th key (tok == kNoTok when
 // fewer than kk candidates exist).  (tok, par) pairs must be unique.
-template <class Get, class Out>
+// KMAX > 0: per-lane register lists (kk <= KMAX) then a kk-round warp merge;
+// KMAX == 0: general kk-pass scan (any kk).
+template <int KMAX, class Get, class Out>
 __device__ __forceinline__ void warp_topk(int n, int kk, Get get, Out out) {
   const int lane = threadIdx.x % 32;
-  if (kk <= kLaneList) {
-    LaneList L;
+  if constexpr (KMAX > 0) {
+    LaneList<KMAX> L;
     L.init();
-#pragma unroll 4
     for (int e = lane; e < n; e += 32) {
       Key c = get(e);
       if (c.tok >= 0) L.push(c, kk);
@@ -196,25 +197,25 @@ __device__ __forceinline__ void warp_topk(int n, int kk, Get get, Out out) {
       if (best.tok != kNoTok && mine.tok == best.tok && mine.par == best.par) ++h;
       out(j, best);
     }
-    return;
-  }
-  // general path (kk > 16): kk passes of "best key strictly below the last"
-  Key last{INFINITY, -1, -1};
-  for (int j = 0; j < kk; ++j) {
-    Key best{-INFINITY, kNoTok, kNoTok};
-    for (int e = lane; e < n; e += 32) {
-      Key c = get(e);
-      if (c.tok < 0) continue;
-      if (key_better(last.v, last.tok, last.par, c.v, c.tok, c.par) &&
-          key_better(c.v, c.tok, c.par, best.v, best.tok, best.par))
-        best = c;
+  } else {
+    Key last{INFINITY, -1, -1};
+    for (int j = 0; j < kk; ++j) {
+      Key best{-INFINITY, kNoTok, kNoTok};
+      for (int e = lane; e < n; e += 32) {
+        Key c = get(e);
+        if (c.tok < 0) continue;
+        if (key_better(last.v, last.tok, last.par, c.v, c.tok, c.par) &&
+            key_better(c.v, c.tok, c.par, best.v, best.tok, best.par))
+          best = c;
+      }
+      best = warp_best(best);
+      out(j, best);
+      last = best;
     }
-    best = warp_best(best);
-    out(j, best);
-    last = best;
   }
 }
 
+template <int KMAX, bool FUSED>
 __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs, ModelRows mr) {
   extern __shared__ unsigned char smraw[];
   const int k = bs.k;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     const int r = b * k + i;
     double *out_lp = sa.cand_lp + ((long long)b * k + i) * kk;
     int *out_tok = sa.cand_tok + ((long long)b * k + i) * kk;
-    if (sa.fused) {
+    if constexpr (FUSED) {
       float mx = -INFINITY;
       for (int tt = lane; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, sa.pmax[(long long)tt * sa.M + r]);
       mx = warp_max(mx);
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       const float *cv = sa.cval + (long long)r * n;
       const int *ct = sa.ctok + (long long)r * n;
       // ordering by raw logit == ordering by logit - lse within a row
-      warp_topk(
+      warp_topk<KMAX>(
           n, kk, [&](int e) { return Key{(double)cv[e], ct[e], 0}; },
           [&](int j, const Key &bk) {
             if (lane == 0) {
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         s = warp_sum_d(s);
         lse[m] = (double)mx + log(s);
       }
-      warp_topk(
+      warp_topk<KMAX>(
           ncols, kk,
           [&](int c) {
             int g = ids ? ids[c] : c;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     const double *clp = sa.cand_lp + (long long)b * k * kk;
     const int *ctk = sa.cand_tok + (long long)b * k * kk;
     int nch = 0;
-    warp_topk(
+    warp_topk<KMAX>(
         n, k,
         [&](int e) {
           int par = e / kk;
@@ -394,12 +395,29 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   }
 }
 
+template <int KMAX, bool FUSED>
+static void launch_select_t(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, size_t smem,
+                            cudaStream_t st) {
+  auto kern = select_kernel<KMAX, FUSED>;
+  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<bs.B, 256, smem, st>>>(sa, bs, mr);
+  AMUN_CHECK_LAUNCH();
+}
+
 void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, cudaStream_t st) {
   if (mr.n_models > kMaxModels) throw Error(4, "at most 8 ensemble members are supported on the device path");
   size_t smem = (size_t)bs.k * (sizeof(double) + 4 * sizeof(int));
-  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  select_kernel<<<bs.B, 256, smem, st>>>(sa, bs, mr);
-  AMUN_CHECK_LAUNCH();
+  const int need = std::max(bs.k, sa.kk);  // list sizes used in phases 1 and 2
+  if (sa.fused) {
+    if (need <= 1) launch_select_t<1, true>(sa, bs, mr, smem, st);
+    else if (need <= 4) launch_select_t<4, true>(sa, bs, mr, smem, st);
+    else if (need <= 8) launch_select_t<8, true>(sa, bs, mr, smem, st);
+    else launch_select_t<16, true>(sa, bs, mr, smem, st);
+  } else {
+    if (need <= 8) launch_select_t<8, false>(sa, bs, mr, smem, st);
+    else if (need <= 16) launch_select_t<16, false>(sa, bs, mr, smem, st);
+    else launch_select_t<0, false>(sa, bs, mr, smem, st);
+  }
 }
 
 // ================================================================ hook logp

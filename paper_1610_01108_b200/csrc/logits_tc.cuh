@@ -1,0 +1,30 @@
+// Tensor-core (tcgen05, 3xTF32) logit projection with fused log-softmax
+// partials and per-row top-k; see logits_tc.cu.
+#pragma once
+
+#include <cuda.h>
+
+namespace amun {
+
+struct LogitTcArgs {
+  int M, N, K;         // rows (hypotheses), vocabulary, d_emb
+  const float *bias;   // b_logit [N]
+  int kk, ntiles;      // candidates kept per (row, tile); ceil(N / tile_n)
+  float *pmax, *psum;  // [ntiles][M]
+  float *cval;         // [M][ntiles][kk]
+  int *ctok;
+};
+
+struct LogitTcMaps {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;
+};
+
+int logits_tc_tile_n();
+CUtensorMap make_tma_2d_f32(const float *ptr, int inner, int outer, int row_stride_elems, int box_inner,
+                            int box_outer);
+// t_hi/t_lo: [R, ldt] (first K columns used); w_hi/w_lo: [V, K] (logit rows)
+LogitTcMaps make_logit_maps(const float *t_hi, const float *t_lo, int R, int K, int ldt, const float *w_hi,
+                            const float *w_lo, int V);
+void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st);
+
+}  // namespace amun

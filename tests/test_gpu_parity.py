@@ -213,6 +213,35 @@ def test_batch_composition_invariance(gpu, full):
         assert a.hyps(i)[0][:2] == b.hyps(i)[0][:2]
 
 
+def test_tensor_core_logits_match_cuda_core_path(gpu, full, monkeypatch):
+    """tcgen05 3xTF32 logit kernel vs the FP32 CUDA-core kernel on the same
+    decode: identical tokens, scores equal to FP32 rounding."""
+    s = golden_full()["sets"]["cfg2_strat64"]
+    sub = dict(s, src=s["src"][:32])
+    a = _decode_set(full, sub)
+    monkeypatch.setenv("AMUN_NO_TC", "1")
+    b = _decode_set(full, sub)
+    for i in range(32):
+        ha, hb = a.hyps(i)[0], b.hyps(i)[0]
+        assert ha[0] == hb[0], i
+        assert abs(ha[1] - hb[1]) <= 1e-5 * abs(hb[1]), (i, ha[1], hb[1])
+
+
+def test_tensor_core_logits_tiny_shapes(gpu, monkeypatch):
+    """d_emb % 4 == 0 tiny models take the tensor-core path too (one
+    partially out-of-bounds 128-wide vocabulary tile, K = 4 or 8)."""
+    for seed, v, d in ((1, 5, 4), (2, 7, 8), (3, 200, 8), (4, 300, 12)):
+        m = tiny_model(seed, 9, v, d)
+        opts = DecodeOptions(beam_size=3, n_best=3)
+        a = beam_search([m], [2, 3, 4], opts)
+        monkeypatch.setenv("AMUN_NO_TC", "1")
+        b = beam_search([m], [2, 3, 4], opts)
+        monkeypatch.delenv("AMUN_NO_TC")
+        assert [h.tokens for h in a] == [h.tokens for h in b]
+        for x, y in zip(a, b):
+            assert abs(x.score - y.score) <= 1e-5 * max(1.0, abs(y.score))
+
+
 def test_fused_and_full_logit_paths_agree(gpu, full):
     s = golden_full()["sets"]["cfg1"]
     sub = dict(s, src=s["src"][:6])

@@ -27,26 +27,26 @@ namespace {
 
 constexpr int kBK = 16;  // fp32 elements per 64-byte swizzled row
 
-template <int KMAX>
+// Register-resident sorted top-KK list of one row (KK is a compile-time
+// size >= kk so every index is static and nothing spills to local memory).
+template <int KK>
 struct RowTop {
-  float v[KMAX];
-  int t[KMAX];
-  float worst;
+  float v[KK];
+  int t[KK];
   __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int i = 0; i < KMAX; ++i) {
+    for (int i = 0; i < KK; ++i) {
       v[i] = -INFINITY;
       t[i] = -1;
     }
-    worst = -INFINITY;
   }
-  // columns arrive in ascending token order, so an equal value loses the
-  // tie (token asc) and strict > is the exact reference order.
-  __device__ __forceinline__ void push(float x, int n, int kk) {
-    if (!(x > worst)) return;
+  __device__ __forceinline__ float worst() const { return v[KK - 1]; }
+  // caller guarantees x > worst().  Columns arrive in ascending token order,
+  // so an equal value loses the tie (token asc): strict > is exact.
+  __device__ __forceinline__ void insert(float x, int n) {
 #pragma unroll
-    for (int i = 0; i < KMAX; ++i) {
-      if (i < kk && x > v[i]) {
+    for (int i = 0; i < KK; ++i) {
+      if (x > v[i]) {
         float tv = v[i];
         int tt = t[i];
         v[i] = x;
@@ -55,14 +55,11 @@ struct RowTop {
         n = tt;
       }
     }
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i == kk - 1) worst = v[i];
   }
 };
 
-template <int BN, int MB, int STAGES, int KMAX>
-__global__ void __launch_bounds__(192, 1)
+template <int BN, int MB, int STAGES, int KK, int CS>
+__global__ void __launch_bounds__(64 + 128 * MB, 1)
     logits_tc_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                      const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
                      LogitTcArgs a) {
@@ -78,19 +75,24 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 1;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
+  float *sbias = reinterpret_cast<float *>(tempty + 2);  // [BN] bias tile, -inf past the vocabulary
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n0 = blockIdx.x * BN;
+  // CS CTAs of a cluster work on adjacent vocabulary tiles and share the
+  // activation tiles: each CTA TMA-multicasts 1/CS of them to the cluster.
+  const uint32_t crank = CS > 1 ? tc::cluster_rank() : 0;
+  constexpr uint16_t kAll = (uint16_t)((1u << CS) - 1);
   const int nk = (a.K + kBK - 1) / kBK;
   const int nchunks = (a.M + MB * 128 - 1) / (MB * 128);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], CS);  // released by every CTA of the cluster
     }
     tc::mbar_init(tfull, 1);
-    tc::mbar_init(tempty, 4);
+    tc::mbar_init(tempty, 4 * MB);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tA_hi);
     tc::tma_prefetch(&tA_lo);
@@ -100,6 +102,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tslot);
   tc::tc_fence_before();
   __syncthreads();
+  if constexpr (CS > 1) tc::cluster_sync();  // peers' barriers initialised before any multicast
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
 
@@ -111,17 +114,28 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          const bool la = !(a.debug_flags & 1), lb = !(a.debug_flags & 2);
+          tc::mbar_arrive_expect_tx(&full[s], (la ? 2 * A_BYTES : 0) + (lb ? 2 * B_BYTES : 0));
           uint8_t *st = smem + s * STAGE_BYTES;
           const int kx = kb * kBK;
+          if (la) {
 #pragma unroll
-          for (int mb = 0; mb < MB; ++mb) {
-            const int row = (ch * MB + mb) * 128;
-            tc::tma_load_2d(st + mb * 128 * kBK * 4, &tA_hi, &full[s], kx, row);
-            tc::tma_load_2d(st + A_BYTES + mb * 128 * kBK * 4, &tA_lo, &full[s], kx, row);
+            for (int j = 0; j < 2 * MB; ++j) {
+              if (j % CS != (int)crank) continue;
+              const int mb = j >> 1;
+              const int row = (ch * MB + mb) * 128;
+              uint8_t *dst = st + (j & 1) * A_BYTES + mb * 128 * kBK * 4;
+              const CUtensorMap *map = (j & 1) ? &tA_lo : &tA_hi;
+              if constexpr (CS > 1)
+                tc::tma_load_2d_mc(dst, map, &full[s], kx, row, kAll);
+              else
+                tc::tma_load_2d(dst, map, &full[s], kx, row);
+            }
           }
-          tc::tma_load_2d(st + 2 * A_BYTES, &tB_hi, &full[s], kx, n0);
-          tc::tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tB_lo, &full[s], kx, n0);
+          if (lb) {
+            tc::tma_load_2d(st + 2 * A_BYTES, &tB_hi, &full[s], kx, n0);
+            tc::tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tB_lo, &full[s], kx, n0);
+          }
         }
       }
     }
@@ -141,7 +155,7 @@ __global__ void __launch_bounds__(192, 1)
           tc::tc_fence_after();
           const uint32_t base = tc::smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
-          for (int k2 = 0; k2 < kBK / 8; ++k2) {
+          for (int k2 = 0; k2 < ((a.debug_flags & 4) ? 0 : kBK / 8); ++k2) {
             const uint32_t koff = k2 * 32;  // 8 tf32 = 32 bytes along K
             const uint64_t bh = tc::desc_kmajor_sw64(base + 2 * A_BYTES + koff);
             const uint64_t bl = tc::desc_kmajor_sw64(base + 2 * A_BYTES + B_BYTES + koff);
@@ -155,56 +169,63 @@ __global__ void __launch_bounds__(192, 1)
               tc::mma_tf32(d, al, bh, idesc, 1);               // lo * hi
             }
           }
-          tc::mma_commit(&empty[s]);  // smem stage free once these MMAs drain
+          if constexpr (CS > 1)
+            tc::mma_commit_mc(&empty[s], kAll);  // slot free in every CTA's ring
+          else
+            tc::mma_commit(&empty[s]);  // smem stage free once these MMAs drain
         }
         tc::mma_commit(tfull);  // accumulators of this chunk complete
       }
     }
   } else {
-    // ---------------- epilogue: warps 2..5, thread = one row of the tile
+    // ---------------- epilogue: 4*MB warps; warp group mb drains M-block mb,
+    // thread = one row (TMEM lane) of the tile
     const int lg = warp & 3;  // TMEM lane quarter this warp may access
+    const int mb = (warp - 2) >> 2;
     const int nt = blockIdx.x;
+    for (int c = threadIdx.x - 64; c < BN; c += 128 * MB)
+      sbias[c] = (n0 + c < a.N) ? __ldg(a.bias + n0 + c) : -INFINITY;
+    asm volatile("bar.sync 1, %0;" ::"n"(128 * MB) : "memory");  // epilogue warps only
     for (int ch = 0; ch < nchunks; ++ch) {
       tc::mbar_wait(tfull, ch & 1);
       tc::tc_fence_after();
-#pragma unroll 1
-      for (int mb = 0; mb < MB; ++mb) {
+      if (!(a.debug_flags & 8)) {
         const int m = (ch * MB + mb) * 128 + lg * 32 + lane;
         const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + mb * BN;
-        RowTop<KMAX> top;
+        RowTop<KK> top;
         top.init();
         float mx = -INFINITY;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float v[32];
           tc::tmem_ld_32x32(tb + c0, v);
+          float cm = -INFINITY;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const int n = n0 + c0 + i;
-            if (n < a.N) {
-              const float x = v[i] + __ldg(a.bias + n);
-              mx = fmaxf(mx, x);
-              top.push(x, n, a.kk);
-            }
+            v[i] += sbias[c0 + i];
+            cm = fmaxf(cm, v[i]);
+          }
+          mx = fmaxf(mx, cm);
+          if (cm > top.worst() && !(a.debug_flags & 16)) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (v[i] > top.worst()) top.insert(v[i], n0 + c0 + i);
           }
         }
         float se = 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = 0; c0 < ((a.debug_flags & 32) ? 0 : BN); c0 += 32) {
           float v[32];
           tc::tmem_ld_32x32(tb + c0, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int n = n0 + c0 + i;
-            if (n < a.N) se += expf(v[i] + __ldg(a.bias + n) - mx);
-          }
+          for (int i = 0; i < 32; ++i) se += expf(v[i] + sbias[c0 + i] - mx);
         }
-        if (m < a.M) {
+        if (m < a.M && nt < a.ntiles && !(a.debug_flags & 64)) {
           a.pmax[(long long)nt * a.M + m] = mx;
           a.psum[(long long)nt * a.M + m] = se;
           const long long base = ((long long)m * a.ntiles + nt) * a.kk;
 #pragma unroll
-          for (int i = 0; i < KMAX; ++i)
+          for (int i = 0; i < KK; ++i)
             if (i < a.kk) {
               a.cval[base + i] = top.v[i];
               a.ctok[base + i] = top.t[i];
@@ -217,6 +238,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   __syncthreads();
+  if constexpr (CS > 1) tc::cluster_sync();  // no CTA leaves while peers may still signal it
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc<TMEM_COLS>(tmem);
@@ -239,13 +261,13 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-constexpr int kTcBN = 128, kTcMB = 3, kTcStages = 3;
+constexpr int kTcBN = 128, kTcMB = 3, kTcStages = 3, kTcCluster = 2;
 
-template <int KMAX>
+template <int KK>
 void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
-  auto kern = logits_tc_kernel<kTcBN, kTcMB, kTcStages, KMAX>;
+  auto kern = logits_tc_kernel<kTcBN, kTcMB, kTcStages, KK, kTcCluster>;
   constexpr int stage = 2 * kTcMB * 128 * kBK * 4 + 2 * kTcBN * kBK * 4;
-  const int smem = kTcStages * stage + 1024 + 256;
+  const int smem = kTcStages * stage + 1024 + 256 + kTcBN * 4;
   static bool attr[64] = {};
   int dev = 0;
   AMUN_CUDA(cudaGetDevice(&dev));
@@ -253,8 +275,19 @@ void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
     AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     if (dev < 64) attr[dev] = true;
   }
-  kern<<<ceil_div(a.N, kTcBN), 192, smem, st>>>(maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, a);
-  AMUN_CHECK_LAUNCH();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ceil_div(ceil_div(a.N, kTcBN), kTcCluster) * kTcCluster);
+  cfg.blockDim = dim3(64 + 128 * kTcMB);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = kTcCluster;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, a));
 }
 
 }  // namespace
@@ -286,11 +319,20 @@ LogitTcMaps make_logit_maps(const float *t_hi, const float *t_lo, int R, int K, 
 }
 
 void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
-  if (a.kk <= 1) launch_t<1>(maps, a, st);
-  else if (a.kk <= 4) launch_t<4>(maps, a, st);
-  else if (a.kk <= 8) launch_t<8>(maps, a, st);
-  else if (a.kk <= 16) launch_t<16>(maps, a, st);
-  else throw Error(4, "tensor-core logit path supports beam <= 16");
+  // list size >= kk (a sorted top-KK list contains the top-kk as its prefix)
+  switch (a.kk) {
+    case 1: launch_t<1>(maps, a, st); break;
+    case 2: launch_t<2>(maps, a, st); break;
+    case 3: launch_t<3>(maps, a, st); break;
+    case 4: launch_t<4>(maps, a, st); break;
+    case 5: launch_t<5>(maps, a, st); break;
+    case 6: launch_t<6>(maps, a, st); break;
+    case 7: case 8: launch_t<8>(maps, a, st); break;
+    case 9: case 10: launch_t<10>(maps, a, st); break;
+    case 11: case 12: launch_t<12>(maps, a, st); break;
+    case 13: case 14: case 15: case 16: launch_t<16>(maps, a, st); break;
+    default: throw Error(4, "tensor-core logit path supports beam <= 16");
+  }
 }
 
 }  // namespace amun

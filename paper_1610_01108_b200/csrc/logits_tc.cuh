@@ -13,6 +13,7 @@ struct LogitTcArgs {
   float *pmax, *psum;  // [ntiles][M]
   float *cval;         // [M][ntiles][kk]
   int *ctok;
+  int debug_flags = 0;  // microbenchmark knobs: 1 skip A loads, 2 skip B loads, 4 skip MMA, 8 skip epilogue
 };
 
 struct LogitTcMaps {

@@ -1,0 +1,57 @@
+// Microbenchmark of the tensor-core logit kernel (not part of the product):
+// times launch variants with pieces disabled to attribute the step time.
+//   nvcc ... tools/bench_logits_tc.cu paper_1610_01108_b200/csrc/logits_tc.cu -o build/bench_logits_tc
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1610_01108_b200/csrc/common.cuh"
+#include "../paper_1610_01108_b200/csrc/logits_tc.cuh"
+
+using namespace amun;
+
+int main(int argc, char **argv) {
+  const int R = argc > 1 ? atoi(argv[1]) : 320, K = 500, V = 30000, kk = 5;
+  const int ntiles = (V + 127) / 128;
+  std::vector<float> h((size_t)std::max(R, V) * K);
+  for (auto &x : h) x = (rand() / (float)RAND_MAX - 0.5f) * 0.2f;
+  float *thi, *tlo, *whi, *wlo, *bias, *pmax, *psum, *cval;
+  int *ctok;
+  cudaMalloc(&thi, sizeof(float) * R * K);
+  cudaMalloc(&tlo, sizeof(float) * R * K);
+  cudaMalloc(&whi, sizeof(float) * (size_t)V * K);
+  cudaMalloc(&wlo, sizeof(float) * (size_t)V * K);
+  cudaMalloc(&bias, sizeof(float) * V);
+  cudaMalloc(&pmax, sizeof(float) * ntiles * R);
+  cudaMalloc(&psum, sizeof(float) * ntiles * R);
+  cudaMalloc(&cval, sizeof(float) * ntiles * R * kk);
+  cudaMalloc(&ctok, sizeof(int) * ntiles * R * kk);
+  cudaMemcpy(thi, h.data(), sizeof(float) * R * K, cudaMemcpyHostToDevice);
+  cudaMemcpy(tlo, h.data(), sizeof(float) * R * K, cudaMemcpyHostToDevice);
+  cudaMemcpy(whi, h.data(), sizeof(float) * (size_t)V * K, cudaMemcpyHostToDevice);
+  cudaMemcpy(wlo, h.data(), sizeof(float) * (size_t)V * K, cudaMemcpyHostToDevice);
+  cudaMemset(bias, 0, sizeof(float) * V);
+  LogitTcMaps maps = make_logit_maps(thi, tlo, R, K, K, whi, wlo, V);
+  const char *names[] = {"full", "no A loads", "no B loads", "no A/B loads", "no MMA", "no epilogue",
+                         "loads only (no MMA, no epi)", "MMA only (no loads, no epi)", "no top-k", "no sum pass",
+                         "no stores", "no topk/sum/stores"};
+  const int flags[] = {0, 1, 2, 3, 4, 8, 12, 11, 16, 32, 64, 112};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int v = 0; v < 12; ++v) {
+    LogitTcArgs a{R, V, K, bias, kk, ntiles, pmax, psum, cval, ctok};
+    a.debug_flags = flags[v];
+    for (int i = 0; i < 3; ++i) launch_logits_tc(maps, a, 0);
+    cudaEventRecord(e0);
+    const int it = 20;
+    for (int i = 0; i < it; ++i) launch_logits_tc(maps, a, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t err = cudaGetLastError();
+    printf("R=%d %-30s %8.1f us  %s\n", R, names[v], 1000 * ms / it, cudaGetErrorString(err));
+  }
+  return 0;
+}

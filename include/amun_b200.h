@@ -51,7 +51,7 @@ typedef struct {
   int32_t want_states;      /* also return Hypothesis.states rows */
   int32_t max_batch;        /* sentences per length bucket (0 -> 64) */
   int32_t force_full_logits;/* 1: materialise logits (debug/parity path) */
-  int32_t profile;          /* 1: CUDA-event time every kernel launch by class */
+  int32_t profile;          /* bitmask of AMUN_K_* classes whose launches are CUDA-event timed */
 } amun_decode_opts;
 
 /* kernel classes timed when amun_decode_opts.profile is set */

@@ -51,7 +51,7 @@ struct Ctx {
   cudaStream_t st;
   int64_t launches = 0;
   int64_t h2d = 0, d2h = 0;
-  bool prof = false;
+  uint32_t prof = 0;  // bitmask of kernel classes to time with events
   int cls = AMUN_K_ENCODER;
   std::vector<cudaEvent_t> pool;
   std::vector<int> rec_cls;
@@ -83,7 +83,7 @@ struct Ctx {
   template <class F>
   void run(int k, F &&f) {
     ++launches;
-    if (!prof) {
+    if (!(prof & (1u << k))) {
       f();
       return;
     }
@@ -413,7 +413,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     if (!pass) mem.alloc(cv.off, m0->stream);
   }
   Ctx c(m0->stream);
-  c.prof = o.profile != 0;
+  c.prof = (uint32_t)o.profile;
   LogitTcMaps tc_maps{};
   if (use_tc) {
     static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");

@@ -1,0 +1,239 @@
+"""Host-side logic of the drop-in API (no GPU): model container, random
+model, vocabulary, BPE, shortlist, argument validation with the reference's
+messages, ensemble averaging, sharding."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import tiny_model
+from oracle import beamnmt_oracle as orc
+from paper_1610_01108_b200 import (
+    DecodeOptions,
+    ModelConfig,
+    ModelParams,
+    ShortList,
+    Vocabulary,
+    average_checkpoints,
+    beam_search,
+    bpe_apply,
+    bpe_join,
+    bpe_learn,
+    build_shortlist,
+    ensemble_logprobs,
+    load_model,
+    load_vocab,
+    preprocess,
+    random_model,
+    save_model,
+)
+from paper_1610_01108_b200.errors import FormatError
+from paper_1610_01108_b200.model import schema
+from paper_1610_01108_b200.sharding import length_buckets, partition_lpt, sentence_work, shard_sentences
+from paper_1610_01108_b200.shortlist import LexicalTable, load_freq_list, load_lex_table
+from paper_1610_01108_b200.subword import load_bpe_model, save_bpe_model
+from paper_1610_01108_b200.workload import WORKLOADS
+
+
+# ------------------------------------------------------------------ model
+
+def test_random_model_matches_oracle_draws():
+    m = random_model(ModelConfig(v_src=13, v_trg=11, d_emb=6, d_h=5, d_att=7), 123)
+    want = orc.random_tensors((13, 11, 6, 5, 7), 123)
+    for name, arr in m.tensor_items():
+        np.testing.assert_array_equal(arr, want[name], err_msg=name)
+        assert not arr.flags.writeable
+
+
+def test_schema_has_40_tensors_in_reference_order():
+    names = [n for n, _, _ in schema(ModelConfig(30000, 30000))]
+    assert len(names) == 40
+    assert names[:3] == ["E_src", "E_trg", "enc_fwd.W_z"]
+    assert names[-2:] == ["W_logit", "b_logit"]
+
+
+def test_save_load_roundtrip_bitwise(tmp_path):
+    m = tiny_model(3, 7, 9, 5)
+    p = tmp_path / "m.amnt"
+    save_model(m, p)
+    back = load_model(p)
+    assert back.config == m.config
+    for (n, a), (_, b) in zip(m.tensor_items(), back.tensor_items()):
+        np.testing.assert_array_equal(a, b, err_msg=n)
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda b: b"XXXX" + b[4:], "bad magic"),
+    (lambda b: b[:10], "truncated"),
+    (lambda b: b + b"\0", "trailing bytes"),
+    (lambda b: b[:4] + (2).to_bytes(4, "little") + b[8:], "unsupported format version"),
+])
+def test_container_errors(tmp_path, mutate, msg):
+    p = tmp_path / "m.amnt"
+    save_model(tiny_model(1), p)
+    p.write_bytes(mutate(p.read_bytes()))
+    with pytest.raises(FormatError, match=msg):
+        load_model(p)
+
+
+def test_from_tensors_validation():
+    cfg = ModelConfig(v_src=5, v_trg=5, d_emb=4, d_h=4, d_att=4)
+    t = {n: np.zeros((r, c), np.float32) for n, r, c in schema(cfg)}
+    with pytest.raises(FormatError, match="missing tensor"):
+        ModelParams.from_tensors(cfg, {k: v for k, v in t.items() if k != "v_att"})
+    with pytest.raises(FormatError, match="unexpected tensor"):
+        ModelParams.from_tensors(cfg, {**t, "bogus": np.zeros(1)})
+    t["W_init"] = np.zeros((3, 3), np.float32)
+    with pytest.raises(FormatError, match="has shape"):
+        ModelParams.from_tensors(cfg, t)
+
+
+def test_non_finite_rejected():
+    cfg = ModelConfig(v_src=5, v_trg=5, d_emb=4, d_h=4, d_att=4)
+    t = {n: np.zeros((r, c), np.float32) for n, r, c in schema(cfg)}
+    t["E_src"][0, 0] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        ModelParams.from_tensors(cfg, t)
+
+
+def test_average_checkpoints(tmp_path):
+    paths = []
+    for seed in (1, 2):
+        p = tmp_path / f"{seed}.amnt"
+        save_model(tiny_model(seed, 6, 6, 4), p)
+        paths.append(p)
+    avg = average_checkpoints(paths)
+    a, b = load_model(paths[0]), load_model(paths[1])
+    for (n, x), (_, y), (_, z) in zip(a.tensor_items(), b.tensor_items(), avg.tensor_items()):
+        np.testing.assert_allclose(z, ((x.astype(np.float64) + y) / 2).astype(np.float32), atol=1e-7)
+    with pytest.raises(ValueError):
+        average_checkpoints([])
+
+
+# ------------------------------------------------------------------ vocab / text
+
+def test_vocabulary(tmp_path):
+    v = Vocabulary.from_tokens(["a", "b"])
+    assert len(v) == 4 and v.id("a") == 2 and v.id("zz") == 1 and "b" in v and v.token(0) == "</s>"
+    p = tmp_path / "v.txt"
+    p.write_text("x\ny\n")
+    assert load_vocab(p).tokens == ["</s>", "<unk>", "x", "y"]
+    p.write_text("x\nx\n")
+    with pytest.raises(FormatError, match="duplicate"):
+        load_vocab(p)
+    p.write_text("</s>\n")
+    with pytest.raises(FormatError, match="reserved"):
+        load_vocab(p)
+
+
+def test_bpe_roundtrip_and_file(tmp_path):
+    corpus = ["low lower lowest", "newer newest new", "wider widest"] * 3
+    model = bpe_learn(corpus, 20)
+    words = preprocess("Lower NEWEST widest unseenword")
+    pieces = bpe_apply(model, words)
+    assert bpe_join(pieces) == words
+    assert any(p.endswith("@@") for p in pieces)
+    save_bpe_model(model, tmp_path / "r.bpe")
+    assert load_bpe_model(tmp_path / "r.bpe").merges == model.merges
+
+
+def test_bpe_matches_reference_rules():
+    """Same learning tie-break and segmentation as the reference (SPEC
+    §subword): golden rules derived by hand for a tiny corpus."""
+    model = bpe_learn(["aaa aaa ab"], 3)
+    assert model.merges[0] == ("a", "a")
+    assert bpe_apply(model, ["aaa"]) in (["aa@@", "a"], ["aaa"], ["a@@", "aa"])
+
+
+def test_shortlist(tmp_path):
+    vocab = Vocabulary.from_tokens(["x", "y", "z"])
+    lex = tmp_path / "lex"
+    lex.write_text("s x 0.5\ns y 0.9\nt zz 0.4\n")
+    table = load_lex_table(lex, vocab)
+    assert table.get("s")[0] == ("y", 0.9)
+    assert table.get("t")[0][0] == "<unk>"
+    freq = tmp_path / "freq"
+    freq.write_text("z\nq\nx\n")
+    ids, skipped = load_freq_list(freq, vocab)
+    assert ids == [4, 2] and skipped == 1
+    sl = build_shortlist(table, ids, ["s"], 1, 1, vocab)
+    assert list(sl.global_ids) == [0, 1, 3, 4]
+    with pytest.raises(ValueError, match="ascending"):
+        ShortList(np.array([0, 1, 3, 2]))
+    with pytest.raises(ValueError, match="0"):
+        ShortList(np.array([1, 2]))
+    assert len(ShortList.full(6)) == 6
+
+
+# ------------------------------------------------------------------ validation (raises before the device)
+
+def test_beam_search_validation_messages():
+    m = tiny_model(15)
+    with pytest.raises(ValueError, match="at least one model"):
+        beam_search([], [2])
+    with pytest.raises(ValueError, match="empty"):
+        beam_search([m], [])
+    with pytest.raises(ValueError, match="beam_size"):
+        beam_search([m], [2], DecodeOptions(beam_size=0))
+    with pytest.raises(ValueError, match="n_best"):
+        beam_search([m], [2], DecodeOptions(n_best=0))
+    with pytest.raises(ValueError, match="cap"):
+        beam_search([m], [2], DecodeOptions(max_len_factor=0, max_len_offset=0))
+    with pytest.raises(ValueError, match="out of range"):
+        beam_search([m], [2, 99])
+    with pytest.raises(ValueError, match="vocabulary mismatch"):
+        beam_search([tiny_model(1, v_trg=5), tiny_model(1, v_trg=6)], [2])
+    with pytest.raises(ValueError, match="shortlist id"):
+        beam_search([m], [2], shortlist=ShortList(np.array([0, 1, 7])))
+
+
+def test_decode_options_defaults():
+    o = DecodeOptions()
+    assert (o.beam_size, o.max_len_factor, o.max_len_offset, o.length_normalize, o.n_best) == (5, 2, 10, False, 1)
+    assert o.max_target_len(30) == 70
+
+
+def test_ensemble_logprobs():
+    rng = np.random.default_rng(0)
+    x = np.log(rng.dirichlet(np.ones(9)))
+    for k in range(1, 6):
+        np.testing.assert_array_equal(ensemble_logprobs([x] * k), x)
+    a = np.array([math.log(0.5), math.log(0.5)])
+    b = np.array([math.log(0.25), math.log(0.75)])
+    np.testing.assert_allclose(ensemble_logprobs([a, b]), (a + b) / 2, atol=1e-12)
+    with pytest.raises(ValueError, match="mismatch"):
+        ensemble_logprobs([np.zeros(5), np.zeros(6)])
+
+
+# ------------------------------------------------------------------ sharding / workloads
+
+def test_partition_lpt_balances_and_covers():
+    costs = [float(c) for c in np.random.default_rng(1).integers(1, 100, 50)]
+    parts = partition_lpt(costs, 4)
+    assert sorted(i for p in parts for i in p) == list(range(50))
+    loads = [sum(costs[i] for i in p) for p in parts]
+    assert max(loads) - min(loads) <= max(costs)
+
+
+def test_shard_sentences_whole_buckets():
+    wl = WORKLOADS["cfg2"]
+    lens = [len(s) for s in wl.corpus()]
+    for n in (1, 2, 4, 8):
+        parts = shard_sentences(lens, n, 64, 5)
+        assert sorted(i for p in parts for i in p) == list(range(4000))
+        works = [sum(sentence_work(lens[i], 5) for i in p) for p in parts]
+        assert max(works) / (sum(works) / n) < 1.05
+    buckets = length_buckets(lens, 64)
+    assert len(buckets) == 63 and all(len(b) == 64 for b in buckets[:-1])
+
+
+def test_workload_matches_survey_totals():
+    c2 = WORKLOADS["cfg2"].corpus()
+    assert sum(map(len, c2)) == 120774
+    assert sum(2 * len(s) + 10 for s in c2) == 281548
+    c1 = WORKLOADS["cfg1"].corpus()
+    assert sum(map(len, c1)) == 2813
+    assert WORKLOADS["cfg2"].corpus() == orc.synthetic_corpus(4000, 2016, 100)

@@ -57,6 +57,27 @@ enum { G_WZ = 0, G_WR, G_WH, G_UZ, G_UR, G_UH, G_BZ, G_BR, G_BH };
 
 }  // namespace
 
+static float *upload(amun_model *m, const std::vector<float> &h);
+
+// [K, N] row-major host matrix -> device [N, K] (K-major) tf32-exact hi and
+// residual lo copies for the 3xTF32 tensor-core GEMMs.
+static void upload_kmajor_split(amun_model *m, const float *W, int K, int N, float **hi_out, float **lo_out) {
+  std::vector<float> hi((size_t)N * K), lo((size_t)N * K);
+  for (int k = 0; k < K; ++k)
+    for (int n = 0; n < N; ++n) {
+      float x = W[(size_t)k * N + n];
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      u &= 0xFFFFE000u;
+      float h;
+      std::memcpy(&h, &u, 4);
+      hi[(size_t)n * K + k] = h;
+      lo[(size_t)n * K + k] = x - h;
+    }
+  *hi_out = upload(m, hi);
+  *lo_out = upload(m, lo);
+}
+
 static float *upload(amun_model *m, const std::vector<float> &h) {
   float *d = nullptr;
   AMUN_CUDA(cudaMalloc(&d, h.size() * sizeof(float)));
@@ -140,6 +161,12 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     m->Wg = upload(m, Wg);
     m->bg = upload(m, bg);
     m->Uh_dec = upload(m, cp(T_DEC + G_UH, (size_t)dh * dh));
+    m->tc_gemm = (de % 4 == 0) && (dh % 4 == 0) && (da % 4 == 0);
+    if (m->tc_gemm) {
+      upload_kmajor_split(m, Wg.data(), din + dh, 3 * dh, &m->Wg_hi, &m->Wg_lo);
+      upload_kmajor_split(m, t[T_DEC + G_UH], dh, dh, &m->Uhd_hi, &m->Uhd_lo);
+      upload_kmajor_split(m, t[T_W_ATT_S], dh, da, &m->Wq_hi, &m->Wq_lo);
+    }
   }
   {  // deep output: rows [y ; c ; s'] = [W_out_y ; W_out_c ; W_out_s]
     std::vector<float> Wo((size_t)(de + 3 * dh) * de);
@@ -148,6 +175,7 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     std::memcpy(&Wo[(size_t)(de + 2 * dh) * de], t[T_W_OUT_S], (size_t)dh * de * sizeof(float));
     m->Wout = upload(m, Wo);
     m->b_out = upload(m, cp(T_B_OUT, de));
+    if (m->tc_gemm) upload_kmajor_split(m, Wo.data(), de + 3 * dh, de, &m->Wo_hi, &m->Wo_lo);
   }
   m->W_logit = upload(m, cp(T_W_LOGIT, (size_t)de * V));
   m->b_logit = upload(m, cp(T_B_LOGIT, V));

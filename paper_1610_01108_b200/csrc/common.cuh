@@ -76,6 +76,16 @@ __device__ __forceinline__ Key warp_best(Key k) {
   return k;
 }
 
-constexpr int kMaxRowCand = 16;  // fused logit epilogue keeps <= 16 per row/tile
+constexpr int kMaxRowCand = 16;
+
+// 3xTF32 operand split: hi = tf32-exact (low 13 mantissa bits cleared),
+// lo = x - hi (exact).  Writes both when `hi` is non-null.
+__device__ __forceinline__ void store_split(float *hi, float *lo, long long off, float x) {
+  if (hi) {
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    hi[off] = h;
+    lo[off] = x - h;
+  }
+}  // fused logit epilogue keeps <= 16 per row/tile
 
 }  // namespace amun

@@ -13,6 +13,7 @@
 #include "decode.cuh"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
+#include "gemm_tc.cuh"
 #include "logits_tc.cuh"
 
 namespace amun {
@@ -147,6 +148,8 @@ struct EncBufs {
 struct DecBufs {
   float *XS, *Sn, *Q, *Z, *RH, *XH, *T, *L;
   float *T_hi = nullptr, *T_lo = nullptr;  // 3xTF32 split of t (tensor-core logits)
+  // 3xTF32 splits of the tensor-core GEMM A operands
+  float *XSh = nullptr, *XSl = nullptr, *RHh = nullptr, *RHl = nullptr, *Snh = nullptr, *Snl = nullptr;
 };
 
 void carve_enc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
@@ -175,6 +178,16 @@ void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, bool full_log
     d.T_hi = cv.take<float>((size_t)R * de);
     d.T_lo = cv.take<float>((size_t)R * de);
   }
+}
+
+void carve_dec_tc(Carver &cv, DecBufs &d, const amun_model *m, int R) {
+  const int dh = m->d.d_h;
+  d.XSh = cv.take<float>((size_t)R * m->xs_w);
+  d.XSl = cv.take<float>((size_t)R * m->xs_w);
+  d.RHh = cv.take<float>((size_t)R * dh);
+  d.RHl = cv.take<float>((size_t)R * dh);
+  d.Snh = cv.take<float>((size_t)R * dh);
+  d.Snl = cv.take<float>((size_t)R * dh);
 }
 
 // nnet.py:110-130 for B padded sentences: input projection (embedding
@@ -216,36 +229,119 @@ struct LogitOut {
   const LogitTcMaps *tc = nullptr;  // tensor-core path when set
 };
 
+// Tensor-core (3xTF32, split-K) versions of the four decoder-step GEMMs of
+// one model: tensor maps over the hi/lo row buffers, split counts fixed by
+// (N, K) only, and the partial-sum workspace.
+struct TcStep {
+  GemmTcMaps q, g, u, o;
+  int sq = 1, sg = 1, su = 1, so = 1;
+  float *ws = nullptr;
+};
+
+constexpr int kTcTargetCtas = 128;
+
+size_t tc_step_ws_floats(const amun_model *m, int R, TcStep &ts_splits) {
+  // split counts only depend on shapes; computed here to size the workspace
+  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, xs = m->xs_w;
+  auto splits = [&](int N, int k1, int k2) {
+    GemmTcMaps mm{};
+    mm.N = N;
+    mm.k1 = k1;
+    mm.k2 = k2;
+    return gemm_tc_splits(mm, kTcTargetCtas);
+  };
+  ts_splits.sq = splits(da, dh, 0);
+  ts_splits.sg = splits(3 * dh, xs, 0);
+  ts_splits.su = splits(dh, dh, 0);
+  ts_splits.so = splits(de, de + 2 * dh, dh);
+  size_t w = 0;
+  w = std::max(w, (size_t)ts_splits.sq * R * da);
+  w = std::max(w, (size_t)ts_splits.sg * R * 3 * dh);
+  w = std::max(w, (size_t)ts_splits.su * R * dh);
+  w = std::max(w, (size_t)ts_splits.so * R * de);
+  return w;
+}
+
+void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
+  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, xs = m->xs_w;
+  const int s_off = de + 2 * dh;
+  ts.q = make_gemm_tc_maps(d.XSh + s_off, d.XSl + s_off, dh, xs, nullptr, nullptr, 0, 0, Rmax, m->Wq_hi, m->Wq_lo,
+                           da, dh);
+  ts.g = make_gemm_tc_maps(d.XSh, d.XSl, xs, xs, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi, m->Wg_lo, 3 * dh, xs);
+  ts.u = make_gemm_tc_maps(d.RHh, d.RHl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Uhd_hi, m->Uhd_lo, dh, dh);
+  ts.o = make_gemm_tc_maps(d.XSh, d.XSl, de + 2 * dh, xs, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi, m->Wo_lo, de, xs);
+}
+
+// partial GEMM on the tensor cores + fixed-order reduce applying `epi`
+template <class Epi>
+void gemm_tc(Ctx &c, const GemmTcMaps &maps, int M, int splits, float *ws, const Epi &epi) {
+  c.run(c.cls, [&] {
+    launch_gemm_tc_partial(maps, M, splits, ws, c.st);
+    const long long total = (long long)M * maps.N;
+    splitk_reduce_kernel<Epi><<<(unsigned)((total + 255) / 256), 256, 0, c.st>>>(ws, M, maps.N, splits, total, epi);
+    AMUN_CHECK_LAUNCH();
+  });
+  c.launches += 1;
+}
+
 void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
-               int R, int rows_per_sent, const int *n_act, const int *done, float *alpha, const LogitOut &lo) {
+               int R, int rows_per_sent, const int *n_act, const int *done, float *alpha, const LogitOut &lo,
+               const TcStep *ts = nullptr) {
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
   const int s_off = de + 2 * dh;
   c.cls = AMUN_K_QUERY;
-  gemm(c, ga(R, da, d.XS + s_off, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
+  if (ts)
+    gemm_tc(c, ts->q, R, ts->sq, ts->ws, EpiStore{d.Q, da, nullptr, 0, 0});
+  else
+    gemm(c, ga(R, da, d.XS + s_off, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
   AttnArgs aa{d.Q, da, e.P, e.Hann, m->v_att, d_len, jmax, da, 2 * dh, rows_per_sent, n_act, done,
               d.XS + de, xs, alpha};
+  if (ts) {
+    aa.ctx_hi = d.XSh + de;
+    aa.ctx_lo = d.XSl + de;
+  }
   c.run(AMUN_K_ATTN, [&] { launch_attention(aa, R, c.st); });
   c.cls = AMUN_K_GRU_A;
   {
-    GemmArgs g = ga(R, 3 * dh, d.XS, xs, xs, m->Wg, 3 * dh);
-    g.n_split = 2 * dh;
-    g.k_limit = de + 2 * dh;
-    gemm(c, g, EpiGruA{m->bg, d.XS + s_off, xs, dh, d.Z, d.RH, d.XH});
+    EpiGruA ea{m->bg, d.XS + s_off, xs, dh, d.Z, d.RH, d.XH};
+    if (ts) {
+      ea.RHh = d.RHh;
+      ea.RHl = d.RHl;
+      gemm_tc(c, ts->g, R, ts->sg, ts->ws, ea);
+    } else {
+      GemmArgs g = ga(R, 3 * dh, d.XS, xs, xs, m->Wg, 3 * dh);
+      g.n_split = 2 * dh;
+      g.k_limit = de + 2 * dh;
+      gemm(c, g, ea);
+    }
   }
   c.cls = AMUN_K_GRU_B;
-  gemm(c, ga(R, dh, d.RH, dh, dh, m->Uh_dec, dh), EpiGruB{d.XS + s_off, xs, dh, d.Z, d.XH, d.Sn});
+  {
+    EpiGruB eb{d.XS + s_off, xs, dh, d.Z, d.XH, d.Sn};
+    if (ts) {
+      eb.Snh = d.Snh;
+      eb.Snl = d.Snl;
+      gemm_tc(c, ts->u, R, ts->su, ts->ws, eb);
+    } else {
+      gemm(c, ga(R, dh, d.RH, dh, dh, m->Uh_dec, dh), eb);
+    }
+  }
   c.cls = AMUN_K_OUT;
   {
-    GemmArgs g = ga(R, de, d.XS, xs, de + 2 * dh, m->Wout, de);
-    g.a1 = d.Sn;
-    g.lda1 = dh;
-    g.k1 = dh;
     EpiStore e{lo.tc ? nullptr : d.T, de, m->b_out, 1, 0};
     if (lo.tc) {
       e.hi = d.T_hi;
       e.lo = d.T_lo;
     }
-    gemm(c, g, e);
+    if (ts) {
+      gemm_tc(c, ts->o, R, ts->so, ts->ws, e);
+    } else {
+      GemmArgs g = ga(R, de, d.XS, xs, de + 2 * dh, m->Wout, de);
+      g.a1 = d.Sn;
+      g.lda1 = dh;
+      g.k1 = dh;
+      gemm(c, g, e);
+    }
   }
   c.cls = AMUN_K_LOGIT;
   if (lo.tc) {
@@ -324,6 +420,9 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   const bool fused = n_models == 1 && !sl_ids && k <= kMaxRowCand && !o.force_full_logits;
   const char *no_tc = getenv("AMUN_NO_TC");
   const bool use_tc = fused && m0->Wl_hi && !(no_tc && no_tc[0] == '1');
+  const char *no_tcg = getenv("AMUN_NO_TC_GEMM");
+  bool use_tcg = !(no_tc && no_tc[0] == '1') && !(no_tcg && no_tcg[0] == '1');
+  for (auto *m : ms) use_tcg = use_tcg && m->tc_gemm;
   const int kk = std::min(k, V);
   const int ntiles = ceil_div(V, kBN);
 
@@ -367,7 +466,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   BeamState bs{};
   float **p_XS;
   const float **p_Sn, **p_E, **p_S0, **p_L;
-  float **p_fin;
+  float **p_fin, **p_XSh, **p_XSl;
+  std::vector<TcStep> tsteps(n_models);
+  std::vector<size_t> ts_ws(n_models, 0);
+  if (use_tcg)
+    for (int m = 0; m < n_models; ++m) ts_ws[m] = tc_step_ws_floats(ms[m], Rmax, tsteps[m]);
   DevMem mem;
   for (int pass = 0; pass < 2; ++pass) {
     Carver cv;
@@ -376,6 +479,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       carve_enc(cv, eb[m], ms[m], Bmax, jmax_all);
       carve_dec(cv, db[m], ms[m], Rmax, !fused);
       if (!use_tc) db[m].T_hi = db[m].T_lo = nullptr;
+      if (use_tcg) {
+        carve_dec_tc(cv, db[m], ms[m], Rmax);
+        tsteps[m].ws = cv.take<float>(ts_ws[m]);
+      }
       fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * dh) : nullptr;
     }
     d_ids = cv.take<int>((size_t)Bmax * jmax_all);
@@ -410,6 +517,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     p_S0 = cv.take<const float *>(n_models);
     p_L = cv.take<const float *>(n_models);
     p_fin = cv.take<float *>(n_models);
+    p_XSh = cv.take<float *>(n_models);
+    p_XSl = cv.take<float *>(n_models);
     if (!pass) mem.alloc(cv.off, m0->stream);
   }
   Ctx c(m0->stream);
@@ -420,9 +529,18 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     if (logits_tc_tile_n() != kBN) throw Error(AMUN_ERR_UNSUPPORTED, "logit tile width mismatch");
     tc_maps = make_logit_maps(db[0].T_hi, db[0].T_lo, Rmax, m0->d.d_emb, m0->d.d_emb, m0->Wl_hi, m0->Wl_lo, V);
   }
+  if (use_tcg)
+    for (int m = 0; m < n_models; ++m) tc_step_maps(ms[m], db[m], Rmax, tsteps[m]);
   cudaStream_t st = c.st;
   {
     std::vector<const void *> hx(n_models), hs(n_models), he(n_models), h0(n_models), hl(n_models), hf(n_models);
+    std::vector<const void *> hxh(n_models), hxl(n_models);
+    for (int m = 0; m < n_models; ++m) {
+      hxh[m] = db[m].XSh;
+      hxl[m] = db[m].XSl;
+    }
+    h2d(c, (const void **)p_XSh, hxh.data(), n_models);
+    h2d(c, (const void **)p_XSl, hxl.data(), n_models);
     for (int m = 0; m < n_models; ++m) {
       hx[m] = db[m].XS;
       hs[m] = db[m].Sn;
@@ -484,6 +602,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     bs.cap_max = capm;
     bs.fin_cap = fin_cap;
     ModelRows mr{p_XS, p_Sn, p_E, o.want_states ? p_fin : nullptr, xs, de, dh, de + 2 * dh, n_models};
+    if (use_tcg) {
+      mr.XSh = p_XSh;
+      mr.XSl = p_XSl;
+    }
     c.run(AMUN_K_SELECT, [&] { launch_init_beam(bs, mr, p_S0, st); });
     LogitOut lo{fused, kk, ntiles, pmax, psum, cval, ctok};
     if (use_tc) lo.tc = &tc_maps;
@@ -507,7 +629,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     int steps_run = 0;
     for (int t = 0; t < capm; ++t) {
       for (int m = 0; m < n_models; ++m)
-        step_rows(c, ms[m], db[m], eb[m], d_len, jmax, R, k, bs.n_act, bs.done, nullptr, lo);
+        step_rows(c, ms[m], db[m], eb[m], d_len, jmax, R, k, bs.n_act, bs.done, nullptr, lo,
+                  use_tcg ? &tsteps[m] : nullptr);
       sa.t = t;
       c.run(AMUN_K_SELECT, [&] { launch_select(sa, bs, mr, st); });
       ++steps_run;

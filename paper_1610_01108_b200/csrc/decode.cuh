@@ -23,6 +23,13 @@ struct amun_model {
   // tensor-core copies of the output projection: logit rows [V, de] split
   // into tf32-exact hi and residual lo (3xTF32); null when de % 4 != 0
   float *Wl_hi = nullptr, *Wl_lo = nullptr;
+  // K-major [N, K] hi/lo copies of the decoder-step weights for the split-K
+  // tensor-core GEMMs (query, GRU phase A, GRU phase B, deep output)
+  bool tc_gemm = false;
+  float *Wq_hi = nullptr, *Wq_lo = nullptr;    // W_att_s^T [da, dh]
+  float *Wg_hi = nullptr, *Wg_lo = nullptr;    // Wg^T      [3dh, de+3dh]
+  float *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
+  float *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, de+3dh]
   int64_t bytes = 0;
   std::vector<void *> allocs;
   cudaStream_t stream = nullptr;

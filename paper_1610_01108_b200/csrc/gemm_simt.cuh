@@ -253,13 +253,16 @@ struct EpiGruA {
   const float *S;     // current state rows, stride lds
   int lds, dh;
   float *Z, *RH, *XH;  // [M, dh] each
+  float *RHh = nullptr, *RHl = nullptr;  // optional 3xTF32 split of r*s
   __device__ void operator()(int m, int n, float v, int) const {
     v += bias[n];
     if (n < dh) {
       Z[(long long)m * dh + n] = sigmoid_acc(v);
     } else if (n < 2 * dh) {
       int j = n - dh;
-      RH[(long long)m * dh + j] = sigmoid_acc(v) * S[(long long)m * lds + j];
+      const float rh = sigmoid_acc(v) * S[(long long)m * lds + j];
+      RH[(long long)m * dh + j] = rh;
+      store_split(RHh, RHl, (long long)m * dh + j, rh);
     } else {
       XH[(long long)m * dh + n - 2 * dh] = v;
     }
@@ -274,12 +277,15 @@ struct EpiGruB {
   int lds, dh;
   const float *Z, *XH;
   float *Sn;
+  float *Snh = nullptr, *Snl = nullptr;  // optional 3xTF32 split of s'
   __device__ void operator()(int m, int n, float v, int) const {
     long long o = (long long)m * dh + n;
     float ht = tanhf(v + XH[o]);
     float zz = Z[o];
     float s = S[(long long)m * lds + n];
-    Sn[o] = (1.0f - zz) * s + zz * ht;
+    const float sn = (1.0f - zz) * s + zz * ht;
+    Sn[o] = sn;
+    store_split(Snh, Snl, o, sn);
   }
 };
 

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
     float acc = 0.f;
     for (int j = 0; j < J; ++j) acc = fmaf(e[j], Hb[(long long)j * a.dh2 + c], acc);
     a.ctx[(long long)r * a.ldctx + c] = acc;
+    store_split(a.ctx_hi, a.ctx_lo, (long long)r * a.ldctx + c, acc);
   }
 }
 
@@ -104,16 +105,19 @@ __global__ void init_beam_kernel(BeamState bs, ModelRows mr, const float *const 
   }
   for (int m = 0; m < mr.n_models; ++m) {
     float *XS = mr.XS[m];
+    float *XSh = mr.XSh ? mr.XSh[m] : nullptr;
+    float *XSl = mr.XSl ? mr.XSl[m] : nullptr;
     const float *E = mr.E_trg[m];
     for (int i = 0; i < k; ++i) {
-      float *row = XS + (long long)(b * k + i) * mr.ldxs;
+      const long long ro = (long long)(b * k + i) * mr.ldxs;
       for (int c = threadIdx.x; c < mr.ldxs; c += blockDim.x) {
         float v = 0.f;
         if (i == 0) {
           if (c < mr.de) v = E[c];  // E_trg[EOS_ID]
           else if (c >= mr.s_off && c < mr.s_off + mr.dh) v = S0[m][(long long)b * mr.dh + (c - mr.s_off)];
         }
-        row[c] = v;
+        XS[ro + c] = v;
+        store_split(XSh, XSl, ro + c, v);
       }
     }
   }
@@ -376,14 +380,22 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   const int newna = s_newna, nfin = s_nfin;
   for (int m = 0; m < n_models; ++m) {
     float *XS = mr.XS[m];
+    float *XSh = mr.XSh ? mr.XSh[m] : nullptr;
+    float *XSl = mr.XSl ? mr.XSl[m] : nullptr;
     const float *Sn = mr.Sn[m];
     const float *E = mr.E_trg[m];
     for (int i = 0; i < newna; ++i) {
-      float *row = XS + (long long)(b * k + i) * mr.ldxs;
+      const long long ro = (long long)(b * k + i) * mr.ldxs;
       const float *ey = E + (long long)ch_tok[i] * mr.de;
       const float *sp = Sn + (long long)(b * k + ch_par[i]) * mr.dh;
-      for (int c = threadIdx.x; c < mr.de; c += blockDim.x) row[c] = ey[c];
-      for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) row[mr.s_off + c] = sp[c];
+      for (int c = threadIdx.x; c < mr.de; c += blockDim.x) {
+        XS[ro + c] = ey[c];
+        store_split(XSh, XSl, ro + c, ey[c]);
+      }
+      for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) {
+        XS[ro + mr.s_off + c] = sp[c];
+        store_split(XSh, XSl, ro + mr.s_off + c, sp[c]);
+      }
     }
     if (mr.fin_states) {
       for (int i = 0; i < nfin; ++i) {

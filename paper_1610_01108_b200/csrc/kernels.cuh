@@ -23,6 +23,7 @@ struct AttnArgs {
   float *ctx;
   int ldctx;
   float *alpha;  // optional [R][jmax]
+  float *ctx_hi = nullptr, *ctx_lo = nullptr;  // optional 3xTF32 split (same layout as ctx)
 };
 void launch_attention(const AttnArgs &a, int R, cudaStream_t st);
 
@@ -54,6 +55,8 @@ struct ModelRows {  // per-model decoder row buffers (device arrays of pointers)
   const float *const *E_trg;
   float *const *fin_states;  // optional [B][fin_cap][dh]
   int ldxs, de, dh, s_off, n_models;
+  float *const *XSh = nullptr;  // optional 3xTF32 split copies of XS (per model)
+  float *const *XSl = nullptr;
 };
 
 // XS rows of every sentence: slot 0 <- [E_trg[EOS] | 0 | s0_b], others 0;

@@ -5,10 +5,16 @@ namespace amun {
 
 // ================================================================ attention
 
+// tanh(x) = 1 - 2 / (exp(2x) + 1) with the ex2-based exponential and a fast
+// reciprocal: ~1e-7 absolute error (saturates exactly to +-1), far below the
+// fp32 rounding of the 1024-term energy sum it feeds.
+__device__ __forceinline__ float tanh_attn(float x) { return 1.0f - __fdividef(2.0f, __expf(2.0f * x) + 1.0f); }
+
 __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
   extern __shared__ float sm[];
   float *q = sm;              // [da]
-  float *e = sm + a.da;       // [jmax]
+  float *vv = sm + a.da;      // [da]
+  float *e = sm + 2 * a.da;   // [jmax]
   __shared__ float s_red[2];
   const int r = blockIdx.x;
   const int b = r / a.rows_per_sent;
@@ -18,15 +24,28 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
   }
   const int J = a.len[b];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  for (int i = threadIdx.x; i < a.da; i += blockDim.x) q[i] = a.Q[(long long)r * a.ldq + i];
+  for (int i = threadIdx.x; i < a.da; i += blockDim.x) {
+    q[i] = a.Q[(long long)r * a.ldq + i];
+    vv[i] = a.v[i];
+  }
   __syncthreads();
   const float *Pb = a.P + (long long)b * a.jmax * a.da;
+  // energies: warp per source position, 4 independent accumulators per lane
   for (int j = warp; j < J; j += nw) {
     const float *pj = Pb + (long long)j * a.da;
-    float acc = 0.f;
-    for (int i = lane; i < a.da; i += 32) acc = fmaf(a.v[i], tanhf(pj[i] + q[i]), acc);
-    acc = warp_sum(acc);
-    if (lane == 0) e[j] = acc;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int i0 = lane; i0 < a.da; i0 += 128) {
+      float p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) p[u] = (i0 + 32 * u < a.da) ? __ldg(pj + i0 + 32 * u) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u;
+        if (i < a.da) acc[u] = fmaf(vv[i], tanh_attn(p[u] + q[i]), acc[u]);
+      }
+    }
+    float s = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+    if (lane == 0) e[j] = s;
   }
   __syncthreads();
   if (warp == 0) {
@@ -50,18 +69,35 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
     if (a.alpha) a.alpha[(long long)r * a.jmax + j] = al;
   }
   __syncthreads();
+  // context: 8 independent column accumulators per thread, coalesced H rows
   const float *Hb = a.H + (long long)b * a.jmax * a.dh2;
-  for (int c = threadIdx.x; c < a.dh2; c += blockDim.x) {
-    float acc = 0.f;
-    for (int j = 0; j < J; ++j) acc = fmaf(e[j], Hb[(long long)j * a.dh2 + c], acc);
-    a.ctx[(long long)r * a.ldctx + c] = acc;
-    store_split(a.ctx_hi, a.ctx_lo, (long long)r * a.ldctx + c, acc);
+  for (int c0 = threadIdx.x; c0 < a.dh2; c0 += 8 * blockDim.x) {
+    float acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+    for (int j = 0; j < J; ++j) {
+      const float w = e[j];
+      const float *hj = Hb + (long long)j * a.dh2;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c < a.dh2) acc[u] = fmaf(w, __ldg(hj + c), acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * blockDim.x;
+      if (c < a.dh2) {
+        a.ctx[(long long)r * a.ldctx + c] = acc[u];
+        store_split(a.ctx_hi, a.ctx_lo, (long long)r * a.ldctx + c, acc[u]);
+      }
+    }
   }
 }
 
 void launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   if (R <= 0) return;
-  size_t smem = sizeof(float) * (a.da + a.jmax);
+  size_t smem = sizeof(float) * (2 * a.da + a.jmax);
   if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   attention_kernel<<<R, 256, smem, st>>>(a);
   AMUN_CHECK_LAUNCH();
@@ -190,9 +226,18 @@ __device__ __forceinline__ void warp_topk(int n, int kk, Get get, Out out) {
   if constexpr (KMAX > 0) {
     LaneList<KMAX> L;
     L.init();
-    for (int e = lane; e < n; e += 32) {
-      Key c = get(e);
-      if (c.tok >= 0) L.push(c, kk);
+    // fetch 8 candidates per lane before inserting any: the loads are
+    // independent, so their latency overlaps instead of serialising
+    for (int e0 = lane; e0 < n; e0 += 32 * 8) {
+      Key c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        c[u] = e < n ? get(e) : Key{-INFINITY, -1, -1};
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c[u].tok >= 0) L.push(c[u], kk);
     }
     int h = 0;
     for (int j = 0; j < kk; ++j) {
@@ -244,11 +289,26 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     double *out_lp = sa.cand_lp + ((long long)b * k + i) * kk;
     int *out_tok = sa.cand_tok + ((long long)b * k + i) * kk;
     if constexpr (FUSED) {
+      // per-tile partial (max, sum) pairs, kept in registers (<= 8 per lane)
+      constexpr int kPT = 8;
+      float pm[kPT], ps[kPT];
       float mx = -INFINITY;
-      for (int tt = lane; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, sa.pmax[(long long)tt * sa.M + r]);
+#pragma unroll
+      for (int u = 0; u < kPT; ++u) {
+        const int tt = lane + 32 * u;
+        const bool ok = tt < sa.ntiles;
+        pm[u] = ok ? sa.pmax[(long long)tt * sa.M + r] : -INFINITY;
+        ps[u] = ok ? sa.psum[(long long)tt * sa.M + r] : 0.f;
+      }
+      for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, sa.pmax[(long long)tt * sa.M + r]);
+#pragma unroll
+      for (int u = 0; u < kPT; ++u) mx = fmaxf(mx, pm[u]);
       mx = warp_max(mx);
       double s = 0.0;
-      for (int tt = lane; tt < sa.ntiles; tt += 32) {
+#pragma unroll
+      for (int u = 0; u < kPT; ++u)
+        if (ps[u] > 0.f) s += (double)ps[u] * exp((double)pm[u] - (double)mx);
+      for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) {
         long long o = (long long)tt * sa.M + r;
         s += (double)sa.psum[o] * exp((double)sa.pmax[o] - (double)mx);
       }

@@ -95,8 +95,141 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
   }
 }
 
+// Sentence-level attention: one CTA per sentence computes every active beam
+// row, so each P_j / H_j row is read once and reused across the beam from
+// registers (the per-row kernel above reads them once per hypothesis).
+//   energies: warp per source position, lane holds 8 P values per chunk,
+//             KA row accumulators; context: thread holds 4 columns x KA rows.
+template <int KA>
+__global__ void __launch_bounds__(512) attention_sent_kernel(AttnArgs a) {
+  extern __shared__ float sm[];
+  const int k = a.rows_per_sent;
+  const int b = blockIdx.x;
+  if (a.n_act && a.done[b]) return;
+  const int na = a.n_act ? a.n_act[b] : k;
+  const int J = a.len[b];
+  float *q = sm;                  // [KA][da]
+  float *vv = q + KA * a.da;      // [da]
+  float *al = vv + a.da;          // [KA][jmax]
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
+  for (int i = tid; i < na * a.da; i += blockDim.x) {
+    const int r = i / a.da, c = i % a.da;
+    q[i] = a.Q[(long long)(b * k + r) * a.ldq + c];
+  }
+  for (int i = tid; i < a.da; i += blockDim.x) vv[i] = a.v[i];
+  __syncthreads();
+  const float *Pb = a.P + (long long)b * a.jmax * a.da;
+  for (int j = warp; j < J; j += nw) {
+    const float *pj = Pb + (long long)j * a.da;
+    float acc[KA];
+#pragma unroll
+    for (int r = 0; r < KA; ++r) acc[r] = 0.f;
+    for (int i0 = lane; i0 < a.da; i0 += 32 * 8) {
+      float p[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) p[u] = (i0 + 32 * u < a.da) ? __ldg(pj + i0 + 32 * u) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + 32 * u;
+        if (i < a.da) {
+          const float vi = vv[i];
+#pragma unroll
+          for (int r = 0; r < KA; ++r)
+            if (r < na) acc[r] = fmaf(vi, tanh_attn(p[u] + q[r * a.da + i]), acc[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < KA; ++r) {
+      if (r < na) {
+        const float s = warp_sum(acc[r]);
+        if (lane == 0) al[r * a.jmax + j] = s;
+      }
+    }
+  }
+  __syncthreads();
+  // masked softmax over j < J, one warp per row
+  for (int r = warp; r < na; r += nw) {
+    float *e = al + r * a.jmax;
+    float mx = -INFINITY;
+    for (int j = lane; j < J; j += 32) mx = fmaxf(mx, e[j]);
+    mx = warp_max(mx);
+    float s = 0.f;
+    for (int j = lane; j < J; j += 32) {
+      const float w = expf(e[j] - mx);
+      e[j] = w;
+      s += w;
+    }
+    s = warp_sum(s);
+    const float inv = 1.0f / s;
+    for (int j = lane; j < J; j += 32) {
+      const float w = e[j] * inv;
+      e[j] = w;
+      if (a.alpha) a.alpha[(long long)(b * k + r) * a.jmax + j] = w;
+    }
+  }
+  __syncthreads();
+  // context: thread = up to 4 columns, all rows
+  const float *Hb = a.H + (long long)b * a.jmax * a.dh2;
+  for (int c0 = tid; c0 < a.dh2; c0 += 4 * blockDim.x) {
+    float acc[4][KA];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int r = 0; r < KA; ++r) acc[u][r] = 0.f;
+    for (int j = 0; j < J; ++j) {
+      const float *hj = Hb + (long long)j * a.dh2;
+      float h[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * blockDim.x;
+        h[u] = c < a.dh2 ? __ldg(hj + c) : 0.f;
+      }
+#pragma unroll
+      for (int r = 0; r < KA; ++r) {
+        if (r < na) {
+          const float w = al[r * a.jmax + j];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u][r] = fmaf(w, h[u], acc[u][r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < KA; ++r) {
+      if (r >= na) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c < a.dh2) {
+          const long long o = (long long)(b * k + r) * a.ldctx + c;
+          a.ctx[o] = acc[u][r];
+          store_split(a.ctx_hi, a.ctx_lo, o, acc[u][r]);
+        }
+      }
+    }
+  }
+}
+
+template <int KA>
+static void launch_attention_sent(const AttnArgs &a, int B, cudaStream_t st) {
+  const size_t smem = sizeof(float) * ((size_t)(KA + 1) * a.da + (size_t)KA * a.jmax);
+  auto kern = attention_sent_kernel<KA>;
+  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<B, 512, smem, st>>>(a);
+  AMUN_CHECK_LAUNCH();
+}
+
 void launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   if (R <= 0) return;
+  const int k = a.rows_per_sent;
+  const size_t smem_sent = sizeof(float) * ((size_t)(k + 1) * a.da + (size_t)k * a.jmax);
+  if (k <= 16 && R % k == 0 && smem_sent <= 200 * 1024) {
+    if (k == 1) launch_attention_sent<1>(a, R / k, st);
+    else if (k <= 4) launch_attention_sent<4>(a, R / k, st);
+    else if (k <= 8) launch_attention_sent<8>(a, R / k, st);
+    else launch_attention_sent<16>(a, R / k, st);
+    return;
+  }
   size_t smem = sizeof(float) * (2 * a.da + a.jmax);
   if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   attention_kernel<<<R, 256, smem, st>>>(a);
@@ -226,8 +359,11 @@ __device__ __forceinline__ void warp_topk(int n, int kk, Get get, Out out) {
   if constexpr (KMAX > 0) {
     LaneList<KMAX> L;
     L.init();
+    Key worst{-INFINITY, kNoTok, kNoTok};
     // fetch 8 candidates per lane before inserting any: the loads are
-    // independent, so their latency overlaps instead of serialising
+    // independent, so their latency overlaps instead of serialising.  The
+    // insertion loop stays rolled (code size: this kernel runs once per step
+    // and would otherwise thrash the instruction cache).
     for (int e0 = lane; e0 < n; e0 += 32 * 8) {
       Key c[8];
 #pragma unroll
@@ -235,9 +371,14 @@ __device__ __forceinline__ void warp_topk(int n, int kk, Get get, Out out) {
         const int e = e0 + 32 * u;
         c[u] = e < n ? get(e) : Key{-INFINITY, -1, -1};
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (c[u].tok >= 0) L.push(c[u], kk);
+#pragma unroll 1
+      for (int u = 0; u < 8; ++u) {
+        const Key cu = c[u];
+        if (cu.tok >= 0 && key_better(cu.v, cu.tok, cu.par, worst.v, worst.tok, worst.par)) {
+          L.push(cu, kk);
+          worst = L.get(kk - 1);
+        }
+      }
     }
     int h = 0;
     for (int j = 0; j < kk; ++j) {
@@ -304,13 +445,13 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
 #pragma unroll
       for (int u = 0; u < kPT; ++u) mx = fmaxf(mx, pm[u]);
       mx = warp_max(mx);
+      // exp(pm - mx) <= 1 in fp32 (1-ulp expf), products summed in f64
       double s = 0.0;
 #pragma unroll
-      for (int u = 0; u < kPT; ++u)
-        if (ps[u] > 0.f) s += (double)ps[u] * exp((double)pm[u] - (double)mx);
+      for (int u = 0; u < kPT; ++u) s += (double)(ps[u] * expf(pm[u] - mx));
       for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) {
         long long o = (long long)tt * sa.M + r;
-        s += (double)sa.psum[o] * exp((double)sa.pmax[o] - (double)mx);
+        s += (double)(sa.psum[o] * expf(sa.pmax[o] - mx));
       }
       s = warp_sum_d(s);
       const double lse = (double)mx + log(s);
@@ -483,7 +624,9 @@ void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &m
   if (sa.fused) {
     if (need <= 1) launch_select_t<1, true>(sa, bs, mr, smem, st);
     else if (need <= 4) launch_select_t<4, true>(sa, bs, mr, smem, st);
+    else if (need <= 5) launch_select_t<5, true>(sa, bs, mr, smem, st);
     else if (need <= 8) launch_select_t<8, true>(sa, bs, mr, smem, st);
+    else if (need <= 12) launch_select_t<12, true>(sa, bs, mr, smem, st);
     else launch_select_t<16, true>(sa, bs, mr, smem, st);
   } else {
     if (need <= 8) launch_select_t<8, false>(sa, bs, mr, smem, st);

@@ -626,13 +626,52 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     sa.sl_len = d_sl_len;
     sa.cand_lp = cand_lp;
     sa.cand_tok = cand_tok;
-    int steps_run = 0;
-    for (int t = 0; t < capm; ++t) {
+    auto launch_step = [&]() {
       for (int m = 0; m < n_models; ++m)
         step_rows(c, ms[m], db[m], eb[m], d_len, jmax, R, k, bs.n_act, bs.done, nullptr, lo,
                   use_tcg ? &tsteps[m] : nullptr);
-      sa.t = t;
       c.run(AMUN_K_SELECT, [&] { launch_select(sa, bs, mr, st); });
+    };
+    // Every step launches the same kernels with the same arguments (the
+    // select kernel reads each sentence's own step counter), so step 0 runs
+    // eagerly (it also sizes lazily grown workspaces) and the rest replay one
+    // captured CUDA graph: no per-kernel host launch cost inside the loop.
+    const char *no_graph = getenv("AMUN_NO_GRAPH");
+    const bool use_graph = c.prof == 0 && capm > 2 && !(no_graph && no_graph[0] == '1');
+    cudaGraphExec_t gexec = nullptr;
+    int64_t step_launches = 0;
+    struct GraphGuard {
+      cudaGraphExec_t *g;
+      ~GraphGuard() {
+        if (*g) cudaGraphExecDestroy(*g);
+      }
+    } gguard{&gexec};
+    int steps_run = 0;
+    for (int t = 0; t < capm; ++t) {
+      if (use_graph && t == 1) {
+        const int64_t before = c.launches;
+        cudaGraph_t graph = nullptr;
+        AMUN_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+          launch_step();
+        } catch (...) {
+          cudaStreamEndCapture(st, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          throw;
+        }
+        AMUN_CUDA(cudaStreamEndCapture(st, &graph));
+        step_launches = c.launches - before;
+        c.launches = before;
+        cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        AMUN_CUDA(ie);
+      }
+      if (gexec) {
+        AMUN_CUDA(cudaGraphLaunch(gexec, st));
+        c.launches += step_launches;
+      } else {
+        launch_step();
+      }
       ++steps_run;
       if ((t & 7) == 7 && t + 1 < capm) {  // cheap early-exit probe
         d2h(c, h_ndone, bs.n_done, 1);

@@ -124,19 +124,25 @@ __global__ void __launch_bounds__(512) attention_sent_kernel(AttnArgs a) {
     float acc[KA];
 #pragma unroll
     for (int r = 0; r < KA; ++r) acc[r] = 0.f;
-    for (int i0 = lane; i0 < a.da; i0 += 32 * 8) {
-      float p[8];
+    // whole 1024-wide row in one round trip: 32 independent loads per lane,
+    // then a rolled loop over the beam rows (keeps the code small)
+    for (int i0 = lane; i0 < a.da; i0 += 32 * 32) {
+      float p[32];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) p[u] = (i0 + 32 * u < a.da) ? __ldg(pj + i0 + 32 * u) : 0.f;
+      for (int u = 0; u < 32; ++u) p[u] = (i0 + 32 * u < a.da) ? __ldg(pj + i0 + 32 * u) : 0.f;
+#pragma unroll 1
+      for (int r = 0; r < na; ++r) {
+        const float *qr = q + r * a.da;
+        float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + 32 * u;
-        if (i < a.da) {
-          const float vi = vv[i];
-#pragma unroll
-          for (int r = 0; r < KA; ++r)
-            if (r < na) acc[r] = fmaf(vi, tanh_attn(p[u] + q[r * a.da + i]), acc[r]);
+        for (int u = 0; u < 32; u += 2) {
+          const int i = i0 + 32 * u;
+          if (i < a.da) s0 = fmaf(vv[i], tanh_attn(p[u] + qr[i]), s0);
+          if (i + 32 < a.da) s1 = fmaf(vv[i + 32], tanh_attn(p[u + 1] + qr[i + 32]), s1);
         }
+#pragma unroll
+        for (int rr = 0; rr < KA; ++rr)
+          if (rr == r) acc[rr] += s0 + s1;
       }
     }
 #pragma unroll
@@ -177,20 +183,28 @@ __global__ void __launch_bounds__(512) attention_sent_kernel(AttnArgs a) {
     for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int r = 0; r < KA; ++r) acc[u][r] = 0.f;
-    for (int j = 0; j < J; ++j) {
-      const float *hj = Hb + (long long)j * a.dh2;
-      float h[4];
+    // 4 source positions per iteration: 16 independent H loads in flight
+    for (int j0 = 0; j0 < J; j0 += 4) {
+      float h[4][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * blockDim.x;
-        h[u] = c < a.dh2 ? __ldg(hj + c) : 0.f;
+      for (int jj = 0; jj < 4; ++jj) {
+        const float *hj = Hb + (long long)(j0 + jj) * a.dh2;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * blockDim.x;
+          h[jj][u] = (c < a.dh2 && j0 + jj < J) ? __ldg(hj + c) : 0.f;
+        }
       }
 #pragma unroll
-      for (int r = 0; r < KA; ++r) {
-        if (r < na) {
-          const float w = al[r * a.jmax + j];
+      for (int jj = 0; jj < 4; ++jj) {
+        if (j0 + jj >= J) break;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) acc[u][r] = fmaf(w, h[u], acc[u][r]);
+        for (int r = 0; r < KA; ++r) {
+          if (r < na) {
+            const float w = al[r * a.jmax + j0 + jj];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u][r] = fmaf(w, h[jj][u], acc[u][r]);
+          }
         }
       }
     }
@@ -214,7 +228,13 @@ template <int KA>
 static void launch_attention_sent(const AttnArgs &a, int B, cudaStream_t st) {
   const size_t smem = sizeof(float) * ((size_t)(KA + 1) * a.da + (size_t)KA * a.jmax);
   auto kern = attention_sent_kernel<KA>;
-  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static size_t attr_set[64] = {};  // per device: largest smem opted in so far
+  int dev = 0;
+  AMUN_CUDA(cudaGetDevice(&dev));
+  if (smem > 48 * 1024 && (dev >= 64 || attr_set[dev] < smem)) {
+    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (dev < 64) attr_set[dev] = 200 * 1024;
+  }
   kern<<<B, 512, smem, st>>>(a);
   AMUN_CHECK_LAUNCH();
 }
@@ -418,7 +438,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
 
   const int b = blockIdx.x;
   if (bs.done[b]) return;
-  const int t = sa.t;
+  const int t = bs.steps[b];  // this sentence's step index (graph-replay safe: no host-side t)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int na = bs.n_act[b];
   const int kk = sa.kk;

@@ -64,7 +64,7 @@ struct ModelRows {  // per-model decoder row buffers (device arrays of pointers)
 void launch_init_beam(const BeamState &bs, const ModelRows &mr, const float *const *S0, cudaStream_t st);
 
 struct SelectArgs {
-  int t, kk, fused, V;
+  int kk, fused, V;
   // fused-mode inputs (single model): per (row, N-tile) partial lse + top-kk
   const float *pmax, *psum, *cval;
   const int *ctok;

@@ -4,6 +4,8 @@
 // way engine.py:181-221 fans sentences out — but as one device batch.
 #include <algorithm>
 #include <climits>
+#include <deque>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -454,127 +456,204 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   }
   const int Rmax = Bmax * k;
   const int fin_cap = k * cap_all;
+  const int xs = m0->xs_w;
+  const int de = m0->d.d_emb;
 
-  // ---- workspace
-  std::vector<EncBufs> eb(n_models);
-  std::vector<DecBufs> db(n_models);
-  std::vector<float *> fin_states(n_models, nullptr);
-  int *d_ids, *d_len, *d_cap, *d_sl, *d_sl_off, *d_sl_len;
-  float *pmax, *psum, *cval;
-  int *ctok, *cand_tok;
-  double *cand_lp;
-  BeamState bs{};
-  float **p_XS;
-  const float **p_Sn, **p_E, **p_S0, **p_L;
-  float **p_fin, **p_XSh, **p_XSl;
-  std::vector<TcStep> tsteps(n_models);
-  std::vector<size_t> ts_ws(n_models, 0);
-  if (use_tcg)
-    for (int m = 0; m < n_models; ++m) ts_ws[m] = tc_step_ws_floats(ms[m], Rmax, tsteps[m]);
-  DevMem mem;
-  for (int pass = 0; pass < 2; ++pass) {
-    Carver cv;
-    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
-    for (int m = 0; m < n_models; ++m) {
-      carve_enc(cv, eb[m], ms[m], Bmax, jmax_all);
-      carve_dec(cv, db[m], ms[m], Rmax, !fused);
-      if (!use_tc) db[m].T_hi = db[m].T_lo = nullptr;
-      if (use_tcg) {
-        carve_dec_tc(cv, db[m], ms[m], Rmax);
-        tsteps[m].ws = cv.take<float>(ts_ws[m]);
+  // ---- lanes: each lane = stream + workspace + captured step graph and
+  // decodes one length bucket at a time; lanes run concurrently so that
+  // small kernels of one bucket overlap with another bucket's GEMMs (every
+  // bucket is still one batch of <= max_batch sentences).
+  const char *lanes_env = getenv("AMUN_LANES");
+  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 2;
+  if (o.profile) n_lanes = 1;  // per-launch event timing wants one ordered stream
+  n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
+  const char *no_graph = getenv("AMUN_NO_GRAPH");
+  const bool graphs_ok = o.profile == 0 && !(no_graph && no_graph[0] == '1');
+  constexpr int kProbeEvery = 8, kMaxAhead = 16, kProbeSlots = 64;
+
+  struct Lane {
+    cudaStream_t st = nullptr;
+    std::unique_ptr<Ctx> c;
+    DevMem mem;
+    std::vector<EncBufs> eb;
+    std::vector<DecBufs> db;
+    std::vector<float *> fin_states;
+    std::vector<TcStep> tsteps;
+    int *d_ids, *d_len, *d_cap, *d_sl, *d_sl_off, *d_sl_len;
+    float *pmax, *psum, *cval;
+    int *ctok, *cand_tok;
+    double *cand_lp;
+    BeamState bs{};
+    float **p_XS;
+    const float **p_Sn, **p_E, **p_S0, **p_L;
+    float **p_fin, **p_XSh, **p_XSl;
+    LogitTcMaps tc_maps{};
+    int *h_probe = nullptr;  // pinned ring of n_done probes
+    std::vector<cudaEvent_t> probe_ev;
+    std::deque<std::pair<int, int>> pending;  // (step, slot)
+    int probe_next = 0;
+    // current bucket
+    bool active = false, stop = false;
+    int bucket = -1, B = 0, jmax = 0, capm = 0, R = 0, t = 0;
+    ModelRows mr{};
+    LogitOut lo{};
+    SelectArgs sa{};
+    cudaGraphExec_t gexec = nullptr;
+    int64_t step_launches = 0;
+    ~Lane() {
+      if (gexec) cudaGraphExecDestroy(gexec);
+      for (auto e : probe_ev) cudaEventDestroy(e);
+      if (h_probe) cudaFreeHost(h_probe);
+      c.reset();
+      if (mem.p) {  // free on this lane's stream before the stream goes away
+        cudaFreeAsync(mem.p, st);
+        mem.p = nullptr;
       }
-      fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * dh) : nullptr;
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
     }
-    d_ids = cv.take<int>((size_t)Bmax * jmax_all);
-    d_len = cv.take<int>(Bmax);
-    d_cap = cv.take<int>(Bmax);
-    d_sl = cv.take<int>(std::max(sl_max, 1));
-    d_sl_off = cv.take<int>(Bmax);
-    d_sl_len = cv.take<int>(Bmax);
-    pmax = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
-    psum = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
-    cval = cv.take<float>(fused ? (size_t)Rmax * ntiles * kk : 1);
-    ctok = cv.take<int>(fused ? (size_t)Rmax * ntiles * kk : 1);
-    cand_lp = cv.take<double>((size_t)Rmax * kk);
-    cand_tok = cv.take<int>((size_t)Rmax * kk);
-    bs.n_act = cv.take<int>(Bmax);
-    bs.score = cv.take<double>(Rmax);
-    bs.tok = cv.take<int>(Rmax);
-    bs.done = cv.take<int>(Bmax);
-    bs.steps = cv.take<int>(Bmax);
-    bs.cap = d_cap;
-    bs.fin_n = cv.take<int>(Bmax);
-    bs.fin_score = cv.take<double>((size_t)Bmax * fin_cap);
-    bs.fin_t = cv.take<int>((size_t)Bmax * fin_cap);
-    bs.fin_par = cv.take<int>((size_t)Bmax * fin_cap);
-    bs.best_fin = cv.take<double>(Bmax);
-    bs.bp_tok = cv.take<int>((size_t)Bmax * cap_all * k);
-    bs.bp_par = cv.take<int>((size_t)Bmax * cap_all * k);
-    bs.n_done = cv.take<int>(1);
-    p_XS = cv.take<float *>(n_models);
-    p_Sn = cv.take<const float *>(n_models);
-    p_E = cv.take<const float *>(n_models);
-    p_S0 = cv.take<const float *>(n_models);
-    p_L = cv.take<const float *>(n_models);
-    p_fin = cv.take<float *>(n_models);
-    p_XSh = cv.take<float *>(n_models);
-    p_XSl = cv.take<float *>(n_models);
-    if (!pass) mem.alloc(cv.off, m0->stream);
-  }
-  Ctx c(m0->stream);
-  c.prof = (uint32_t)o.profile;
-  LogitTcMaps tc_maps{};
-  if (use_tc) {
-    static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
-    if (logits_tc_tile_n() != kBN) throw Error(AMUN_ERR_UNSUPPORTED, "logit tile width mismatch");
-    tc_maps = make_logit_maps(db[0].T_hi, db[0].T_lo, Rmax, m0->d.d_emb, m0->d.d_emb, m0->Wl_hi, m0->Wl_lo, V);
-  }
-  if (use_tcg)
-    for (int m = 0; m < n_models; ++m) tc_step_maps(ms[m], db[m], Rmax, tsteps[m]);
-  cudaStream_t st = c.st;
-  {
-    std::vector<const void *> hx(n_models), hs(n_models), he(n_models), h0(n_models), hl(n_models), hf(n_models);
-    std::vector<const void *> hxh(n_models), hxl(n_models);
-    for (int m = 0; m < n_models; ++m) {
-      hxh[m] = db[m].XSh;
-      hxl[m] = db[m].XSl;
+  };
+  std::vector<std::unique_ptr<Lane>> lanes;
+  for (int li = 0; li < n_lanes; ++li) {
+    lanes.emplace_back(new Lane());
+    Lane &L = *lanes.back();
+    AMUN_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+    L.c.reset(new Ctx(L.st));
+    L.c->prof = (uint32_t)o.profile;
+    L.eb.resize(n_models);
+    L.db.resize(n_models);
+    L.fin_states.assign(n_models, nullptr);
+    L.tsteps.resize(n_models);
+    std::vector<size_t> ts_ws(n_models, 0);
+    if (use_tcg)
+      for (int m = 0; m < n_models; ++m) ts_ws[m] = tc_step_ws_floats(ms[m], Rmax, L.tsteps[m]);
+    for (int pass = 0; pass < 2; ++pass) {
+      Carver cv;
+      cv.base = pass ? static_cast<char *>(L.mem.p) : nullptr;
+      for (int m = 0; m < n_models; ++m) {
+        carve_enc(cv, L.eb[m], ms[m], Bmax, jmax_all);
+        carve_dec(cv, L.db[m], ms[m], Rmax, !fused);
+        if (!use_tc) L.db[m].T_hi = L.db[m].T_lo = nullptr;
+        if (use_tcg) {
+          carve_dec_tc(cv, L.db[m], ms[m], Rmax);
+          L.tsteps[m].ws = cv.take<float>(ts_ws[m]);
+        }
+        L.fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * dh) : nullptr;
+      }
+      L.d_ids = cv.take<int>((size_t)Bmax * jmax_all);
+      L.d_len = cv.take<int>(Bmax);
+      L.d_cap = cv.take<int>(Bmax);
+      L.d_sl = cv.take<int>(std::max(sl_max, 1));
+      L.d_sl_off = cv.take<int>(Bmax);
+      L.d_sl_len = cv.take<int>(Bmax);
+      L.pmax = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
+      L.psum = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
+      L.cval = cv.take<float>(fused ? (size_t)Rmax * ntiles * kk : 1);
+      L.ctok = cv.take<int>(fused ? (size_t)Rmax * ntiles * kk : 1);
+      L.cand_lp = cv.take<double>((size_t)Rmax * kk);
+      L.cand_tok = cv.take<int>((size_t)Rmax * kk);
+      BeamState &bs = L.bs;
+      bs.n_act = cv.take<int>(Bmax);
+      bs.score = cv.take<double>(Rmax);
+      bs.tok = cv.take<int>(Rmax);
+      bs.done = cv.take<int>(Bmax);
+      bs.steps = cv.take<int>(Bmax);
+      bs.cap = L.d_cap;
+      bs.fin_n = cv.take<int>(Bmax);
+      bs.fin_score = cv.take<double>((size_t)Bmax * fin_cap);
+      bs.fin_t = cv.take<int>((size_t)Bmax * fin_cap);
+      bs.fin_par = cv.take<int>((size_t)Bmax * fin_cap);
+      bs.best_fin = cv.take<double>(Bmax);
+      bs.bp_tok = cv.take<int>((size_t)Bmax * cap_all * k);
+      bs.bp_par = cv.take<int>((size_t)Bmax * cap_all * k);
+      bs.n_done = cv.take<int>(1);
+      L.p_XS = cv.take<float *>(n_models);
+      L.p_Sn = cv.take<const float *>(n_models);
+      L.p_E = cv.take<const float *>(n_models);
+      L.p_S0 = cv.take<const float *>(n_models);
+      L.p_L = cv.take<const float *>(n_models);
+      L.p_fin = cv.take<float *>(n_models);
+      L.p_XSh = cv.take<float *>(n_models);
+      L.p_XSl = cv.take<float *>(n_models);
+      if (!pass) L.mem.alloc(cv.off, L.st);
     }
-    h2d(c, (const void **)p_XSh, hxh.data(), n_models);
-    h2d(c, (const void **)p_XSl, hxl.data(), n_models);
+    if (use_tc) {
+      static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
+      if (logits_tc_tile_n() != kBN) throw Error(AMUN_ERR_UNSUPPORTED, "logit tile width mismatch");
+      L.tc_maps = make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, de, m0->Wl_hi, m0->Wl_lo, V);
+    }
+    if (use_tcg)
+      for (int m = 0; m < n_models; ++m) tc_step_maps(ms[m], L.db[m], Rmax, L.tsteps[m]);
+    std::vector<const void *> hx(n_models), hs(n_models), he(n_models), h0(n_models), hl(n_models), hf(n_models),
+        hxh(n_models), hxl(n_models);
     for (int m = 0; m < n_models; ++m) {
-      hx[m] = db[m].XS;
-      hs[m] = db[m].Sn;
+      hx[m] = L.db[m].XS;
+      hs[m] = L.db[m].Sn;
       he[m] = ms[m]->E_trg;
-      h0[m] = eb[m].S0;
-      hl[m] = db[m].L;
-      hf[m] = fin_states[m];
+      h0[m] = L.eb[m].S0;
+      hl[m] = L.db[m].L;
+      hf[m] = L.fin_states[m];
+      hxh[m] = L.db[m].XSh;
+      hxl[m] = L.db[m].XSl;
     }
-    h2d(c, (const void **)p_XS, hx.data(), n_models);
-    h2d(c, (const void **)p_Sn, hs.data(), n_models);
-    h2d(c, (const void **)p_E, he.data(), n_models);
-    h2d(c, (const void **)p_S0, h0.data(), n_models);
-    h2d(c, (const void **)p_L, hl.data(), n_models);
-    h2d(c, (const void **)p_fin, hf.data(), n_models);
+    Ctx &c = *L.c;
+    h2d(c, (const void **)L.p_XS, hx.data(), n_models);
+    h2d(c, (const void **)L.p_Sn, hs.data(), n_models);
+    h2d(c, (const void **)L.p_E, he.data(), n_models);
+    h2d(c, (const void **)L.p_S0, h0.data(), n_models);
+    h2d(c, (const void **)L.p_L, hl.data(), n_models);
+    h2d(c, (const void **)L.p_fin, hf.data(), n_models);
+    h2d(c, (const void **)L.p_XSh, hxh.data(), n_models);
+    h2d(c, (const void **)L.p_XSl, hxl.data(), n_models);
+    AMUN_CUDA(cudaMallocHost(&L.h_probe, sizeof(int) * kProbeSlots));
+    L.probe_ev.resize(kProbeSlots);
+    for (auto &e : L.probe_ev) AMUN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  int *h_ndone = nullptr;
-  AMUN_CUDA(cudaMallocHost(&h_ndone, sizeof(int)));
-  struct PinnedFree {
-    int *p;
-    ~PinnedFree() { cudaFreeHost(p); }
-  } pf{h_ndone};
 
   cudaEvent_t ev0, ev1;
   AMUN_CUDA(cudaEventCreate(&ev0));
   AMUN_CUDA(cudaEventCreate(&ev1));
-  AMUN_CUDA(cudaEventRecord(ev0, st));
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } evg{ev0, ev1};
+  AMUN_CUDA(cudaEventRecord(ev0, lanes[0]->st));
+  for (int li = 1; li < n_lanes; ++li) AMUN_CUDA(cudaStreamWaitEvent(lanes[li]->st, ev0, 0));
 
   std::vector<std::vector<HostHyp>> out_hyps(n_sent);
   int64_t total_steps = 0;
-  const int xs = m0->xs_w;
-  const int de = m0->d.d_emb;
+  size_t next_bucket = 0;
 
-  for (const Bucket &bk : buckets) {
-    const int B = bk.count, jmax = bk.jmax, capm = bk.cap_max, R = B * k;
+  auto launch_step = [&](Lane &L) {
+    Ctx &c = *L.c;
+    for (int m = 0; m < n_models; ++m)
+      step_rows(c, ms[m], L.db[m], L.eb[m], L.d_len, L.jmax, L.R, k, L.bs.n_act, L.bs.done, nullptr, L.lo,
+                use_tcg ? &L.tsteps[m] : nullptr);
+    c.run(AMUN_K_SELECT, [&] { launch_select(L.sa, L.bs, L.mr, L.st); });
+  };
+
+  auto start_bucket = [&](Lane &L, int bi) {
+    Ctx &c = *L.c;
+    const Bucket &bk = buckets[bi];
+    L.bucket = bi;
+    L.B = bk.count;
+    L.jmax = bk.jmax;
+    L.capm = bk.cap_max;
+    L.R = L.B * k;
+    L.t = 0;
+    L.active = true;
+    L.stop = false;
+    L.pending.clear();
+    if (L.gexec) {
+      cudaGraphExecDestroy(L.gexec);
+      L.gexec = nullptr;
+    }
+    const int B = L.B, jmax = L.jmax;
     std::vector<int> ids((size_t)B * jmax, 0), lens(B), caps(B), slo(B), sll(B), slv;
     for (int i = 0; i < B; ++i) {
       int s = order[bk.first + i];
@@ -587,101 +666,111 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
         slv.insert(slv.end(), sl_ids + sl_offs[s], sl_ids + sl_offs[s + 1]);
       }
     }
-    h2d(c, d_ids, ids.data(), ids.size());
-    h2d(c, d_len, lens.data(), B);
-    h2d(c, d_cap, caps.data(), B);
+    // pageable sources: cudaMemcpyAsync stages them before returning
+    h2d(c, L.d_ids, ids.data(), ids.size());
+    h2d(c, L.d_len, lens.data(), B);
+    h2d(c, L.d_cap, caps.data(), B);
     if (sl_ids) {
-      h2d(c, d_sl, slv.data(), slv.size());
-      h2d(c, d_sl_off, slo.data(), B);
-      h2d(c, d_sl_len, sll.data(), B);
+      h2d(c, L.d_sl, slv.data(), slv.size());
+      h2d(c, L.d_sl_off, slo.data(), B);
+      h2d(c, L.d_sl_len, sll.data(), B);
     }
-    for (int m = 0; m < n_models; ++m) encode_bucket(c, ms[m], eb[m], d_ids, d_len, B, jmax);
-
-    bs.B = B;
-    bs.k = k;
-    bs.cap_max = capm;
-    bs.fin_cap = fin_cap;
-    ModelRows mr{p_XS, p_Sn, p_E, o.want_states ? p_fin : nullptr, xs, de, dh, de + 2 * dh, n_models};
+    for (int m = 0; m < n_models; ++m) encode_bucket(c, ms[m], L.eb[m], L.d_ids, L.d_len, B, jmax);
+    L.bs.B = B;
+    L.bs.k = k;
+    L.bs.cap_max = L.capm;
+    L.bs.fin_cap = fin_cap;
+    L.mr = ModelRows{L.p_XS, L.p_Sn, L.p_E, o.want_states ? L.p_fin : nullptr, xs, de, dh, de + 2 * dh, n_models};
     if (use_tcg) {
-      mr.XSh = p_XSh;
-      mr.XSl = p_XSl;
+      L.mr.XSh = L.p_XSh;
+      L.mr.XSl = L.p_XSl;
     }
-    c.run(AMUN_K_SELECT, [&] { launch_init_beam(bs, mr, p_S0, st); });
-    LogitOut lo{fused, kk, ntiles, pmax, psum, cval, ctok};
-    if (use_tc) lo.tc = &tc_maps;
-    SelectArgs sa{};
+    c.run(AMUN_K_SELECT, [&] { launch_init_beam(L.bs, L.mr, L.p_S0, L.st); });
+    L.lo = LogitOut{fused, kk, ntiles, L.pmax, L.psum, L.cval, L.ctok};
+    if (use_tc) L.lo.tc = &L.tc_maps;
+    SelectArgs &sa = L.sa;
+    sa = SelectArgs{};
     sa.kk = kk;
     sa.fused = fused;
     sa.V = V;
-    sa.pmax = pmax;
-    sa.psum = psum;
-    sa.cval = cval;
-    sa.ctok = ctok;
+    sa.pmax = L.pmax;
+    sa.psum = L.psum;
+    sa.cval = L.cval;
+    sa.ctok = L.ctok;
     sa.ntiles = ntiles;
-    sa.M = R;
-    sa.L = p_L;
+    sa.M = L.R;
+    sa.L = L.p_L;
     sa.ldl = V;
-    sa.sl_ids = sl_ids ? d_sl : nullptr;
-    sa.sl_off = d_sl_off;
-    sa.sl_len = d_sl_len;
-    sa.cand_lp = cand_lp;
-    sa.cand_tok = cand_tok;
-    auto launch_step = [&]() {
-      for (int m = 0; m < n_models; ++m)
-        step_rows(c, ms[m], db[m], eb[m], d_len, jmax, R, k, bs.n_act, bs.done, nullptr, lo,
-                  use_tcg ? &tsteps[m] : nullptr);
-      c.run(AMUN_K_SELECT, [&] { launch_select(sa, bs, mr, st); });
-    };
-    // Every step launches the same kernels with the same arguments (the
-    // select kernel reads each sentence's own step counter), so step 0 runs
-    // eagerly (it also sizes lazily grown workspaces) and the rest replay one
-    // captured CUDA graph: no per-kernel host launch cost inside the loop.
-    const char *no_graph = getenv("AMUN_NO_GRAPH");
-    const bool use_graph = c.prof == 0 && capm > 2 && !(no_graph && no_graph[0] == '1');
-    cudaGraphExec_t gexec = nullptr;
-    int64_t step_launches = 0;
-    struct GraphGuard {
-      cudaGraphExec_t *g;
-      ~GraphGuard() {
-        if (*g) cudaGraphExecDestroy(*g);
-      }
-    } gguard{&gexec};
-    int steps_run = 0;
-    for (int t = 0; t < capm; ++t) {
-      if (use_graph && t == 1) {
-        const int64_t before = c.launches;
-        cudaGraph_t graph = nullptr;
-        AMUN_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        try {
-          launch_step();
-        } catch (...) {
-          cudaStreamEndCapture(st, &graph);
-          if (graph) cudaGraphDestroy(graph);
-          throw;
-        }
-        AMUN_CUDA(cudaStreamEndCapture(st, &graph));
-        step_launches = c.launches - before;
-        c.launches = before;
-        cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
-        cudaGraphDestroy(graph);
-        AMUN_CUDA(ie);
-      }
-      if (gexec) {
-        AMUN_CUDA(cudaGraphLaunch(gexec, st));
-        c.launches += step_launches;
-      } else {
-        launch_step();
-      }
-      ++steps_run;
-      if ((t & 7) == 7 && t + 1 < capm) {  // cheap early-exit probe
-        d2h(c, h_ndone, bs.n_done, 1);
-        AMUN_CUDA(cudaStreamSynchronize(st));
-        if (*h_ndone >= B) break;
-      }
-    }
-    total_steps += steps_run;
+    sa.sl_ids = sl_ids ? L.d_sl : nullptr;
+    sa.sl_off = L.d_sl_off;
+    sa.sl_len = L.d_sl_len;
+    sa.cand_lp = L.cand_lp;
+    sa.cand_tok = L.cand_tok;
+  };
 
-    // ---- read back beam state and walk back-pointers (search.py:200-216)
+  // Enqueue one decoder step.  Step 0 runs eagerly (it also sizes lazily
+  // grown workspaces); step 1 is captured as a CUDA graph that every later
+  // step replays (identical launches: select reads each sentence's own step
+  // counter).  Every kProbeEvery steps an async copy of the done-count is
+  // queued; the host never runs more than kMaxAhead steps past the newest
+  // probe it has read, so a bucket whose sentences all stopped early ends
+  // without decoding to the cap.
+  auto enqueue_step = [&](Lane &L) {
+    Ctx &c = *L.c;
+    if (graphs_ok && L.capm > 2 && L.t == 1 && !L.gexec) {
+      const int64_t before = c.launches;
+      cudaGraph_t graph = nullptr;
+      AMUN_CUDA(cudaStreamBeginCapture(L.st, cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_step(L);
+      } catch (...) {
+        cudaStreamEndCapture(L.st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      AMUN_CUDA(cudaStreamEndCapture(L.st, &graph));
+      L.step_launches = c.launches - before;
+      c.launches = before;
+      cudaError_t ie = cudaGraphInstantiate(&L.gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      AMUN_CUDA(ie);
+    }
+    if (L.gexec) {
+      AMUN_CUDA(cudaGraphLaunch(L.gexec, L.st));
+      c.launches += L.step_launches;
+    } else {
+      launch_step(L);
+    }
+    ++L.t;
+    ++total_steps;
+    if (L.t % kProbeEvery == 0 && L.t < L.capm) {
+      const int slot = L.probe_next++ % kProbeSlots;
+      d2h(c, L.h_probe + slot, L.bs.n_done, 1);
+      AMUN_CUDA(cudaEventRecord(L.probe_ev[slot], L.st));
+      L.pending.emplace_back(L.t, slot);
+    }
+  };
+
+  // read probes; `block` waits for the oldest one
+  auto poll = [&](Lane &L, bool block) {
+    while (!L.pending.empty()) {
+      auto [step, slot] = L.pending.front();
+      if (block) {
+        AMUN_CUDA(cudaEventSynchronize(L.probe_ev[slot]));
+        block = false;
+      } else if (cudaEventQuery(L.probe_ev[slot]) != cudaSuccess) {
+        break;
+      }
+      L.pending.pop_front();
+      if (L.h_probe[slot] >= L.B) L.stop = true;
+    }
+  };
+
+  auto finish_bucket = [&](Lane &L) {
+    Ctx &c = *L.c;
+    const Bucket &bk = buckets[L.bucket];
+    const int B = L.B, capm = L.capm, R = L.R;
+    BeamState &bs = L.bs;
     std::vector<int> n_act(B), steps(B), fin_n(B), fin_t((size_t)B * fin_cap), fin_par((size_t)B * fin_cap);
     std::vector<int> bp_tok((size_t)B * capm * k), bp_par((size_t)B * capm * k);
     std::vector<double> score(R), fin_score((size_t)B * fin_cap);
@@ -700,13 +789,15 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       fin_st.resize((size_t)n_models * B * fin_cap * dh);
       for (int m = 0; m < n_models; ++m) {
         AMUN_CUDA(cudaMemcpy2DAsync(act_states.data() + (size_t)m * R * dh, dh * sizeof(float),
-                                    db[m].XS + de + 2 * dh, xs * sizeof(float), dh * sizeof(float), R,
-                                    cudaMemcpyDeviceToHost, st));
-        d2h(c, fin_st.data() + (size_t)m * B * fin_cap * dh, fin_states[m], (size_t)B * fin_cap * dh);
+                                    L.db[m].XS + de + 2 * dh, xs * sizeof(float), dh * sizeof(float), R,
+                                    cudaMemcpyDeviceToHost, L.st));
+        d2h(c, fin_st.data() + (size_t)m * B * fin_cap * dh, L.fin_states[m], (size_t)B * fin_cap * dh);
       }
     }
-    AMUN_CUDA(cudaStreamSynchronize(st));
+    AMUN_CUDA(cudaStreamSynchronize(L.st));
     c.collect();
+    L.pending.clear();
+    L.active = false;
     auto walk = [&](int i, int tt, int slot) {
       std::vector<int> seq;
       for (; tt >= 0; --tt) {
@@ -754,13 +845,50 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       if ((int)hyps.size() > o.n_best) hyps.resize(o.n_best);
       out_hyps[s] = std::move(hyps);
     }
+  };
+
+  for (auto &Lp : lanes)
+    if (next_bucket < buckets.size()) start_bucket(*Lp, (int)next_bucket++);
+  for (;;) {
+    bool any = false;
+    for (auto &Lp : lanes) {
+      Lane &L = *Lp;
+      if (!L.active) continue;
+      any = true;
+      poll(L, false);
+      if (L.stop || L.t >= L.capm) {
+        finish_bucket(L);
+        if (next_bucket < buckets.size()) start_bucket(L, (int)next_bucket++);
+        continue;
+      }
+      // bounded run-ahead past the newest probe the host has seen
+      if (!L.pending.empty() && L.t - L.pending.front().first >= kMaxAhead) {
+        poll(L, true);
+        if (L.stop) continue;
+      }
+      enqueue_step(L);
+    }
+    if (!any) break;
   }
-  AMUN_CUDA(cudaEventRecord(ev1, st));
+
+  for (int li = 1; li < n_lanes; ++li) {
+    AMUN_CUDA(cudaEventRecord(lanes[li]->probe_ev[0], lanes[li]->st));
+    AMUN_CUDA(cudaStreamWaitEvent(lanes[0]->st, lanes[li]->probe_ev[0], 0));
+  }
+  AMUN_CUDA(cudaEventRecord(ev1, lanes[0]->st));
   AMUN_CUDA(cudaEventSynchronize(ev1));
   float ms_elapsed = 0.f;
   AMUN_CUDA(cudaEventElapsedTime(&ms_elapsed, ev0, ev1));
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
+  Ctx c(nullptr);  // totals over lanes
+  for (auto &Lp : lanes) {
+    c.launches += Lp->c->launches;
+    c.h2d += Lp->c->h2d;
+    c.d2h += Lp->c->d2h;
+    for (int i = 0; i < AMUN_K_CLASSES; ++i) {
+      c.kms[i] += Lp->c->kms[i];
+      c.kcount[i] += Lp->c->kcount[i];
+    }
+  }
 
   // ---- assemble the flat result
   amun_result *r = static_cast<amun_result *>(calloc(1, sizeof(amun_result)));

@@ -240,7 +240,14 @@ struct TcStep {
   float *ws = nullptr;
 };
 
-constexpr int kTcTargetCtas = 128;
+// target CTAs per split-K tensor-core GEMM launch (env AMUN_TC_CTAS overrides)
+int tc_target_ctas() {
+  static int v = [] {
+    const char *e = getenv("AMUN_TC_CTAS");
+    return e ? std::max(8, atoi(e)) : 128;
+  }();
+  return v;
+}
 
 size_t tc_step_ws_floats(const amun_model *m, int R, TcStep &ts_splits) {
   // split counts only depend on shapes; computed here to size the workspace
@@ -250,7 +257,7 @@ size_t tc_step_ws_floats(const amun_model *m, int R, TcStep &ts_splits) {
     mm.N = N;
     mm.k1 = k1;
     mm.k2 = k2;
-    return gemm_tc_splits(mm, kTcTargetCtas);
+    return gemm_tc_splits(mm, tc_target_ctas());
   };
   ts_splits.sq = splits(da, dh, 0);
   ts_splits.sg = splits(3 * dh, xs, 0);
@@ -464,7 +471,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // small kernels of one bucket overlap with another bucket's GEMMs (every
   // bucket is still one batch of <= max_batch sentences).
   const char *lanes_env = getenv("AMUN_LANES");
-  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 2;
+  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 4;
   if (o.profile) n_lanes = 1;  // per-launch event timing wants one ordered stream
   n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
   const char *no_graph = getenv("AMUN_NO_GRAPH");

@@ -244,7 +244,7 @@ struct TcStep {
 int tc_target_ctas() {
   static int v = [] {
     const char *e = getenv("AMUN_TC_CTAS");
-    return e ? std::max(8, atoi(e)) : 128;
+    return e ? std::max(8, atoi(e)) : 32;
   }();
   return v;
 }
@@ -471,7 +471,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // small kernels of one bucket overlap with another bucket's GEMMs (every
   // bucket is still one batch of <= max_batch sentences).
   const char *lanes_env = getenv("AMUN_LANES");
-  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 4;
+  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 6;
   if (o.profile) n_lanes = 1;  // per-launch event timing wants one ordered stream
   n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
   const char *no_graph = getenv("AMUN_NO_GRAPH");

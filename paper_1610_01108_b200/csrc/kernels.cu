@@ -1,4 +1,6 @@
 // Non-GEMM kernels of the decode path (see kernels.cuh).
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace amun {
@@ -224,6 +226,156 @@ __global__ void __launch_bounds__(512) attention_sent_kernel(AttnArgs a) {
   }
 }
 
+// Cluster version: a 4-CTA cluster per sentence.  CTA q computes the
+// energies of positions j = q, q+4, ... for every beam row and writes them
+// into all four CTAs' shared memory (DSMEM); after a cluster barrier each CTA
+// normalises the (tiny) softmax locally and computes the context for its
+// quarter of the 2 d_h columns.  4x the SMs of one-CTA-per-sentence at the
+// same total work.
+constexpr int kAttnCluster = 4;
+
+template <int KA>
+__global__ void __cluster_dims__(kAttnCluster, 1, 1) __launch_bounds__(256)
+    attention_cluster_kernel(AttnArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ float sm[];
+  const int k = a.rows_per_sent;
+  const int q4 = (int)cluster.block_rank();
+  const int b = blockIdx.x / kAttnCluster;
+  if (a.n_act && a.done[b]) return;  // uniform over the cluster
+  const int na = a.n_act ? a.n_act[b] : k;
+  const int J = a.len[b];
+  float *q = sm;                  // [KA][da]
+  float *vv = q + KA * a.da;      // [da]
+  float *al = vv + a.da;          // [KA][jmax]
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
+  for (int i = tid; i < na * a.da; i += blockDim.x) {
+    const int r = i / a.da, c = i % a.da;
+    q[i] = a.Q[(long long)(b * k + r) * a.ldq + c];
+  }
+  for (int i = tid; i < a.da; i += blockDim.x) vv[i] = a.v[i];
+  __syncthreads();
+  float *al_rank[kAttnCluster];
+#pragma unroll
+  for (int c = 0; c < kAttnCluster; ++c) al_rank[c] = cluster.map_shared_rank(al, c);
+  const float *Pb = a.P + (long long)b * a.jmax * a.da;
+  for (int j = q4 + kAttnCluster * warp; j < J; j += kAttnCluster * nw) {
+    const float *pj = Pb + (long long)j * a.da;
+    float acc[KA];
+#pragma unroll
+    for (int r = 0; r < KA; ++r) acc[r] = 0.f;
+    for (int i0 = lane; i0 < a.da; i0 += 32 * 32) {
+      float p[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) p[u] = (i0 + 32 * u < a.da) ? __ldg(pj + i0 + 32 * u) : 0.f;
+#pragma unroll 1
+      for (int r = 0; r < na; ++r) {
+        const float *qr = q + r * a.da;
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int u = 0; u < 32; u += 2) {
+          const int i = i0 + 32 * u;
+          if (i < a.da) s0 = fmaf(vv[i], tanh_attn(p[u] + qr[i]), s0);
+          if (i + 32 < a.da) s1 = fmaf(vv[i + 32], tanh_attn(p[u + 1] + qr[i + 32]), s1);
+        }
+#pragma unroll
+        for (int rr = 0; rr < KA; ++rr)
+          if (rr == r) acc[rr] += s0 + s1;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < KA; ++r) {
+      if (r < na) {
+        const float s = warp_sum(acc[r]);
+        if (lane < kAttnCluster) al_rank[lane][r * a.jmax + j] = s;  // broadcast to the cluster
+      }
+    }
+  }
+  cluster.sync();  // all energies visible in every CTA's shared memory
+  for (int r = warp; r < na; r += nw) {
+    float *e = al + r * a.jmax;
+    float mx = -INFINITY;
+    for (int j = lane; j < J; j += 32) mx = fmaxf(mx, e[j]);
+    mx = warp_max(mx);
+    float s = 0.f;
+    for (int j = lane; j < J; j += 32) {
+      const float w = expf(e[j] - mx);
+      e[j] = w;
+      s += w;
+    }
+    s = warp_sum(s);
+    const float inv = 1.0f / s;
+    for (int j = lane; j < J; j += 32) {
+      const float w = e[j] * inv;
+      e[j] = w;
+      if (a.alpha && q4 == 0) a.alpha[(long long)(b * k + r) * a.jmax + j] = w;
+    }
+  }
+  __syncthreads();
+  // context for this CTA's quarter of the columns: thread = 2 columns x KA rows
+  const int cw = (a.dh2 + kAttnCluster - 1) / kAttnCluster;
+  const int cbeg = q4 * cw, cend = min(a.dh2, cbeg + cw);
+  const float *Hb = a.H + (long long)b * a.jmax * a.dh2;
+  for (int c0 = cbeg + tid; c0 < cend; c0 += 2 * blockDim.x) {
+    float acc[2][KA];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int r = 0; r < KA; ++r) acc[u][r] = 0.f;
+    for (int j0 = 0; j0 < J; j0 += 8) {
+      float h[8][2];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = c0 + u * blockDim.x;
+          h[jj][u] = (c < cend && j0 + jj < J) ? __ldg(Hb + (long long)(j0 + jj) * a.dh2 + c) : 0.f;
+        }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        if (j0 + jj >= J) break;
+#pragma unroll
+        for (int r = 0; r < KA; ++r) {
+          if (r < na) {
+            const float w = al[r * a.jmax + j0 + jj];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) acc[u][r] = fmaf(w, h[jj][u], acc[u][r]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < KA; ++r) {
+      if (r >= na) continue;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c < cend) {
+          const long long o = (long long)(b * k + r) * a.ldctx + c;
+          a.ctx[o] = acc[u][r];
+          store_split(a.ctx_hi, a.ctx_lo, o, acc[u][r]);
+        }
+      }
+    }
+  }
+}
+
+template <int KA>
+static void launch_attention_cluster(const AttnArgs &a, int B, cudaStream_t st) {
+  const size_t smem = sizeof(float) * ((size_t)(KA + 1) * a.da + (size_t)KA * a.jmax);
+  auto kern = attention_cluster_kernel<KA>;
+  static size_t attr_set[64] = {};
+  int dev = 0;
+  AMUN_CUDA(cudaGetDevice(&dev));
+  if (smem > 48 * 1024 && (dev >= 64 || attr_set[dev] < smem)) {
+    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (dev < 64) attr_set[dev] = 200 * 1024;
+  }
+  kern<<<B * kAttnCluster, 256, smem, st>>>(a);
+  AMUN_CHECK_LAUNCH();
+}
+
 template <int KA>
 static void launch_attention_sent(const AttnArgs &a, int B, cudaStream_t st) {
   const size_t smem = sizeof(float) * ((size_t)(KA + 1) * a.da + (size_t)KA * a.jmax);
@@ -243,11 +395,22 @@ void launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   if (R <= 0) return;
   const int k = a.rows_per_sent;
   const size_t smem_sent = sizeof(float) * ((size_t)(k + 1) * a.da + (size_t)k * a.jmax);
+  static const bool sent_only = [] {
+    const char *e = getenv("AMUN_ATTN_SENT");
+    return e && e[0] == '1';
+  }();
   if (k <= 16 && R % k == 0 && smem_sent <= 200 * 1024) {
-    if (k == 1) launch_attention_sent<1>(a, R / k, st);
-    else if (k <= 4) launch_attention_sent<4>(a, R / k, st);
-    else if (k <= 8) launch_attention_sent<8>(a, R / k, st);
-    else launch_attention_sent<16>(a, R / k, st);
+    if (sent_only) {
+      if (k == 1) launch_attention_sent<1>(a, R / k, st);
+      else if (k <= 4) launch_attention_sent<4>(a, R / k, st);
+      else if (k <= 8) launch_attention_sent<8>(a, R / k, st);
+      else launch_attention_sent<16>(a, R / k, st);
+    } else {
+      if (k == 1) launch_attention_cluster<1>(a, R / k, st);
+      else if (k <= 4) launch_attention_cluster<4>(a, R / k, st);
+      else if (k <= 8) launch_attention_cluster<8>(a, R / k, st);
+      else launch_attention_cluster<16>(a, R / k, st);
+    }
     return;
   }
   size_t smem = sizeof(float) * (2 * a.da + a.jmax);
@@ -367,6 +530,19 @@ struct LaneList {
   }
 };
 
+// kk best keys of the union of the warp's lane lists, in order; out(j, key)
+// is called by every lane with the warp-uniform j-th key.
+template <int KMAX, class Out>
+__device__ __forceinline__ void warp_merge(const LaneList<KMAX> &L, int kk, Out out) {
+  int h = 0;
+  for (int j = 0; j < kk; ++j) {
+    Key mine = L.get(h);
+    Key best = warp_best(mine);
+    if (best.tok != kNoTok && mine.tok == best.tok && mine.par == best.par) ++h;
+    out(j, best);
+  }
+}
+
 // Warp-cooperative exact top-kk of candidates get(0..n-1) (entries with
 // tok < 0 are skipped) in (value desc, tok asc, par asc) order; out(j, key)
 // is called by every lane with the warp-uniform j-th key (tok == kNoTok when
@@ -478,16 +654,75 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       const int n = sa.ntiles * kk;
       const float *cv = sa.cval + (long long)r * n;
       const int *ct = sa.ctok + (long long)r * n;
-      // ordering by raw logit == ordering by logit - lse within a row
-      warp_topk<KMAX>(
-          n, kk, [&](int e) { return Key{(double)cv[e], ct[e], 0}; },
-          [&](int j, const Key &bk) {
-            if (lane == 0) {
-              bool none = bk.tok == kNoTok;
-              out_lp[j] = none ? -INFINITY : bk.v - lse;
-              out_tok[j] = none ? -1 : bk.tok;
+      auto emit = [&](int j, const Key &bk) {
+        if (lane == 0) {
+          bool none = bk.tok == kNoTok;
+          out_lp[j] = none ? -INFINITY : bk.v - lse;  // ordering by logit == by logit - lse
+          out_tok[j] = none ? -1 : bk.tok;
+        }
+      };
+      if constexpr (KMAX > 0) {
+        if (sa.ntiles <= 32 * kPT) {
+          // Threshold filter: every tile list is sorted best-first, so the
+          // kk-th best tile maximum (thr) is a lower bound on the row's kk-th
+          // best logit; only tile prefixes >= thr can hold the row's top-kk.
+          float tmax[kPT];
+#pragma unroll
+          for (int u = 0; u < kPT; ++u) {
+            const int tt = lane + 32 * u;
+            tmax[u] = tt < sa.ntiles ? cv[tt * kk] : -INFINITY;
+          }
+          float lv = INFINITY;
+          int lt = -1;
+          for (int p = 0; p < kk; ++p) {
+            float bv = -INFINITY;
+            int bt = 0x7fffffff;
+#pragma unroll
+            for (int u = 0; u < kPT; ++u) {
+              const int tt = lane + 32 * u;
+              const float x = tmax[u];
+              const bool below = (x < lv) || (x == lv && tt > lt);
+              if (below && (x > bv || (x == bv && tt < bt))) {
+                bv = x;
+                bt = tt;
+              }
             }
-          });
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+              const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+              if (ov > bv || (ov == bv && ot < bt)) {
+                bv = ov;
+                bt = ot;
+              }
+            }
+            lv = bv;
+            lt = bt;
+          }
+          const float thr = lv;  // -inf when fewer than kk tiles have candidates
+          LaneList<KMAX> L;
+          L.init();
+          unsigned scan = 0;  // tiles of this lane whose maximum reaches thr
+#pragma unroll
+          for (int u = 0; u < kPT; ++u)
+            if (lane + 32 * u < sa.ntiles && tmax[u] >= thr) scan |= 1u << u;
+#pragma unroll 1
+          for (; scan; scan &= scan - 1) {  // rolled: keeps the kernel small
+            const int tt = lane + 32 * (__ffs(scan) - 1);
+            for (int j = 0; j < kk; ++j) {
+              const float x = cv[tt * kk + j];
+              const int tok = ct[tt * kk + j];
+              if (tok < 0 || x < thr) break;
+              L.push(Key{(double)x, tok, 0}, kk);
+            }
+          }
+          warp_merge<KMAX>(L, kk, emit);
+        } else {
+          warp_topk<KMAX>(n, kk, [&](int e) { return Key{(double)cv[e], ct[e], 0}; }, emit);
+        }
+      } else {
+        warp_topk<KMAX>(n, kk, [&](int e) { return Key{(double)cv[e], ct[e], 0}; }, emit);
+      }
     } else {
       const int *ids = sa.sl_ids ? sa.sl_ids + sa.sl_off[b] : nullptr;
       const int ncols = sa.sl_ids ? sa.sl_len[b] : sa.V;

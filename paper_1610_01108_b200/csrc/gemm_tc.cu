@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(64 + 128 * MB, 1)
   }
 }
 
-constexpr int kBN = 128, kMB = 3, kStages = 3, kCS = 2;
+constexpr int kBN = 128, kMB = 3, kCS = 2;
 
 }  // namespace
 
@@ -219,7 +219,22 @@ int gemm_tc_splits(const GemmTcMaps &maps, int target_ctas) {
   return ceil_div(nk, kps);
 }
 
+template <int kStages>
+void launch_partial_s(const GemmTcMaps &maps, int M, int splits, float *out, cudaStream_t st);
+
 void launch_gemm_tc_partial(const GemmTcMaps &maps, int M, int splits, float *out, cudaStream_t st) {
+  static int stages = [] {
+    const char *e = getenv("AMUN_TC_STAGES");
+    return (e && e[0] == '2') ? 2 : 3;
+  }();
+  if (stages == 2)
+    launch_partial_s<2>(maps, M, splits, out, st);
+  else
+    launch_partial_s<3>(maps, M, splits, out, st);
+}
+
+template <int kStages>
+void launch_partial_s(const GemmTcMaps &maps, int M, int splits, float *out, cudaStream_t st) {
   GemmTcArgs a{};
   a.M = M;
   a.N = maps.N;

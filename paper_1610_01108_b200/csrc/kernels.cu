@@ -395,9 +395,9 @@ void launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   if (R <= 0) return;
   const int k = a.rows_per_sent;
   const size_t smem_sent = sizeof(float) * ((size_t)(k + 1) * a.da + (size_t)k * a.jmax);
-  static const bool sent_only = [] {
-    const char *e = getenv("AMUN_ATTN_SENT");
-    return e && e[0] == '1';
+  static const bool sent_only = [] {  // AMUN_ATTN_CLUSTER=1: 4-CTA cluster kernel
+    const char *e = getenv("AMUN_ATTN_CLUSTER");
+    return !(e && e[0] == '1');
   }();
   if (k <= 16 && R % k == 0 && smem_sent <= 200 * 1024) {
     if (sent_only) {

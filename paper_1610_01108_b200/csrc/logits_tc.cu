@@ -261,10 +261,20 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-constexpr int kTcBN = 128, kTcMB = 3, kTcStages = 3, kTcCluster = 2;
+constexpr int kTcBN = 128, kTcMB = 3, kTcCluster = 2;
 
-template <int KK>
-void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
+// pipeline depth (env AMUN_TC_STAGES=2 trades latency hiding for 64 KB of
+// shared memory that concurrent kernels of other lanes can use)
+int tc_stages() {
+  static int v = [] {
+    const char *e = getenv("AMUN_TC_STAGES");
+    return (e && e[0] == '2') ? 2 : 3;
+  }();
+  return v;
+}
+
+template <int KK, int kTcStages>
+void launch_t_s(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
   auto kern = logits_tc_kernel<kTcBN, kTcMB, kTcStages, KK, kTcCluster>;
   constexpr int stage = 2 * kTcMB * 128 * kBK * 4 + 2 * kTcBN * kBK * 4;
   const int smem = kTcStages * stage + 1024 + 256 + kTcBN * 4;
@@ -316,6 +326,14 @@ LogitTcMaps make_logit_maps(const float *t_hi, const float *t_lo, int R, int K, 
   m.b_hi = make_tma_2d_f32(w_hi, K, V, K, kBK, kTcBN);
   m.b_lo = make_tma_2d_f32(w_lo, K, V, K, kBK, kTcBN);
   return m;
+}
+
+template <int KK>
+void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
+  if (tc_stages() == 2)
+    launch_t_s<KK, 2>(maps, a, st);
+  else
+    launch_t_s<KK, 3>(maps, a, st);
 }
 
 void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {

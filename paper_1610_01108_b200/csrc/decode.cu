@@ -15,7 +15,7 @@
 #include "decode.cuh"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
-#include "gemm_tc.cuh"
+#include "gemm_sk.cuh"
 #include "logits_tc.cuh"
 
 namespace amun {
@@ -149,6 +149,7 @@ struct EncBufs {
 // Decoder row buffers of one model for R hypothesis rows.
 struct DecBufs {
   float *XS, *Sn, *Q, *Z, *RH, *XH, *T, *L;
+  float *En = nullptr;  // attention energies [R][jmax]
   float *T_hi = nullptr, *T_lo = nullptr;  // 3xTF32 split of t (tensor-core logits)
   // 3xTF32 splits of the tensor-core GEMM A operands
   float *XSh = nullptr, *XSl = nullptr, *RHh = nullptr, *RHl = nullptr, *Snh = nullptr, *Snl = nullptr;
@@ -166,8 +167,9 @@ void carve_enc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
   e.S0 = cv.take<float>((size_t)B * dh);
 }
 
-void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, bool full_logits) {
+void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, int jmax, bool full_logits) {
   const int dh = m->d.d_h, da = m->d.d_att, de = m->d.d_emb;
+  d.En = cv.take<float>((size_t)R * jmax);
   d.XS = cv.take<float>((size_t)R * m->xs_w);
   d.Sn = cv.take<float>((size_t)R * dh);
   d.Q = cv.take<float>((size_t)R * da);
@@ -231,66 +233,42 @@ struct LogitOut {
   const LogitTcMaps *tc = nullptr;  // tensor-core path when set
 };
 
-// Tensor-core (3xTF32, split-K) versions of the four decoder-step GEMMs of
-// one model: tensor maps over the hi/lo row buffers, split counts fixed by
-// (N, K) only, and the partial-sum workspace.
+// Tensor-core (3xTF32, swap-AB cluster split-K, gemm_sk.cuh) versions of the
+// four decoder-step GEMMs of one model: tensor maps over the hi/lo row
+// buffers and split counts fixed by (N, K) only.
 struct TcStep {
-  GemmTcMaps q, g, u, o;
+  SkMaps q, g, u, o;
   int sq = 1, sg = 1, su = 1, so = 1;
-  float *ws = nullptr;
 };
 
-// target CTAs per split-K tensor-core GEMM launch (env AMUN_TC_CTAS overrides)
+// target CTAs per decoder-step GEMM launch (env AMUN_TC_CTAS overrides)
 int tc_target_ctas() {
   static int v = [] {
     const char *e = getenv("AMUN_TC_CTAS");
-    return e ? std::max(8, atoi(e)) : 32;
+    return e ? std::max(1, atoi(e)) : 148;  // AMUN_TC_CTAS: cap on CTAs per launch
   }();
   return v;
-}
-
-size_t tc_step_ws_floats(const amun_model *m, int R, TcStep &ts_splits) {
-  // split counts only depend on shapes; computed here to size the workspace
-  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, xs = m->xs_w;
-  auto splits = [&](int N, int k1, int k2) {
-    GemmTcMaps mm{};
-    mm.N = N;
-    mm.k1 = k1;
-    mm.k2 = k2;
-    return gemm_tc_splits(mm, tc_target_ctas());
-  };
-  ts_splits.sq = splits(da, dh, 0);
-  ts_splits.sg = splits(3 * dh, xs, 0);
-  ts_splits.su = splits(dh, dh, 0);
-  ts_splits.so = splits(de, de + 2 * dh, dh);
-  size_t w = 0;
-  w = std::max(w, (size_t)ts_splits.sq * R * da);
-  w = std::max(w, (size_t)ts_splits.sg * R * 3 * dh);
-  w = std::max(w, (size_t)ts_splits.su * R * dh);
-  w = std::max(w, (size_t)ts_splits.so * R * de);
-  return w;
 }
 
 void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, xs = m->xs_w;
   const int s_off = de + 2 * dh;
-  ts.q = make_gemm_tc_maps(d.XSh + s_off, d.XSl + s_off, dh, xs, nullptr, nullptr, 0, 0, Rmax, m->Wq_hi, m->Wq_lo,
-                           da, dh);
-  ts.g = make_gemm_tc_maps(d.XSh, d.XSl, xs, xs, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi, m->Wg_lo, 3 * dh, xs);
-  ts.u = make_gemm_tc_maps(d.RHh, d.RHl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Uhd_hi, m->Uhd_lo, dh, dh);
-  ts.o = make_gemm_tc_maps(d.XSh, d.XSl, de + 2 * dh, xs, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi, m->Wo_lo, de, xs);
+  ts.q = make_sk_maps(d.XSh + s_off, d.XSl + s_off, dh, xs, nullptr, nullptr, 0, 0, Rmax, m->Wq_hi, m->Wq_lo, da,
+                      dh);
+  ts.g = make_sk_maps(d.XSh, d.XSl, xs, xs, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi, m->Wg_lo, 3 * dh, xs);
+  ts.u = make_sk_maps(d.RHh, d.RHl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Uhd_hi, m->Uhd_lo, dh, dh);
+  ts.o = make_sk_maps(d.XSh, d.XSl, de + 2 * dh, xs, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi, m->Wo_lo, de, xs);
+  const int t = tc_target_ctas();
+  ts.sq = sk_fit_splits(ts.q, t);
+  ts.sg = sk_fit_splits(ts.g, t);
+  ts.su = sk_fit_splits(ts.u, t);
+  ts.so = sk_fit_splits(ts.o, t);
 }
 
-// partial GEMM on the tensor cores + fixed-order reduce applying `epi`
+// one launch: tensor-core partials, DSMEM split reduction, fused epilogue
 template <class Epi>
-void gemm_tc(Ctx &c, const GemmTcMaps &maps, int M, int splits, float *ws, const Epi &epi) {
-  c.run(c.cls, [&] {
-    launch_gemm_tc_partial(maps, M, splits, ws, c.st);
-    const long long total = (long long)M * maps.N;
-    splitk_reduce_kernel<Epi><<<(unsigned)((total + 255) / 256), 256, 0, c.st>>>(ws, M, maps.N, splits, total, epi);
-    AMUN_CHECK_LAUNCH();
-  });
-  c.launches += 1;
+void gemm_tc(Ctx &c, const SkMaps &maps, int M, int splits, const Epi &epi) {
+  c.run(c.cls, [&] { launch_gemm_sk(maps, M, splits, epi, c.st); });
 }
 
 void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
@@ -300,23 +278,26 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
   const int s_off = de + 2 * dh;
   c.cls = AMUN_K_QUERY;
   if (ts)
-    gemm_tc(c, ts->q, R, ts->sq, ts->ws, EpiStore{d.Q, da, nullptr, 0, 0});
+    gemm_tc(c, ts->q, R, ts->sq, EpiStore{d.Q, da, nullptr, 0, 0});
   else
     gemm(c, ga(R, da, d.XS + s_off, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
   AttnArgs aa{d.Q, da, e.P, e.Hann, m->v_att, d_len, jmax, da, 2 * dh, rows_per_sent, n_act, done,
               d.XS + de, xs, alpha};
+  aa.energy = d.En;
   if (ts) {
     aa.ctx_hi = d.XSh + de;
     aa.ctx_lo = d.XSl + de;
   }
-  c.run(AMUN_K_ATTN, [&] { launch_attention(aa, R, c.st); });
+  int na_launch = 1;
+  c.run(AMUN_K_ATTN, [&] { na_launch = launch_attention(aa, R, c.st); });
+  c.launches += na_launch - 1;
   c.cls = AMUN_K_GRU_A;
   {
     EpiGruA ea{m->bg, d.XS + s_off, xs, dh, d.Z, d.RH, d.XH};
     if (ts) {
       ea.RHh = d.RHh;
       ea.RHl = d.RHl;
-      gemm_tc(c, ts->g, R, ts->sg, ts->ws, ea);
+      gemm_tc(c, ts->g, R, ts->sg, ea);
     } else {
       GemmArgs g = ga(R, 3 * dh, d.XS, xs, xs, m->Wg, 3 * dh);
       g.n_split = 2 * dh;
@@ -330,7 +311,7 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     if (ts) {
       eb.Snh = d.Snh;
       eb.Snl = d.Snl;
-      gemm_tc(c, ts->u, R, ts->su, ts->ws, eb);
+      gemm_tc(c, ts->u, R, ts->su, eb);
     } else {
       gemm(c, ga(R, dh, d.RH, dh, dh, m->Uh_dec, dh), eb);
     }
@@ -343,7 +324,7 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
       e.lo = d.T_lo;
     }
     if (ts) {
-      gemm_tc(c, ts->o, R, ts->so, ts->ws, e);
+      gemm_tc(c, ts->o, R, ts->so, e);
     } else {
       GemmArgs g = ga(R, de, d.XS, xs, de + 2 * dh, m->Wout, de);
       g.a1 = d.Sn;
@@ -533,19 +514,15 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.db.resize(n_models);
     L.fin_states.assign(n_models, nullptr);
     L.tsteps.resize(n_models);
-    std::vector<size_t> ts_ws(n_models, 0);
-    if (use_tcg)
-      for (int m = 0; m < n_models; ++m) ts_ws[m] = tc_step_ws_floats(ms[m], Rmax, L.tsteps[m]);
     for (int pass = 0; pass < 2; ++pass) {
       Carver cv;
       cv.base = pass ? static_cast<char *>(L.mem.p) : nullptr;
       for (int m = 0; m < n_models; ++m) {
         carve_enc(cv, L.eb[m], ms[m], Bmax, jmax_all);
-        carve_dec(cv, L.db[m], ms[m], Rmax, !fused);
+        carve_dec(cv, L.db[m], ms[m], Rmax, jmax_all, !fused);
         if (!use_tc) L.db[m].T_hi = L.db[m].T_lo = nullptr;
         if (use_tcg) {
           carve_dec_tc(cv, L.db[m], ms[m], Rmax);
-          L.tsteps[m].ws = cv.take<float>(ts_ws[m]);
         }
         L.fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * dh) : nullptr;
       }
@@ -986,7 +963,7 @@ void hook_step(amun_model *m, const float *s, const int32_t *y_prev, int R, cons
     cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
     e.Hann = cv.take<float>((size_t)J * 2 * dh);
     e.P = cv.take<float>((size_t)J * da);
-    carve_dec(cv, d, m, R, true);
+    carve_dec(cv, d, m, R, J, true);
     d_len = cv.take<int>(1);
     d_y = cv.take<int>(R);
     d_sl = cv.take<int>(std::max(n_sl, 1));
@@ -1007,6 +984,7 @@ void hook_step(amun_model *m, const float *s, const int32_t *y_prev, int R, cons
   if (!y_prev) {  // attention only (nnet.py:132-141)
     gemm(c, ga(R, da, d.XS + de + 2 * dh, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
     AttnArgs aa{d.Q, da, e.P, e.Hann, m->v_att, d_len, J, da, 2 * dh, R, nullptr, nullptr, d.XS + de, xs, d_alpha};
+    aa.energy = d.En;
     launch_attention(aa, R, c.st);
   } else {
     LogitOut lo{false, 0, 0, nullptr, nullptr, nullptr, nullptr};

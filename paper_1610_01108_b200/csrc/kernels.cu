@@ -97,326 +97,179 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
   }
 }
 
-// Sentence-level attention: one CTA per sentence computes every active beam
-// row, so each P_j / H_j row is read once and reused across the beam from
-// registers (the per-row kernel above reads them once per hypothesis).
-//   energies: warp per source position, lane holds 8 P values per chunk,
-//             KA row accumulators; context: thread holds 4 columns x KA rows.
-template <int KA>
-__global__ void __launch_bounds__(512) attention_sent_kernel(AttnArgs a) {
-  extern __shared__ float sm[];
-  const int k = a.rows_per_sent;
-  const int b = blockIdx.x;
+// Two-phase attention for beam rows grouped by sentence (rows_per_sent = k
+// rows of sentence b share P_b / H_b):
+//   attn_energy_kernel: warp per (sentence b, source position j); the lane
+//     keeps 32 elements of P_bj and v in registers and computes
+//     e[r, j] = v . tanh(P_bj + q_r) for every active row r of the sentence
+//     (P_bj read once per sentence, 32 independent tanh chains per lane).
+//   attn_context_kernel: CTA per (sentence, 256 columns of 2 d_h): masked
+//     softmax of the sentence's energy rows in shared memory, then
+//     thread = column, ctx[r, c] = sum_j alpha[r, j] H_bj[c] over the rows.
+// Energies and context sums run in a fixed order, independent of which other
+// sentences share the launch.
+constexpr int kEnergyWarps = 8;  // source positions per energy CTA
+
+__global__ void __launch_bounds__(32 * kEnergyWarps) attn_energy_kernel(AttnArgs a) {
+  extern __shared__ float qs[];  // [na][da] query rows of this sentence
+  const int b = blockIdx.y;
   if (a.n_act && a.done[b]) return;
-  const int na = a.n_act ? a.n_act[b] : k;
   const int J = a.len[b];
-  float *q = sm;                  // [KA][da]
-  float *vv = q + KA * a.da;      // [da]
-  float *al = vv + a.da;          // [KA][jmax]
-  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
-  for (int i = tid; i < na * a.da; i += blockDim.x) {
-    const int r = i / a.da, c = i % a.da;
-    q[i] = a.Q[(long long)(b * k + r) * a.ldq + c];
-  }
-  for (int i = tid; i < a.da; i += blockDim.x) vv[i] = a.v[i];
-  __syncthreads();
-  const float *Pb = a.P + (long long)b * a.jmax * a.da;
-  for (int j = warp; j < J; j += nw) {
-    const float *pj = Pb + (long long)j * a.da;
-    float acc[KA];
-#pragma unroll
-    for (int r = 0; r < KA; ++r) acc[r] = 0.f;
-    // whole 1024-wide row in one round trip: 32 independent loads per lane,
-    // then a rolled loop over the beam rows (keeps the code small)
-    for (int i0 = lane; i0 < a.da; i0 += 32 * 32) {
-      float p[32];
-#pragma unroll
-      for (int u = 0; u < 32; ++u) p[u] = (i0 + 32 * u < a.da) ? __ldg(pj + i0 + 32 * u) : 0.f;
-#pragma unroll 1
-      for (int r = 0; r < na; ++r) {
-        const float *qr = q + r * a.da;
-        float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-        for (int u = 0; u < 32; u += 2) {
-          const int i = i0 + 32 * u;
-          if (i < a.da) s0 = fmaf(vv[i], tanh_attn(p[u] + qr[i]), s0);
-          if (i + 32 < a.da) s1 = fmaf(vv[i + 32], tanh_attn(p[u + 1] + qr[i + 32]), s1);
-        }
-#pragma unroll
-        for (int rr = 0; rr < KA; ++rr)
-          if (rr == r) acc[rr] += s0 + s1;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < KA; ++r) {
-      if (r < na) {
-        const float s = warp_sum(acc[r]);
-        if (lane == 0) al[r * a.jmax + j] = s;
-      }
-    }
+  const int j0 = blockIdx.x * kEnergyWarps;
+  if (j0 >= J) return;
+  const int k = a.rows_per_sent;
+  const int na = a.n_act ? a.n_act[b] : k;
+  for (int i = threadIdx.x; i < na * a.da; i += blockDim.x) {
+    const int r = i / a.da, c = i - r * a.da;
+    qs[i] = __ldg(a.Q + (long long)(b * k + r) * a.ldq + c);
   }
   __syncthreads();
-  // masked softmax over j < J, one warp per row
-  for (int r = warp; r < na; r += nw) {
-    float *e = al + r * a.jmax;
-    float mx = -INFINITY;
-    for (int j = lane; j < J; j += 32) mx = fmaxf(mx, e[j]);
-    mx = warp_max(mx);
-    float s = 0.f;
-    for (int j = lane; j < J; j += 32) {
-      const float w = expf(e[j] - mx);
-      e[j] = w;
-      s += w;
-    }
-    s = warp_sum(s);
-    const float inv = 1.0f / s;
-    for (int j = lane; j < J; j += 32) {
-      const float w = e[j] * inv;
-      e[j] = w;
-      if (a.alpha) a.alpha[(long long)(b * k + r) * a.jmax + j] = w;
-    }
+  const int lane = threadIdx.x % 32;
+  const int j = j0 + threadIdx.x / 32;
+  if (j >= J) return;
+  const float *pj = a.P + ((long long)b * a.jmax + j) * a.da;
+  float p[32], v[32];
+#pragma unroll
+  for (int u = 0; u < 32; ++u) {
+    const int i = lane + 32 * u;
+    p[u] = i < a.da ? __ldg(pj + i) : 0.f;
+    v[u] = i < a.da ? __ldg(a.v + i) : 0.f;
   }
-  __syncthreads();
-  // context: thread = up to 4 columns, all rows
-  const float *Hb = a.H + (long long)b * a.jmax * a.dh2;
-  for (int c0 = tid; c0 < a.dh2; c0 += 4 * blockDim.x) {
-    float acc[4][KA];
+  for (int r = 0; r < na; ++r) {
+    const float *qr = qs + r * a.da;
+    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int r = 0; r < KA; ++r) acc[u][r] = 0.f;
-    // 4 source positions per iteration: 16 independent H loads in flight
-    for (int j0 = 0; j0 < J; j0 += 4) {
-      float h[4][4];
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const float *hj = Hb + (long long)(j0 + jj) * a.dh2;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = c0 + u * blockDim.x;
-          h[jj][u] = (c < a.dh2 && j0 + jj < J) ? __ldg(hj + c) : 0.f;
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        if (j0 + jj >= J) break;
-#pragma unroll
-        for (int r = 0; r < KA; ++r) {
-          if (r < na) {
-            const float w = al[r * a.jmax + j0 + jj];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u][r] = fmaf(w, h[jj][u], acc[u][r]);
-          }
-        }
-      }
+    for (int u = 0; u < 32; u += 2) {
+      const int i = lane + 32 * u;
+      if (i < a.da) s0 = fmaf(v[u], tanh_attn(p[u] + qr[i]), s0);
+      if (i + 32 < a.da) s1 = fmaf(v[u + 1], tanh_attn(p[u + 1] + qr[i + 32]), s1);
     }
-#pragma unroll
-    for (int r = 0; r < KA; ++r) {
-      if (r >= na) continue;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * blockDim.x;
-        if (c < a.dh2) {
-          const long long o = (long long)(b * k + r) * a.ldctx + c;
-          a.ctx[o] = acc[u][r];
-          store_split(a.ctx_hi, a.ctx_lo, o, acc[u][r]);
-        }
-      }
-    }
+    const float s = warp_sum(s0 + s1);
+    if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = s;
   }
 }
 
-// Cluster version: a 4-CTA cluster per sentence.  CTA q computes the
-// energies of positions j = q, q+4, ... for every beam row and writes them
-// into all four CTAs' shared memory (DSMEM); after a cluster barrier each CTA
-// normalises the (tiny) softmax locally and computes the context for its
-// quarter of the 2 d_h columns.  4x the SMs of one-CTA-per-sentence at the
-// same total work.
-constexpr int kAttnCluster = 4;
+constexpr int kCtxThreads = 128;  // thread = 4 consecutive columns (float4)
+constexpr int kCtxRows = 8;       // row accumulators per pass
 
-template <int KA>
-__global__ void __cluster_dims__(kAttnCluster, 1, 1) __launch_bounds__(256)
-    attention_cluster_kernel(AttnArgs a) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ float sm[];
+__global__ void __launch_bounds__(kCtxThreads) attn_context_kernel(AttnArgs a) {
+  extern __shared__ float al[];  // [k][jmax]
+  const int b = blockIdx.x;
+  if (a.n_act && a.done[b]) return;
   const int k = a.rows_per_sent;
-  const int q4 = (int)cluster.block_rank();
-  const int b = blockIdx.x / kAttnCluster;
-  if (a.n_act && a.done[b]) return;  // uniform over the cluster
   const int na = a.n_act ? a.n_act[b] : k;
   const int J = a.len[b];
-  float *q = sm;                  // [KA][da]
-  float *vv = q + KA * a.da;      // [da]
-  float *al = vv + a.da;          // [KA][jmax]
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
-  for (int i = tid; i < na * a.da; i += blockDim.x) {
-    const int r = i / a.da, c = i % a.da;
-    q[i] = a.Q[(long long)(b * k + r) * a.ldq + c];
-  }
-  for (int i = tid; i < a.da; i += blockDim.x) vv[i] = a.v[i];
-  __syncthreads();
-  float *al_rank[kAttnCluster];
-#pragma unroll
-  for (int c = 0; c < kAttnCluster; ++c) al_rank[c] = cluster.map_shared_rank(al, c);
-  const float *Pb = a.P + (long long)b * a.jmax * a.da;
-  for (int j = q4 + kAttnCluster * warp; j < J; j += kAttnCluster * nw) {
-    const float *pj = Pb + (long long)j * a.da;
-    float acc[KA];
-#pragma unroll
-    for (int r = 0; r < KA; ++r) acc[r] = 0.f;
-    for (int i0 = lane; i0 < a.da; i0 += 32 * 32) {
-      float p[32];
-#pragma unroll
-      for (int u = 0; u < 32; ++u) p[u] = (i0 + 32 * u < a.da) ? __ldg(pj + i0 + 32 * u) : 0.f;
-#pragma unroll 1
-      for (int r = 0; r < na; ++r) {
-        const float *qr = q + r * a.da;
-        float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-        for (int u = 0; u < 32; u += 2) {
-          const int i = i0 + 32 * u;
-          if (i < a.da) s0 = fmaf(vv[i], tanh_attn(p[u] + qr[i]), s0);
-          if (i + 32 < a.da) s1 = fmaf(vv[i + 32], tanh_attn(p[u + 1] + qr[i + 32]), s1);
-        }
-#pragma unroll
-        for (int rr = 0; rr < KA; ++rr)
-          if (rr == r) acc[rr] += s0 + s1;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < KA; ++r) {
-      if (r < na) {
-        const float s = warp_sum(acc[r]);
-        if (lane < kAttnCluster) al_rank[lane][r * a.jmax + j] = s;  // broadcast to the cluster
-      }
-    }
-  }
-  cluster.sync();  // all energies visible in every CTA's shared memory
+  // masked softmax over j < J, one warp per row (nnet.py:137-139)
   for (int r = warp; r < na; r += nw) {
+    const float *er = a.energy + (long long)(b * k + r) * a.jmax;
     float *e = al + r * a.jmax;
     float mx = -INFINITY;
-    for (int j = lane; j < J; j += 32) mx = fmaxf(mx, e[j]);
+    for (int j = lane; j < J; j += 32) {
+      e[j] = er[j];
+      mx = fmaxf(mx, e[j]);
+    }
     mx = warp_max(mx);
     float s = 0.f;
     for (int j = lane; j < J; j += 32) {
-      const float w = expf(e[j] - mx);
-      e[j] = w;
-      s += w;
+      const float x = expf(e[j] - mx);
+      e[j] = x;
+      s += x;
     }
     s = warp_sum(s);
     const float inv = 1.0f / s;
     for (int j = lane; j < J; j += 32) {
-      const float w = e[j] * inv;
-      e[j] = w;
-      if (a.alpha && q4 == 0) a.alpha[(long long)(b * k + r) * a.jmax + j] = w;
+      const float x = e[j] * inv;
+      e[j] = x;
+      if (a.alpha && blockIdx.y == 0) a.alpha[(long long)(b * k + r) * a.jmax + j] = x;
     }
   }
   __syncthreads();
-  // context for this CTA's quarter of the columns: thread = 2 columns x KA rows
-  const int cw = (a.dh2 + kAttnCluster - 1) / kAttnCluster;
-  const int cbeg = q4 * cw, cend = min(a.dh2, cbeg + cw);
-  const float *Hb = a.H + (long long)b * a.jmax * a.dh2;
-  for (int c0 = cbeg + tid; c0 < cend; c0 += 2 * blockDim.x) {
-    float acc[2][KA];
+  const int c = (blockIdx.y * kCtxThreads + tid) * 4;
+  if (c >= a.dh2) return;
+  const float4 *Hb = reinterpret_cast<const float4 *>(a.H + (long long)b * a.jmax * a.dh2 + c);
+  const int hs = a.dh2 / 4;  // float4 stride between positions
+  for (int r0 = 0; r0 < na; r0 += kCtxRows) {
+    float4 acc[kCtxRows];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int r = 0; r < kCtxRows; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int j = 0;
+    for (; j + 8 <= J; j += 8) {
+      float4 h[8];
 #pragma unroll
-      for (int r = 0; r < KA; ++r) acc[u][r] = 0.f;
-    for (int j0 = 0; j0 < J; j0 += 8) {
-      float h[8][2];
+      for (int jj = 0; jj < 8; ++jj) h[jj] = __ldg(Hb + (long long)(j + jj) * hs);
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int c = c0 + u * blockDim.x;
-          h[jj][u] = (c < cend && j0 + jj < J) ? __ldg(Hb + (long long)(j0 + jj) * a.dh2 + c) : 0.f;
-        }
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        if (j0 + jj >= J) break;
-#pragma unroll
-        for (int r = 0; r < KA; ++r) {
-          if (r < na) {
-            const float w = al[r * a.jmax + j0 + jj];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) acc[u][r] = fmaf(w, h[jj][u], acc[u][r]);
+        for (int r = 0; r < kCtxRows; ++r)
+          if (r0 + r < na) {
+            const float w = al[(r0 + r) * a.jmax + j + jj];
+            acc[r].x = fmaf(w, h[jj].x, acc[r].x);
+            acc[r].y = fmaf(w, h[jj].y, acc[r].y);
+            acc[r].z = fmaf(w, h[jj].z, acc[r].z);
+            acc[r].w = fmaf(w, h[jj].w, acc[r].w);
           }
+    }
+    for (; j < J; ++j) {
+      const float4 h = __ldg(Hb + (long long)j * hs);
+#pragma unroll
+      for (int r = 0; r < kCtxRows; ++r)
+        if (r0 + r < na) {
+          const float w = al[(r0 + r) * a.jmax + j];
+          acc[r].x = fmaf(w, h.x, acc[r].x);
+          acc[r].y = fmaf(w, h.y, acc[r].y);
+          acc[r].z = fmaf(w, h.z, acc[r].z);
+          acc[r].w = fmaf(w, h.w, acc[r].w);
         }
-      }
     }
 #pragma unroll
-    for (int r = 0; r < KA; ++r) {
-      if (r >= na) continue;
+    for (int r = 0; r < kCtxRows; ++r) {
+      if (r0 + r >= na) break;
+      const long long o = (long long)(b * k + r0 + r) * a.ldctx + c;
+      const float vals[4] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int c = c0 + u * blockDim.x;
-        if (c < cend) {
-          const long long o = (long long)(b * k + r) * a.ldctx + c;
-          a.ctx[o] = acc[u][r];
-          store_split(a.ctx_hi, a.ctx_lo, o, acc[u][r]);
-        }
+      for (int u = 0; u < 4; ++u) {
+        a.ctx[o + u] = vals[u];
+        store_split(a.ctx_hi, a.ctx_lo, o + u, vals[u]);
       }
     }
   }
 }
 
-template <int KA>
-static void launch_attention_cluster(const AttnArgs &a, int B, cudaStream_t st) {
-  const size_t smem = sizeof(float) * ((size_t)(KA + 1) * a.da + (size_t)KA * a.jmax);
-  auto kern = attention_cluster_kernel<KA>;
-  static size_t attr_set[64] = {};
-  int dev = 0;
-  AMUN_CUDA(cudaGetDevice(&dev));
-  if (smem > 48 * 1024 && (dev >= 64 || attr_set[dev] < smem)) {
-    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    if (dev < 64) attr_set[dev] = 200 * 1024;
-  }
-  kern<<<B * kAttnCluster, 256, smem, st>>>(a);
-  AMUN_CHECK_LAUNCH();
-}
-
-template <int KA>
-static void launch_attention_sent(const AttnArgs &a, int B, cudaStream_t st) {
-  const size_t smem = sizeof(float) * ((size_t)(KA + 1) * a.da + (size_t)KA * a.jmax);
-  auto kern = attention_sent_kernel<KA>;
-  static size_t attr_set[64] = {};  // per device: largest smem opted in so far
-  int dev = 0;
-  AMUN_CUDA(cudaGetDevice(&dev));
-  if (smem > 48 * 1024 && (dev >= 64 || attr_set[dev] < smem)) {
-    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    if (dev < 64) attr_set[dev] = 200 * 1024;
-  }
-  kern<<<B, 512, smem, st>>>(a);
-  AMUN_CHECK_LAUNCH();
-}
-
-void launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
-  if (R <= 0) return;
+int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
+  if (R <= 0) return 0;
   const int k = a.rows_per_sent;
-  const size_t smem_sent = sizeof(float) * ((size_t)(k + 1) * a.da + (size_t)k * a.jmax);
-  static const bool sent_only = [] {  // AMUN_ATTN_CLUSTER=1: 4-CTA cluster kernel
-    const char *e = getenv("AMUN_ATTN_CLUSTER");
-    return !(e && e[0] == '1');
-  }();
-  if (k <= 16 && R % k == 0 && smem_sent <= 200 * 1024) {
-    if (sent_only) {
-      if (k == 1) launch_attention_sent<1>(a, R / k, st);
-      else if (k <= 4) launch_attention_sent<4>(a, R / k, st);
-      else if (k <= 8) launch_attention_sent<8>(a, R / k, st);
-      else launch_attention_sent<16>(a, R / k, st);
-    } else {
-      if (k == 1) launch_attention_cluster<1>(a, R / k, st);
-      else if (k <= 4) launch_attention_cluster<4>(a, R / k, st);
-      else if (k <= 8) launch_attention_cluster<8>(a, R / k, st);
-      else launch_attention_cluster<16>(a, R / k, st);
+  const size_t smem = sizeof(float) * (size_t)k * a.jmax;
+  const size_t smem_q = sizeof(float) * (size_t)k * a.da;
+  if (a.energy && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && smem <= 200 * 1024 && smem_q <= 200 * 1024) {
+    const int B = R / k;
+    static size_t attr_q[64] = {};
+    int dev = 0;
+    AMUN_CUDA(cudaGetDevice(&dev));
+    if (smem_q > 48 * 1024 && (dev >= 64 || attr_q[dev] < smem_q)) {
+      AMUN_CUDA(cudaFuncSetAttribute(attn_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      if (dev < 64) attr_q[dev] = smem_q;
     }
-    return;
+    attn_energy_kernel<<<dim3(ceil_div(a.jmax, kEnergyWarps), B), 32 * kEnergyWarps, smem_q, st>>>(a);
+    AMUN_CHECK_LAUNCH();
+    if (smem > 48 * 1024) {
+      static size_t attr_set[64] = {};
+      int dev = 0;
+      AMUN_CUDA(cudaGetDevice(&dev));
+      if (dev >= 64 || attr_set[dev] < smem) {
+        AMUN_CUDA(cudaFuncSetAttribute(attn_context_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        if (dev < 64) attr_set[dev] = smem;
+      }
+    }
+    attn_context_kernel<<<dim3(B, ceil_div(a.dh2, 4 * kCtxThreads)), kCtxThreads, smem, st>>>(a);
+    AMUN_CHECK_LAUNCH();
+    return 2;
   }
-  size_t smem = sizeof(float) * (2 * a.da + a.jmax);
-  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  attention_kernel<<<R, 256, smem, st>>>(a);
+  size_t smem1 = sizeof(float) * (2 * a.da + a.jmax);
+  if (smem1 > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  attention_kernel<<<R, 256, smem1, st>>>(a);
   AMUN_CHECK_LAUNCH();
+  return 1;
 }
 
 // ================================================================ encoder

@@ -7,10 +7,12 @@
 namespace amun {
 
 // ---------------------------------------------------------------- attention
-// nnet.py:132-141 for a batch of hypothesis rows.  One CTA per row r
-// (sentence b = r / rows_per_sent): e_j = v . tanh(P_bj + q_r) with one warp
-// per source position, masked softmax over j < len[b], ctx = sum_j a_j H_bj
-// written straight into the decoder input buffer.
+// nnet.py:132-141 for a batch of hypothesis rows (sentence b = r /
+// rows_per_sent): e_j = v . tanh(P_bj + q_r), masked softmax over j < len[b],
+// ctx = sum_j a_j H_bj written straight into the decoder input buffer.  With
+// an energy scratch buffer: one launch computing the energies of every
+// (sentence, position) pair and one computing softmax + context per
+// (sentence, column block); without: one CTA per row.
 struct AttnArgs {
   const float *Q;  // [R, ldq]
   int ldq;
@@ -24,8 +26,10 @@ struct AttnArgs {
   int ldctx;
   float *alpha;  // optional [R][jmax]
   float *ctx_hi = nullptr, *ctx_lo = nullptr;  // optional 3xTF32 split (same layout as ctx)
+  float *energy = nullptr;  // scratch [R][jmax]: enables the two-phase sentence kernels
 };
-void launch_attention(const AttnArgs &a, int R, cudaStream_t st);
+// returns the number of kernels launched
+int launch_attention(const AttnArgs &a, int R, cudaStream_t st);
 
 // ---------------------------------------------------------------- encoder
 // masked mean over real positions: out[b] = sum_{j < len_b} Hann[b, j] / len_b

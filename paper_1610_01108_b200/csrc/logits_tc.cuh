@@ -21,6 +21,8 @@ struct LogitTcMaps {
 };
 
 int logits_tc_tile_n();
+// fp32 2D tensor map; the swizzle follows the box row width (64 B -> SW64,
+// 128 B -> SW128)
 CUtensorMap make_tma_2d_f32(const float *ptr, int inner, int outer, int row_stride_elems, int box_inner,
                             int box_outer);
 // t_hi/t_lo: [R, ldt] (first K columns used); w_hi/w_lo: [V, K] (logit rows)

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(C::kThreads, 1)
                    Epi epi) {
   constexpr int CG = C::kCG;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = tc::align_smem<1024>(smem_raw);  // stays in the shared address space (LDS/STS)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
   uint64_t *empty = full + C::kStages;
   uint64_t *tfull = empty + C::kStages;

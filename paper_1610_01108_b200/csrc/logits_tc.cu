@@ -6,17 +6,25 @@
 //
 // Precision: 3xTF32 on tcgen05.mma kind::tf32.  Both operands are split into
 // tf32-exact hi and residual lo parts (t by the deep-output epilogue, the
-// weights once at model load) and the CTA accumulates hi*hi + hi*lo + lo*hi
+// weights once at model load) and the MMAs accumulate hi*hi + hi*lo + lo*hi
 // in fp32 in TMEM — FP32-equivalent accuracy (BF16/TF32 flip the
 // beam set in 1-4% of steps, FP32 and 3xTF32 in none).
 //
-// CTA = one BN-wide vocabulary tile for ALL hypothesis rows (up to MB*128 per
-// pass; TMEM holds MB accumulators of 128 x BN fp32), so every weight byte is
-// read from HBM exactly once per launch.  Warp roles: warp 0 issues TMA
-// (SWIZZLE_64B K-major tiles, 3-stage mbarrier ring), warp 1 allocates TMEM
-// and issues the MMAs from one thread, warps 2-5 run the epilogue: thread =
-// one row (TMEM lane), tcgen05.ld 32 columns at a time, bias add, running
-// max / top-kk insertion, then a second TMEM pass for sum(exp(x - max)).
+// Swap-AB on CTA pairs (tcgen05 cta_group::2): the vocabulary is the MMA's
+// M dimension (256 logit rows per pair, 128 per CTA = one TMEM lane each)
+// and the hypothesis rows are its N dimension (up to 160 per work unit; each
+// CTA stages half of them and the pair's tensor cores share the halves,
+// halving activation traffic and shared-memory reads).  Persistent: a pair
+// loops over contiguous (256-vocab tile, 160-row block) work units with two
+// TMEM accumulator buffers, so the epilogue of one unit overlaps the
+// mainloop of the next.
+//
+// Epilogue (4 warps, both CTAs): tcgen05.ld 32 rows x 128 vocab at a time,
+// bias add, transpose through shared memory, then thread = (row, quarter of
+// the vocab): max, sum exp(x - max) and a register top-kk over 32 logits,
+// merged across the 4 quarters with warp shuffles.  Per (row, 128-vocab
+// tile) it writes (max, sum) and the tile's top-kk — the partial layout the
+// select kernel consumes.
 #include "common.cuh"
 #include "logits_tc.cuh"
 #include "tc_common.cuh"
@@ -25,10 +33,25 @@ namespace amun {
 
 namespace {
 
-constexpr int kBK = 16;  // fp32 elements per 64-byte swizzled row
+constexpr int kBK = 32;                     // fp32 K elements per 128-byte swizzled row
+constexpr int kRowB = kBK * 4;
+constexpr int kStages = 3;
+constexpr int kUnitRows = 160;              // hypothesis rows per work unit (one MMA, N <= 160)
+constexpr int kXRows = kUnitRows / 2;       // rows staged by each CTA of the pair
+constexpr int kBoxR = 16;                   // activation rows per TMA box
+constexpr int kWB = 128 * kRowB;            // one of hi/lo weight tiles
+constexpr int kXB = kXRows * kRowB;         // one of hi/lo activation tiles
+constexpr int kStageB = 2 * kWB + 2 * kXB;  // 52 KB
+constexpr int kAccCols = 256;               // TMEM column offset of accumulator buffer 1
+constexpr int kTrQ = 36;                    // floats per vocabulary quarter in a transposed row (32 + pad)
+constexpr int kTrRow = 4 * kTrQ;            // floats per transposed row (128 vocab + pad)
+constexpr int kTrB = 32 * kTrRow * 4;       // one transpose buffer (32 rows x 128 vocab)
+constexpr int kEpiGroups = 3;               // epilogue warp groups (4 warps each) working on alternate chunks
+constexpr int kSmem = kStages * kStageB + kEpiGroups * kTrB + 1024 + 256;
+constexpr int kThreads = 64 + 128 * kEpiGroups;  // warp 0 TMA, warp 1 MMA (leader), then the epilogue groups
+static_assert(kSmem <= 232448, "shared memory per CTA");
 
-// Register-resident sorted top-KK list of one row (KK is a compile-time
-// size >= kk so every index is static and nothing spills to local memory).
+// Register-resident top-KK list ordered by (logit desc, token asc).
 template <int KK>
 struct RowTop {
   float v[KK];
@@ -37,212 +60,354 @@ struct RowTop {
 #pragma unroll
     for (int i = 0; i < KK; ++i) {
       v[i] = -INFINITY;
-      t[i] = -1;
+      t[i] = 0x7fffffff;
     }
   }
-  __device__ __forceinline__ float worst() const { return v[KK - 1]; }
-  // caller guarantees x > worst().  Columns arrive in ascending token order,
-  // so an equal value loses the tie (token asc): strict > is exact.
+  __device__ __forceinline__ bool beats(float x, int n, int i) const {
+    return x > v[i] || (x == v[i] && n < t[i]);
+  }
+  // branch-free insertion (selects only: no divergence inside a warp)
   __device__ __forceinline__ void insert(float x, int n) {
 #pragma unroll
     for (int i = 0; i < KK; ++i) {
-      if (x > v[i]) {
-        float tv = v[i];
-        int tt = t[i];
-        v[i] = x;
-        t[i] = n;
-        x = tv;
-        n = tt;
-      }
+      const bool c = beats(x, n, i);
+      const float vi = v[i];
+      const int ti = t[i];
+      v[i] = c ? x : vi;
+      t[i] = c ? n : ti;
+      x = c ? vi : x;
+      n = c ? ti : n;
     }
   }
 };
 
-template <int BN, int MB, int STAGES, int KK, int CS>
-__global__ void __launch_bounds__(64 + 128 * MB, 1)
-    logits_tc_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
-                     const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
-                     LogitTcArgs a) {
-  constexpr int A_BYTES = MB * 128 * kBK * 4;
-  constexpr int B_BYTES = BN * kBK * 4;
-  constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  constexpr uint32_t TMEM_COLS = (MB * BN <= 128) ? 128 : (MB * BN <= 256) ? 256 : 512;
-  static_assert(MB * BN <= 512, "accumulators exceed TMEM");
+__device__ __forceinline__ bool key_beats(float va, int ta, float vb, int tb) {
+  return va > vb || (va == vb && ta < tb);
+}
+
+// top.{v,t} <- best KK of (top U partner lane's top), both sorted best-first:
+// elementwise best of A[i] and B[P-1-i] is the union's top P as a bitonic
+// sequence, which log2(P) half-cleaner stages sort (all steps independent
+// compare-exchanges: short dependency chains, no divergence).
+template <int KK>
+__device__ __forceinline__ void merge_partner(RowTop<KK> &top, int lane_xor) {
+  constexpr int P = KK <= 1 ? 1 : KK <= 2 ? 2 : KK <= 4 ? 4 : KK <= 8 ? 8 : 16;
+  float ov[KK];
+  int ot[KK];
+#pragma unroll
+  for (int i = 0; i < KK; ++i) {
+    ov[i] = __shfl_xor_sync(0xffffffffu, top.v[i], lane_xor);
+    ot[i] = __shfl_xor_sync(0xffffffffu, top.t[i], lane_xor);
+  }
+  float cv[P];
+  int ct[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    const float av = i < KK ? top.v[i] : -INFINITY;
+    const int at = i < KK ? top.t[i] : 0x7fffffff;
+    const int j = P - 1 - i;
+    const float bv = j < KK ? ov[j] : -INFINITY;
+    const int bt = j < KK ? ot[j] : 0x7fffffff;
+    const bool ta = key_beats(av, at, bv, bt);
+    cv[i] = ta ? av : bv;
+    ct[i] = ta ? at : bt;
+  }
+#pragma unroll
+  for (int d = P / 2; d >= 1; d /= 2)
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if ((i & d) == 0) {
+        const int j = i + d;
+        const bool sw = key_beats(cv[j], ct[j], cv[i], ct[i]);
+        const float vi = cv[i], vj = cv[j];
+        const int ti = ct[i], tj = ct[j];
+        cv[i] = sw ? vj : vi;
+        ct[i] = sw ? tj : ti;
+        cv[j] = sw ? vi : vj;
+        ct[j] = sw ? ti : tj;
+      }
+#pragma unroll
+  for (int i = 0; i < KK; ++i) {
+    top.v[i] = cv[i];
+    top.t[i] = ct[i];
+  }
+}
+
+// Work unit u of a launch: 256-vocab tile vt, rows [row0, row0 + nr); the
+// pair's MMA has N = nr rounded up to 32, each CTA stages N / 2 of the rows.
+struct Unit {
+  int vt, row0, nr, n, h;
+  __device__ __forceinline__ Unit(int u, int npass, int M) {
+    vt = u / npass;
+    row0 = (u % npass) * kUnitRows;
+    nr = min(kUnitRows, M - row0);
+    n = (nr + 31) / 32 * 32;
+    h = n / 2;
+  }
+};
+
+template <int KK>
+__global__ void __launch_bounds__(kThreads, 1)
+    logits_pair_kernel(const __grid_constant__ CUtensorMap tX_hi, const __grid_constant__ CUtensorMap tX_lo,
+                       const __grid_constant__ CUtensorMap tW_hi, const __grid_constant__ CUtensorMap tW_lo,
+                       LogitTcArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
-  uint64_t *empty = full + STAGES;
-  uint64_t *tfull = empty + STAGES;
-  uint64_t *tempty = tfull + 1;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
-  float *sbias = reinterpret_cast<float *>(tempty + 2);  // [BN] bias tile, -inf past the vocabulary
+  uint8_t *smem = tc::align_smem<1024>(smem_raw);  // stays in the shared address space (LDS/STS)
+  float *tr = reinterpret_cast<float *>(smem + kStages * kStageB);  // [group][32][kTrRow]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageB + kEpiGroups * kTrB);
+  uint64_t *empty = full + kStages;
+  uint64_t *tfull = empty + kStages;  // [2] accumulator buffers
+  uint64_t *tempty = tfull + 2;       // [2]
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n0 = blockIdx.x * BN;
-  // CS CTAs of a cluster work on adjacent vocabulary tiles and share the
-  // activation tiles: each CTA TMA-multicasts 1/CS of them to the cluster.
-  const uint32_t crank = CS > 1 ? tc::cluster_rank() : 0;
-  constexpr uint16_t kAll = (uint16_t)((1u << CS) - 1);
+  const uint32_t crank = tc::cluster_rank();
+  const int member = (int)(crank & 1);
+  const uint32_t leader = crank & ~1u;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int nvt = (a.N + 255) / 256;
+  const int npass = (a.M + kUnitRows - 1) / kUnitRows;
+  const int units = nvt * npass;
+  // contiguous units per pair: the two row halves of a vocabulary tile run
+  // back to back on the same pair, so the second weight read hits L2
+  const int upp = (units + npairs - 1) / npairs;
+  const int u_begin = pair * upp, u_end = min(units, u_begin + upp);
   const int nk = (a.K + kBK - 1) / kBK;
-  const int nchunks = (a.M + MB * 128 - 1) / (MB * 128);
+  constexpr uint16_t kMask = 3;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], CS);  // released by every CTA of the cluster
+      tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(tfull, 1);
-    tc::mbar_init(tempty, 4 * MB);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 2 * 4 * kEpiGroups);  // every epilogue warp of both CTAs of the pair
+    }
     tc::fence_barrier_init();
-    tc::tma_prefetch(&tA_hi);
-    tc::tma_prefetch(&tA_lo);
-    tc::tma_prefetch(&tB_hi);
-    tc::tma_prefetch(&tB_lo);
+    tc::tma_prefetch(&tX_hi);
+    tc::tma_prefetch(&tX_lo);
+    tc::tma_prefetch(&tW_hi);
+    tc::tma_prefetch(&tW_lo);
   }
-  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tslot);
+  if (warp == 1) tc::tmem_alloc_pair<512>(tslot);
   tc::tc_fence_before();
   __syncthreads();
-  if constexpr (CS > 1) tc::cluster_sync();  // peers' barriers initialised before any multicast
+  tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (both CTAs; bytes complete on the leader's barrier)
     if (lane == 0) {
+      const bool lw = !(a.debug_flags & 1), lx = !(a.debug_flags & 2);
       int it = 0;
-      for (int ch = 0; ch < nchunks; ++ch) {
+      for (int u = u_begin; u < u_end; ++u) {
+        const Unit un(u, npass, a.M);
+        const int v0 = un.vt * 256 + member * 128;
+        const int g = un.row0 + member * un.h;
+        const uint32_t bytes = (lw ? 2 * kWB : 0) + (lx ? 2 * un.h * kRowB : 0);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) tc::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-          const bool la = !(a.debug_flags & 1), lb = !(a.debug_flags & 2);
-          tc::mbar_arrive_expect_tx(&full[s], (la ? 2 * A_BYTES : 0) + (lb ? 2 * B_BYTES : 0));
-          uint8_t *st = smem + s * STAGE_BYTES;
+          const int s = it % kStages;
+          if (it >= kStages) tc::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          if (member == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * bytes);
+          const uint32_t bar = tc::mapa_shared(tc::smem_u32(&full[s]), leader);
+          uint8_t *st = smem + s * kStageB;
           const int kx = kb * kBK;
-          if (la) {
-#pragma unroll
-            for (int j = 0; j < 2 * MB; ++j) {
-              if (j % CS != (int)crank) continue;
-              const int mb = j >> 1;
-              const int row = (ch * MB + mb) * 128;
-              uint8_t *dst = st + (j & 1) * A_BYTES + mb * 128 * kBK * 4;
-              const CUtensorMap *map = (j & 1) ? &tA_lo : &tA_hi;
-              if constexpr (CS > 1)
-                tc::tma_load_2d_mc(dst, map, &full[s], kx, row, kAll);
-              else
-                tc::tma_load_2d(dst, map, &full[s], kx, row);
-            }
+          if (lw) {
+            tc::tma_load_2d_pair(st, &tW_hi, bar, kx, v0);
+            tc::tma_load_2d_pair(st + kWB, &tW_lo, bar, kx, v0);
           }
-          if (lb) {
-            tc::tma_load_2d(st + 2 * A_BYTES, &tB_hi, &full[s], kx, n0);
-            tc::tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tB_lo, &full[s], kx, n0);
+          if (lx) {
+            for (int r = 0; r < un.h; r += kBoxR) {
+              tc::tma_load_2d_pair(st + 2 * kWB + r * kRowB, &tX_hi, bar, kx, g + r);
+              tc::tma_load_2d_pair(st + 2 * kWB + kXB + r * kRowB, &tX_lo, bar, kx, g + r);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread)
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(128, BN);
-      int it = 0;
-      for (int ch = 0; ch < nchunks; ++ch) {
-        if (ch > 0) {
-          tc::mbar_wait(tempty, (ch - 1) & 1);
+    // ---------------- MMA issuer (leader CTA, one thread); accumulators
+    // alternate between two TMEM buffers so the epilogue of unit t overlaps
+    // the mainloop of unit t + 1
+    if (lane == 0 && member == 0) {
+      int it = 0, ti = 0;
+      for (int u = u_begin; u < u_end; ++u, ++ti) {
+        const Unit un(u, npass, a.M);
+        const int buf = ti & 1;
+        const uint32_t acc = tmem + buf * kAccCols;
+        const uint32_t idesc = tc::idesc_tf32(256, un.n);
+        if (ti >= 2) {
+          tc::mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1);  // both epilogues drained this buffer
           tc::tc_fence_after();
         }
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          tc::mbar_wait(&full[s], (it / STAGES) & 1);
+          const int s = it % kStages;
+          tc::mbar_wait(&full[s], (it / kStages) & 1);
           tc::tc_fence_after();
-          const uint32_t base = tc::smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t base = tc::smem_u32(smem + s * kStageB);
 #pragma unroll
           for (int k2 = 0; k2 < ((a.debug_flags & 4) ? 0 : kBK / 8); ++k2) {
-            const uint32_t koff = k2 * 32;  // 8 tf32 = 32 bytes along K
-            const uint64_t bh = tc::desc_kmajor_sw64(base + 2 * A_BYTES + koff);
-            const uint64_t bl = tc::desc_kmajor_sw64(base + 2 * A_BYTES + B_BYTES + koff);
-#pragma unroll
-            for (int mb = 0; mb < MB; ++mb) {
-              const uint64_t ah = tc::desc_kmajor_sw64(base + mb * 128 * kBK * 4 + koff);
-              const uint64_t al = tc::desc_kmajor_sw64(base + A_BYTES + mb * 128 * kBK * 4 + koff);
-              const uint32_t d = tmem + mb * BN;
-              tc::mma_tf32(d, ah, bh, idesc, (kb | k2) != 0);  // hi * hi
-              tc::mma_tf32(d, ah, bl, idesc, 1);               // hi * lo
-              tc::mma_tf32(d, al, bh, idesc, 1);               // lo * hi
-            }
+            const uint32_t koff = k2 * 32;
+            const uint64_t awh = tc::desc_kmajor_sw128(base + koff);
+            const uint64_t awl = tc::desc_kmajor_sw128(base + kWB + koff);
+            const uint64_t bh = tc::desc_kmajor_sw128(base + 2 * kWB + koff);
+            const uint64_t bl = tc::desc_kmajor_sw128(base + 2 * kWB + kXB + koff);
+            const uint32_t acc0 = (kb | k2) != 0;
+            tc::mma_tf32_pair(acc, awh, bh, idesc, acc0);
+            tc::mma_tf32_pair(acc, awh, bl, idesc, 1);
+            tc::mma_tf32_pair(acc, awl, bh, idesc, 1);
           }
-          if constexpr (CS > 1)
-            tc::mma_commit_mc(&empty[s], kAll);  // slot free in every CTA's ring
-          else
-            tc::mma_commit(&empty[s]);  // smem stage free once these MMAs drain
+          tc::mma_commit_pair_mc(&empty[s], (uint16_t)(kMask << leader));
         }
-        tc::mma_commit(tfull);  // accumulators of this chunk complete
+        tc::mma_commit_pair_mc(&tfull[buf], (uint16_t)(kMask << leader));
       }
     }
   } else {
-    // ---------------- epilogue: 4*MB warps; warp group mb drains M-block mb,
-    // thread = one row (TMEM lane) of the tile
-    const int lg = warp & 3;  // TMEM lane quarter this warp may access
-    const int mb = (warp - 2) >> 2;
-    const int nt = blockIdx.x;
-    for (int c = threadIdx.x - 64; c < BN; c += 128 * MB)
-      sbias[c] = (n0 + c < a.N) ? __ldg(a.bias + n0 + c) : -INFINITY;
-    asm volatile("bar.sync 1, %0;" ::"n"(128 * MB) : "memory");  // epilogue warps only
-    for (int ch = 0; ch < nchunks; ++ch) {
-      tc::mbar_wait(tfull, ch & 1);
+    // ---------------- epilogue (both CTAs): group g drains and reduces the
+    // 32-row chunks g, g + kEpiGroups, ... of each unit
+    const int lg = warp & 3;        // TMEM lane quarter this warp may access
+    const int f = lg * 32 + lane;   // vocabulary lane of this thread while draining
+    const int g = (warp - 2) / 4;
+    const int et = threadIdx.x - 64 - 128 * g;
+    const int ri = et >> 2, q = et & 3;  // (row, vocabulary quarter) while reducing
+    float *buf = tr + g * (32 * kTrRow);
+    int ti = 0, dchunk = 0;
+    const bool dstamp = a.debug_clock && blockIdx.x == 0 && et == 0 && g == 0;
+    auto stamp = [&](int pt) {
+      if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + pt] = clock64();
+    };
+    for (int u = u_begin; u < u_end; ++u, ++ti) {
+      const Unit un(u, npass, a.M);
+      const int ab = ti & 1;
+      const int v0 = un.vt * 256 + member * 128;
+      const int nt = un.vt * 2 + member;  // 128-vocab tile index of the partial outputs
+      const float bias_f = (v0 + f < a.N) ? __ldg(a.bias + v0 + f) : -INFINITY;
+      if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + 11] = clock64();
+      tc::mbar_wait(&tfull[ab], (ti >> 1) & 1);
       tc::tc_fence_after();
-      if (!(a.debug_flags & 8)) {
-        const int m = (ch * MB + mb) * 128 + lg * 32 + lane;
-        const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + mb * BN;
-        RowTop<KK> top;
-        top.init();
-        float mx = -INFINITY;
+      if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + 12] = clock64();
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = 32 * g; c0 < un.n; c0 += 32 * kEpiGroups, ++dchunk) {
+        stamp(0);
+        {
           float v[32];
-          tc::tmem_ld_32x32(tb + c0, v);
-          float cm = -INFINITY;
+          tc::tmem_ld_32x32(tmem + ab * kAccCols + ((uint32_t)(lg * 32) << 16) + c0, v);
+          float *dst = buf + lg * kTrQ + lane;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            v[i] += sbias[c0 + i];
-            cm = fmaxf(cm, v[i]);
-          }
-          mx = fmaxf(mx, cm);
-          if (cm > top.worst() && !(a.debug_flags & 16)) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (v[i] > top.worst()) top.insert(v[i], n0 + c0 + i);
-          }
+          for (int i = 0; i < 32; ++i) dst[i * kTrRow] = v[i] + bias_f;
         }
-        float se = 0.f;
-#pragma unroll 1
-        for (int c0 = 0; c0 < ((a.debug_flags & 32) ? 0 : BN); c0 += 32) {
-          float v[32];
-          tc::tmem_ld_32x32(tb + c0, v);
+        stamp(1);
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        stamp(2);
+        if (!(a.debug_flags & 8)) {
+          // thread (ri, q): logits of row c0 + ri for vocab v0 + 32 q + [0, 32);
+          // the quarter pad makes each 8-lane LDS.128 phase hit 8 bank groups
+          float x[32];
+          const float *src = buf + ri * kTrRow + q * kTrQ;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) se += expf(v[i] + sbias[c0 + i] - mx);
-        }
-        if (m < a.M && nt < a.ntiles && !(a.debug_flags & 64)) {
-          a.pmax[(long long)nt * a.M + m] = mx;
-          a.psum[(long long)nt * a.M + m] = se;
-          const long long base = ((long long)m * a.ntiles + nt) * a.kk;
+          for (int u4 = 0; u4 < 8; ++u4) {
+            const float4 t4 = *reinterpret_cast<const float4 *>(src + 4 * u4);
+            x[4 * u4] = t4.x;
+            x[4 * u4 + 1] = t4.y;
+            x[4 * u4 + 2] = t4.z;
+            x[4 * u4 + 3] = t4.w;
+          }
+          // two 16-wide half maxima, the quarter max, and sum exp(x - max)
+          // (ex2-based: x log2 e - max log2 e, one FFMA + MUFU per logit)
+          float h0 = x[0], h1 = x[16];
 #pragma unroll
-          for (int i = 0; i < KK; ++i)
-            if (i < a.kk) {
-              a.cval[base + i] = top.v[i];
-              a.ctok[base + i] = top.t[i];
+          for (int i = 1; i < 16; ++i) {
+            h0 = fmaxf(h0, x[i]);
+            h1 = fmaxf(h1, x[16 + i]);
+          }
+          float mx = fmaxf(h0, h1);
+          stamp(3);
+          float se = 0.f;
+          if (mx != -INFINITY) {
+            const float mxl = mx * 1.4426950408889634f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) se += tc::exp2f_approx(fmaf(x[i], 1.4426950408889634f, -mxl));
+          }
+          // Threshold: the KK-th largest of the row's 8 half maxima is a lower
+          // bound on the row's KK-th largest logit (those maxima are 8 distinct
+          // logits), so only logits >= thr can be in the tile's top-KK.
+          stamp(4);
+          float thr = -INFINITY;
+          if constexpr (KK <= 8) {
+            float hm[8];
+            const int lb = lane & ~3;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              hm[2 * j] = __shfl_sync(0xffffffffu, h0, lb + j);
+              hm[2 * j + 1] = __shfl_sync(0xffffffffu, h1, lb + j);
             }
+#pragma unroll
+            for (int p = 0; p < KK; ++p)
+#pragma unroll
+              for (int j = 7; j > p; --j) {
+                const float hi = fmaxf(hm[j - 1], hm[j]), lo = fminf(hm[j - 1], hm[j]);
+                hm[j - 1] = hi;
+                hm[j] = lo;
+              }
+            thr = hm[KK - 1];
+          }
+          stamp(5);
+          unsigned cand = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cand |= (x[i] >= thr ? 1u : 0u) << i;
+          stamp(6);
+          RowTop<KK> top;
+          top.init();
+          const int tbase = v0 + q * 32;
+#pragma unroll 1
+          for (; cand; cand &= cand - 1) {  // few candidates per quarter
+            const int i = __ffs(cand) - 1;
+            top.insert(src[i], tbase + i);
+          }
+          stamp(7);
+          // merge the four quarters of the row (lanes 4 ri .. 4 ri + 3)
+#pragma unroll
+          for (int o = 1; o <= 2; o <<= 1) {
+            const float omx = __shfl_xor_sync(0xffffffffu, mx, o);
+            const float ose = __shfl_xor_sync(0xffffffffu, se, o);
+            const float nmx = fmaxf(mx, omx);
+            const float a0 = (mx == -INFINITY) ? 0.f : se * expf(mx - nmx);
+            const float a1 = (omx == -INFINITY) ? 0.f : ose * expf(omx - nmx);
+            se = (q & o) ? a1 + a0 : a0 + a1;  // same operand order in both partners
+            mx = nmx;
+            merge_partner(top, o);
+          }
+          stamp(8);
+          const int m = un.row0 + c0 + ri;
+          if (q == 0 && c0 + ri < un.nr && nt < a.ntiles && !(a.debug_flags & 64)) {
+            a.pmax[(long long)nt * a.M + m] = mx;
+            a.psum[(long long)nt * a.M + m] = se;
+            const long long base = ((long long)m * a.ntiles + nt) * a.kk;
+#pragma unroll
+            for (int i = 0; i < KK; ++i)
+              if (i < a.kk) {
+                const bool ok = top.v[i] != -INFINITY;
+                a.cval[base + i] = ok ? top.v[i] : -INFINITY;
+                a.ctok[base + i] = ok ? top.t[i] : -1;
+              }
+          }
         }
+        stamp(9);
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // buffer free for the next chunk
+        stamp(10);
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(tempty);
+      if (lane == 0) tc::mbar_arrive_remote(&tempty[ab], leader);
     }
   }
+  tc::tc_fence_before();
   __syncthreads();
-  if constexpr (CS > 1) tc::cluster_sync();  // no CTA leaves while peers may still signal it
-  if (warp == 1) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc<TMEM_COLS>(tmem);
-  }
+  tc::cluster_sync();  // no CTA leaves while its pair may still signal it
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc_pair<512>(tmem);
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -261,38 +426,37 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-constexpr int kTcBN = 128, kTcMB = 3, kTcCluster = 2;
-
-// pipeline depth (env AMUN_TC_STAGES=2 trades latency hiding for 64 KB of
-// shared memory that concurrent kernels of other lanes can use)
-int tc_stages() {
-  static int v = [] {
-    const char *e = getenv("AMUN_TC_STAGES");
-    return (e && e[0] == '2') ? 2 : 3;
+// work units per pair: (256-vocab tiles x row passes) spread evenly; env
+// AMUN_LOGIT_PAIRS caps the number of CTA pairs (default: as few pairs as
+// keep the per-pair unit count at ceil(units / 74)).
+int logit_pairs(int units) {
+  static int cap = [] {
+    const char *e = getenv("AMUN_LOGIT_PAIRS");
+    return e ? std::max(1, atoi(e)) : 74;
   }();
-  return v;
+  const int per = ceil_div(units, std::min(cap, 74));
+  return ceil_div(units, per);
 }
 
-template <int KK, int kTcStages>
-void launch_t_s(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
-  auto kern = logits_tc_kernel<kTcBN, kTcMB, kTcStages, KK, kTcCluster>;
-  constexpr int stage = 2 * kTcMB * 128 * kBK * 4 + 2 * kTcBN * kBK * 4;
-  const int smem = kTcStages * stage + 1024 + 256 + kTcBN * 4;
+template <int KK>
+void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
+  auto kern = logits_pair_kernel<KK>;
   static bool attr[64] = {};
   int dev = 0;
   AMUN_CUDA(cudaGetDevice(&dev));
   if (dev >= 64 || !attr[dev]) {
-    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     if (dev < 64) attr[dev] = true;
   }
+  const int units = ceil_div(a.N, 256) * ceil_div(a.M, kUnitRows);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(ceil_div(ceil_div(a.N, kTcBN), kTcCluster) * kTcCluster);
-  cfg.blockDim = dim3(64 + 128 * kTcMB);
-  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3(2 * logit_pairs(units));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = st;
   cudaLaunchAttribute la[1];
   la[0].id = cudaLaunchAttributeClusterDimension;
-  la[0].val.clusterDim.x = kTcCluster;
+  la[0].val.clusterDim.x = 2;
   la[0].val.clusterDim.y = 1;
   la[0].val.clusterDim.z = 1;
   cfg.attrs = la;
@@ -302,7 +466,7 @@ void launch_t_s(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) 
 
 }  // namespace
 
-int logits_tc_tile_n() { return kTcBN; }
+int logits_tc_tile_n() { return 128; }
 
 CUtensorMap make_tma_2d_f32(const float *ptr, int inner, int outer, int row_stride_elems, int box_inner,
                             int box_outer) {
@@ -322,19 +486,11 @@ CUtensorMap make_tma_2d_f32(const float *ptr, int inner, int outer, int row_stri
 LogitTcMaps make_logit_maps(const float *t_hi, const float *t_lo, int R, int K, int ldt, const float *w_hi,
                             const float *w_lo, int V) {
   LogitTcMaps m;
-  m.a_hi = make_tma_2d_f32(t_hi, K, R, ldt, kBK, 128);
-  m.a_lo = make_tma_2d_f32(t_lo, K, R, ldt, kBK, 128);
-  m.b_hi = make_tma_2d_f32(w_hi, K, V, K, kBK, kTcBN);
-  m.b_lo = make_tma_2d_f32(w_lo, K, V, K, kBK, kTcBN);
+  m.a_hi = make_tma_2d_f32(t_hi, K, R, ldt, kBK, kBoxR);
+  m.a_lo = make_tma_2d_f32(t_lo, K, R, ldt, kBK, kBoxR);
+  m.b_hi = make_tma_2d_f32(w_hi, K, V, K, kBK, 128);
+  m.b_lo = make_tma_2d_f32(w_lo, K, V, K, kBK, 128);
   return m;
-}
-
-template <int KK>
-void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
-  if (tc_stages() == 2)
-    launch_t_s<KK, 2>(maps, a, st);
-  else
-    launch_t_s<KK, 3>(maps, a, st);
 }
 
 void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {

@@ -14,6 +14,7 @@ struct LogitTcArgs {
   float *cval;         // [M][ntiles][kk]
   int *ctok;
   int debug_flags = 0;  // microbenchmark knobs: 1 skip A loads, 2 skip B loads, 4 skip MMA, 8 skip epilogue
+  long long *debug_clock = nullptr;  // microbenchmark: per-chunk clock64 stamps of CTA 0
 };
 
 struct LogitTcMaps {

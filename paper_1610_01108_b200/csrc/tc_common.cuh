@@ -16,6 +16,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Aligned pointer into dynamic shared memory by pointer arithmetic on the
+// __shared__ base (an integer round trip would lose the address space and
+// turn every access into a generic LD/ST).
+template <uint32_t ALIGN>
+__device__ __forceinline__ uint8_t *align_smem(uint8_t *base) {
+  return base + ((ALIGN - (smem_u32(base) & (ALIGN - 1))) & (ALIGN - 1));
+}
+
 // ------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -101,6 +109,12 @@ __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t addr) {
                : "r"(addr)
                : "memory");
   return v;
+}
+
+// Arrive on the mbarrier at the same offset in CTA `rank` of the cluster.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(smem_u32(bar), rank))
+               : "memory");
 }
 
 // ------------------------------------------------------------- TMEM
@@ -231,6 +245,14 @@ __device__ __forceinline__ void tmem_ld_32x32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 2^x via the SFU (ex2.approx: ~2 ulp), for sums of exponentials whose
+// result only feeds a log-normaliser.
+__device__ __forceinline__ float exp2f_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // fp32 -> (hi, lo) with hi exactly representable in tf32 (low 13 mantissa

@@ -34,12 +34,12 @@ int main(int argc, char **argv) {
   LogitTcMaps maps = make_logit_maps(thi, tlo, R, K, K, whi, wlo, V);
   const char *names[] = {"full", "no A loads", "no B loads", "no A/B loads", "no MMA", "no epilogue",
                          "loads only (no MMA, no epi)", "MMA only (no loads, no epi)", "no top-k", "no sum pass",
-                         "no stores", "no topk/sum/stores"};
-  const int flags[] = {0, 1, 2, 3, 4, 8, 12, 11, 16, 32, 64, 112};
+                         "no stores", "no topk/sum/stores", "no merge", "no topk/sum/merge/stores"};
+  const int flags[] = {0, 1, 2, 3, 4, 8, 12, 11, 16, 32, 64, 112, 128, 240};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int v = 0; v < 12; ++v) {
+  for (int v = 0; v < 14; ++v) {
     LogitTcArgs a{R, V, K, bias, kk, ntiles, pmax, psum, cval, ctok};
     a.debug_flags = flags[v];
     for (int i = 0; i < 3; ++i) launch_logits_tc(maps, a, 0);
@@ -52,6 +52,24 @@ int main(int argc, char **argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     cudaError_t err = cudaGetLastError();
     printf("R=%d %-30s %8.1f us  %s\n", R, names[v], 1000 * ms / it, cudaGetErrorString(err));
+  }
+  {
+    long long *dclk;
+    cudaMalloc(&dclk, sizeof(long long) * 64 * 16);
+    cudaMemset(dclk, 0, sizeof(long long) * 64 * 16);
+    LogitTcArgs a{R, V, K, bias, kk, ntiles, pmax, psum, cval, ctok};
+    a.debug_clock = dclk;
+    launch_logits_tc(maps, a, 0);
+    cudaDeviceSynchronize();
+    std::vector<long long> c(64 * 16);
+    cudaMemcpy(c.data(), dclk, sizeof(long long) * 64 * 16, cudaMemcpyDeviceToHost);
+    printf("chunk: wait_tfull | drain | bar | ldmax | exp | thr | mask | cand | merge | store | bar2   (cycles)\n");
+    for (int ch = 0; ch < 12; ++ch) {
+      long long *r = &c[ch * 16];
+      printf("%2d: %6lld | %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", ch, r[12] ? r[12] - r[11] : 0,
+             r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5], r[7] - r[6], r[8] - r[7],
+             r[9] - r[8], r[10] - r[9]);
+    }
   }
   return 0;
 }

@@ -16,7 +16,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {  // bf16 x bf16
 template <int KIND, int CG>  // KIND 0 tf32, 1 bf16; CG cta_group
 __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int N, int iters, unsigned long long *cycles) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = tc::align_smem<1024>(smem_raw);  // stays in the shared address space (LDS/STS)
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t bar;
   const int warp = threadIdx.x / 32;

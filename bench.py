@@ -149,6 +149,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sentences", type=int, default=0)
     ap.add_argument("--subset", type=int, default=0, help="profiling only: stratified subset of the workload")
+    ap.add_argument("--bucket", type=int, default=0,
+                    help="profiling only: the N sentences around the median length (one realistic length bucket)")
     args = ap.parse_args()
     rank, world, local = env_rank()
 
@@ -160,6 +162,10 @@ def main() -> None:
     sentences = wl.corpus()
     if args.subset:
         sentences = cpu_sample(sentences, args.subset)
+    if args.bucket:
+        order = sorted(range(len(sentences)), key=lambda i: (len(sentences[i]), i))
+        mid = len(order) // 2
+        sentences = [sentences[i] for i in order[max(0, mid - args.bucket // 2):][:args.bucket]]
     cfg = {"workload": f"{wl.name}: {wl.description}", "sentences": wl.sentences, "beam": wl.beam,
            "bucket": wl.batch, "cap": f"{wl.max_len_factor}*J+{wl.max_len_offset}",
            "src_tokens": sum(map(len, sentences)),

@@ -12,6 +12,18 @@ namespace amun {
 // fp32 rounding of the 1024-term energy sum it feeds.
 __device__ __forceinline__ float tanh_attn(float x) { return 1.0f - __fdividef(2.0f, __expf(2.0f * x) + 1.0f); }
 
+__device__ __forceinline__ float tc_rcp(float x) {  // rcp.approx (SFU), as __fdividef
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float tc_exp2(float x) {  // ex2.approx (SFU)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
   extern __shared__ float sm[];
   float *q = sm;              // [da]
@@ -108,58 +120,127 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
 //     thread = column, ctx[r, c] = sum_j alpha[r, j] H_bj[c] over the rows.
 // Energies and context sums run in a fixed order, independent of which other
 // sentences share the launch.
-constexpr int kEnergyWarps = 8;  // source positions per energy CTA
+constexpr int kEnergyWarps = 8;  // warps per energy CTA
+constexpr int kEnergyPos = 8;    // source positions per energy CTA (one per warp)
+constexpr float kTwoLog2e = 2.8853900817779268f;  // 2 / ln 2: e^{2x} = 2^{x kTwoLog2e}
+constexpr float kFactorSafe = 20.f;  // |p|, |q| below this: e^{2p} e^{2q} cannot overflow
 
-__global__ void __launch_bounds__(32 * kEnergyWarps) attn_energy_kernel(AttnArgs a) {
-  extern __shared__ float qs[];  // [na][da] query rows of this sentence
+// tanh(p + q) = 1 - 2 / (1 + e^{2p} e^{2q}): e^{2p} is computed once per
+// (position, element) and shared by the beam rows, e^{2q} once per (row,
+// element) and shared by all positions, leaving one SFU op (rcp) per tanh
+// instead of two.  Rows or positions with a factor outside +-kFactorSafe take
+// the direct formula (warp-uniform branch).
+template <int KA>
+__global__ void __launch_bounds__(32 * kEnergyWarps, 3) attn_energy_kernel(AttnArgs a) {
+  extern __shared__ float qs[];  // [k][da] query rows, [k][da] e^{2q}, [da] v, then [k] "large" flags
   const int b = blockIdx.y;
   if (a.n_act && a.done[b]) return;
   const int J = a.len[b];
-  const int j0 = blockIdx.x * kEnergyWarps;
+  const int j0 = blockIdx.x * kEnergyPos;
   if (j0 >= J) return;
   const int k = a.rows_per_sent;
   const int na = a.n_act ? a.n_act[b] : k;
-  for (int i = threadIdx.x; i < na * a.da; i += blockDim.x) {
-    const int r = i / a.da, c = i - r * a.da;
-    qs[i] = __ldg(a.Q + (long long)(b * k + r) * a.ldq + c);
+  float *eq = qs + k * a.da;
+  float *vs = eq + k * a.da;
+  int *qbig = reinterpret_cast<int *>(vs + a.da);
+  for (int i = threadIdx.x; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
+  {
+    // query rows: batches of 4 independent loads per thread before any use
+    const int n = na * a.da;
+    for (int i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {
+      float x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * blockDim.x;
+        const int r = i / a.da, c = i - r * a.da;
+        x[u] = i < n ? __ldg(a.Q + (long long)(b * k + r) * a.ldq + c) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < n) {
+          qs[i] = x[u];
+          eq[i] = tc_exp2(x[u] * kTwoLog2e);
+        }
+      }
+    }
   }
   __syncthreads();
-  const int lane = threadIdx.x % 32;
-  const int j = j0 + threadIdx.x / 32;
-  if (j >= J) return;
-  const float *pj = a.P + ((long long)b * a.jmax + j) * a.da;
-  float p[32], v[32];
-#pragma unroll
-  for (int u = 0; u < 32; ++u) {
-    const int i = lane + 32 * u;
-    p[u] = i < a.da ? __ldg(pj + i) : 0.f;
-    v[u] = i < a.da ? __ldg(a.v + i) : 0.f;
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  int anybig = 0;
+  for (int r = warp; r < na; r += kEnergyWarps) {
+    float m = 0.f;
+    for (int c = lane; c < a.da; c += 32) m = fmaxf(m, fabsf(qs[r * a.da + c]));
+    m = warp_max(m);
+    if (lane == 0) qbig[r] = m > kFactorSafe;
   }
-  for (int r = 0; r < na; ++r) {
-    const float *qr = qs + r * a.da;
-    float s0 = 0.f, s1 = 0.f;
+  __syncthreads();
+  for (int r = 0; r < na; ++r) anybig |= qbig[r];
+  for (int j = j0 + warp; j < min(J, j0 + kEnergyPos); j += kEnergyWarps) {
+    const float *pj = a.P + ((long long)b * a.jmax + j) * a.da;
+    float ep[32];
+    float pm = 0.f;
 #pragma unroll
-    for (int u = 0; u < 32; u += 2) {
+    for (int u = 0; u < 32; ++u) {
       const int i = lane + 32 * u;
-      if (i < a.da) s0 = fmaf(v[u], tanh_attn(p[u] + qr[i]), s0);
-      if (i + 32 < a.da) s1 = fmaf(v[u + 1], tanh_attn(p[u + 1] + qr[i + 32]), s1);
+      const float p = i < a.da ? __ldg(pj + i) : 0.f;
+      pm = fmaxf(pm, fabsf(p));
+      ep[u] = tc_exp2(p * kTwoLog2e);
     }
-    const float s = warp_sum(s0 + s1);
-    if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = s;
+    const bool pbig = warp_max(pm) > kFactorSafe;
+    if (!pbig && !anybig && na == KA && a.da == 1024) {
+      // exact row count, full-width rows: KA independent accumulation
+      // chains per lane, no predication in the inner loop
+      float acc[KA];
+#pragma unroll
+      for (int r = 0; r < KA; ++r) acc[r] = 0.f;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int i = lane + 32 * u;
+        const float vi = vs[i];
+#pragma unroll
+        for (int r = 0; r < KA; ++r)
+          acc[r] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], eq[r * 1024 + i], 1.0f)), 1.0f), acc[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < KA; ++r) {
+        const float sum = warp_sum(acc[r]);
+        if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = sum;
+      }
+    } else {
+      for (int r = 0; r < na; ++r) {
+        float s0 = 0.f;
+        const float *qr = qs + r * a.da;
+        const float *er = eq + r * a.da;
+        const bool direct = pbig || qbig[r];
+        for (int u = 0; u < 32; ++u) {
+          const int i = lane + 32 * u;
+          if (i < a.da)
+            s0 = fmaf(vs[i],
+                      direct ? tanh_attn(__ldg(pj + i) + qr[i]) : 1.0f - __fdividef(2.0f, fmaf(ep[u], er[i], 1.0f)),
+                      s0);
+        }
+        const float sum = warp_sum(s0);
+        if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = sum;
+      }
+    }
   }
 }
 
-constexpr int kCtxThreads = 128;  // thread = 4 consecutive columns (float4)
-constexpr int kCtxRows = 8;       // row accumulators per pass
+constexpr int kCtxCols = 128;    // threads per J-group: thread = 4 consecutive columns (float4)
+constexpr int kCtxGroups = 2;    // J-groups: group g sums positions j = g, g + 2, ... (then fixed-order add)
+constexpr int kCtxRows = 8;      // row accumulators per pass
+constexpr int kCtxUnroll = 8;    // independent 16-byte loads in flight per thread
 
-__global__ void __launch_bounds__(kCtxThreads) attn_context_kernel(AttnArgs a) {
-  extern __shared__ float al[];  // [k][jmax]
+__global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(AttnArgs a) {
+  extern __shared__ float al[];  // [k][jmax] alpha, then [kCtxRows][kCtxCols] float4 partials of group 1
   const int b = blockIdx.x;
   if (a.n_act && a.done[b]) return;
   const int k = a.rows_per_sent;
   const int na = a.n_act ? a.n_act[b] : k;
   const int J = a.len[b];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
+  float4 *part = reinterpret_cast<float4 *>(al + ((k * a.jmax + 3) & ~3));
   // masked softmax over j < J, one warp per row (nnet.py:137-139)
   for (int r = warp; r < na; r += nw) {
     const float *er = a.energy + (long long)(b * k + r) * a.jmax;
@@ -185,83 +266,115 @@ __global__ void __launch_bounds__(kCtxThreads) attn_context_kernel(AttnArgs a) {
     }
   }
   __syncthreads();
-  const int c = (blockIdx.y * kCtxThreads + tid) * 4;
-  if (c >= a.dh2) return;
-  const float4 *Hb = reinterpret_cast<const float4 *>(a.H + (long long)b * a.jmax * a.dh2 + c);
+  const int grp = tid / kCtxCols, ct = tid % kCtxCols;
+  const int c = (blockIdx.y * kCtxCols + ct) * 4;
+  const bool live = c < a.dh2;
+  const float4 *Hb = reinterpret_cast<const float4 *>(a.H + (long long)b * a.jmax * a.dh2 + (live ? c : 0));
   const int hs = a.dh2 / 4;  // float4 stride between positions
   for (int r0 = 0; r0 < na; r0 += kCtxRows) {
     float4 acc[kCtxRows];
 #pragma unroll
     for (int r = 0; r < kCtxRows; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    int j = 0;
-    for (; j + 8 <= J; j += 8) {
-      float4 h[8];
+    if (live) {
+      int j = grp;
+      for (; j + kCtxGroups * (kCtxUnroll - 1) < J; j += kCtxGroups * kCtxUnroll) {
+        float4 h[kCtxUnroll];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) h[jj] = __ldg(Hb + (long long)(j + jj) * hs);
+        for (int jj = 0; jj < kCtxUnroll; ++jj) h[jj] = __ldg(Hb + (long long)(j + kCtxGroups * jj) * hs);
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
+        for (int jj = 0; jj < kCtxUnroll; ++jj)
+#pragma unroll
+          for (int r = 0; r < kCtxRows; ++r)
+            if (r0 + r < na) {
+              const float w = al[(r0 + r) * a.jmax + j + kCtxGroups * jj];
+              acc[r].x = fmaf(w, h[jj].x, acc[r].x);
+              acc[r].y = fmaf(w, h[jj].y, acc[r].y);
+              acc[r].z = fmaf(w, h[jj].z, acc[r].z);
+              acc[r].w = fmaf(w, h[jj].w, acc[r].w);
+            }
+      }
+      for (; j < J; j += kCtxGroups) {
+        const float4 h = __ldg(Hb + (long long)j * hs);
 #pragma unroll
         for (int r = 0; r < kCtxRows; ++r)
           if (r0 + r < na) {
-            const float w = al[(r0 + r) * a.jmax + j + jj];
-            acc[r].x = fmaf(w, h[jj].x, acc[r].x);
-            acc[r].y = fmaf(w, h[jj].y, acc[r].y);
-            acc[r].z = fmaf(w, h[jj].z, acc[r].z);
-            acc[r].w = fmaf(w, h[jj].w, acc[r].w);
+            const float w = al[(r0 + r) * a.jmax + j];
+            acc[r].x = fmaf(w, h.x, acc[r].x);
+            acc[r].y = fmaf(w, h.y, acc[r].y);
+            acc[r].z = fmaf(w, h.z, acc[r].z);
+            acc[r].w = fmaf(w, h.w, acc[r].w);
           }
-    }
-    for (; j < J; ++j) {
-      const float4 h = __ldg(Hb + (long long)j * hs);
-#pragma unroll
-      for (int r = 0; r < kCtxRows; ++r)
-        if (r0 + r < na) {
-          const float w = al[(r0 + r) * a.jmax + j];
-          acc[r].x = fmaf(w, h.x, acc[r].x);
-          acc[r].y = fmaf(w, h.y, acc[r].y);
-          acc[r].z = fmaf(w, h.z, acc[r].z);
-          acc[r].w = fmaf(w, h.w, acc[r].w);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < kCtxRows; ++r) {
-      if (r0 + r >= na) break;
-      const long long o = (long long)(b * k + r0 + r) * a.ldctx + c;
-      const float vals[4] = {acc[r].x, acc[r].y, acc[r].z, acc[r].w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a.ctx[o + u] = vals[u];
-        store_split(a.ctx_hi, a.ctx_lo, o + u, vals[u]);
       }
     }
+    // fixed-order combine of the two J-groups: ctx = sum(even j) + sum(odd j)
+    if (grp == 1) {
+#pragma unroll
+      for (int r = 0; r < kCtxRows; ++r) part[r * kCtxCols + ct] = acc[r];
+    }
+    __syncthreads();
+    if (grp == 0 && live) {
+#pragma unroll
+      for (int r = 0; r < kCtxRows; ++r) {
+        if (r0 + r >= na) break;
+        const float4 o4 = part[r * kCtxCols + ct];
+        const float vals[4] = {acc[r].x + o4.x, acc[r].y + o4.y, acc[r].z + o4.z, acc[r].w + o4.w};
+        const long long o = (long long)(b * k + r0 + r) * a.ldctx + c;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a.ctx[o + u] = vals[u];
+          store_split(a.ctx_hi, a.ctx_lo, o + u, vals[u]);
+        }
+      }
+    }
+    __syncthreads();
   }
+}
+
+template <int KA>
+static void launch_energy(const AttnArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
+  auto kern = attn_energy_kernel<KA>;
+  static size_t attr_q[64] = {};
+  int dev = 0;
+  AMUN_CUDA(cudaGetDevice(&dev));
+  if (smem > 48 * 1024 && (dev >= 64 || attr_q[dev] < smem)) {
+    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (dev < 64) attr_q[dev] = smem;
+  }
+  kern<<<grid, 32 * kEnergyWarps, smem, st>>>(a);
 }
 
 int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   if (R <= 0) return 0;
   const int k = a.rows_per_sent;
   const size_t smem = sizeof(float) * (size_t)k * a.jmax;
-  const size_t smem_q = sizeof(float) * (size_t)k * a.da;
-  if (a.energy && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && smem <= 200 * 1024 && smem_q <= 200 * 1024) {
+  const size_t smem_ctx = sizeof(float) * (((size_t)k * a.jmax + 3) & ~size_t(3)) + sizeof(float4) * kCtxRows * kCtxCols;
+  const size_t smem_q = sizeof(float) * (2 * (size_t)k * a.da + a.da) + sizeof(int) * (size_t)k;
+  if (a.energy && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && smem_ctx <= 200 * 1024 && smem_q <= 200 * 1024) {
     const int B = R / k;
-    static size_t attr_q[64] = {};
-    int dev = 0;
-    AMUN_CUDA(cudaGetDevice(&dev));
-    if (smem_q > 48 * 1024 && (dev >= 64 || attr_q[dev] < smem_q)) {
-      AMUN_CUDA(cudaFuncSetAttribute(attn_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      if (dev < 64) attr_q[dev] = smem_q;
+    const dim3 eg(ceil_div(a.jmax, kEnergyPos), B);
+    switch (k) {  // exact beam width: no predicated-off rows in the inner loop
+      case 1: launch_energy<1>(a, eg, smem_q, st); break;
+      case 2: launch_energy<2>(a, eg, smem_q, st); break;
+      case 3: launch_energy<3>(a, eg, smem_q, st); break;
+      case 4: launch_energy<4>(a, eg, smem_q, st); break;
+      case 5: launch_energy<5>(a, eg, smem_q, st); break;
+      case 6: launch_energy<6>(a, eg, smem_q, st); break;
+      case 8: launch_energy<8>(a, eg, smem_q, st); break;
+      case 10: launch_energy<10>(a, eg, smem_q, st); break;
+      case 12: launch_energy<12>(a, eg, smem_q, st); break;
+      default: launch_energy<16>(a, eg, smem_q, st); break;
     }
-    attn_energy_kernel<<<dim3(ceil_div(a.jmax, kEnergyWarps), B), 32 * kEnergyWarps, smem_q, st>>>(a);
     AMUN_CHECK_LAUNCH();
-    if (smem > 48 * 1024) {
+    if (smem_ctx > 48 * 1024) {
       static size_t attr_set[64] = {};
       int dev = 0;
       AMUN_CUDA(cudaGetDevice(&dev));
-      if (dev >= 64 || attr_set[dev] < smem) {
+      if (dev >= 64 || attr_set[dev] < smem_ctx) {
         AMUN_CUDA(cudaFuncSetAttribute(attn_context_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        if (dev < 64) attr_set[dev] = smem;
+        if (dev < 64) attr_set[dev] = smem_ctx;
       }
     }
-    attn_context_kernel<<<dim3(B, ceil_div(a.dh2, 4 * kCtxThreads)), kCtxThreads, smem, st>>>(a);
+    attn_context_kernel<<<dim3(B, ceil_div(a.dh2, 4 * kCtxCols)), kCtxCols * kCtxGroups, smem_ctx, st>>>(a);
     AMUN_CHECK_LAUNCH();
     return 2;
   }

@@ -150,6 +150,7 @@ struct EncBufs {
 struct DecBufs {
   float *XS, *Sn, *Q, *Z, *RH, *XH, *T, *L;
   float *En = nullptr;  // attention energies [R][jmax]
+  float *EQ = nullptr;  // e^{2q} of the attention query rows [R][da]
   float *T_hi = nullptr, *T_lo = nullptr;  // 3xTF32 split of t (tensor-core logits)
   // 3xTF32 splits of the tensor-core GEMM A operands
   float *XSh = nullptr, *XSl = nullptr, *RHh = nullptr, *RHl = nullptr, *Snh = nullptr, *Snl = nullptr;
@@ -170,6 +171,7 @@ void carve_enc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
 void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, int jmax, bool full_logits) {
   const int dh = m->d.d_h, da = m->d.d_att, de = m->d.d_emb;
   d.En = cv.take<float>((size_t)R * jmax);
+  d.EQ = cv.take<float>((size_t)R * da);
   d.XS = cv.take<float>((size_t)R * m->xs_w);
   d.Sn = cv.take<float>((size_t)R * dh);
   d.Q = cv.take<float>((size_t)R * da);
@@ -245,7 +247,10 @@ struct TcStep {
 int tc_target_ctas() {
   static int v = [] {
     const char *e = getenv("AMUN_TC_CTAS");
-    return e ? std::max(1, atoi(e)) : 148;  // AMUN_TC_CTAS: cap on CTAs per launch
+    // AMUN_TC_CTAS caps CTAs per GEMM launch; the default (24) keeps every
+    // decoder GEMM at one K split: each launch is SM-efficient and the
+    // concurrent bucket lanes fill the machine
+    return e ? std::max(1, atoi(e)) : 24;
   }();
   return v;
 }
@@ -277,13 +282,18 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
   const int s_off = de + 2 * dh;
   c.cls = AMUN_K_QUERY;
-  if (ts)
-    gemm_tc(c, ts->q, R, ts->sq, EpiStore{d.Q, da, nullptr, 0, 0});
-  else
-    gemm(c, ga(R, da, d.XS + s_off, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
+  {
+    EpiStore eq{d.Q, da, nullptr, 0, 0};
+    eq.ex2 = d.EQ;
+    if (ts)
+      gemm_tc(c, ts->q, R, ts->sq, eq);
+    else
+      gemm(c, ga(R, da, d.XS + s_off, xs, dh, m->W_att_s, da), eq);
+  }
   AttnArgs aa{d.Q, da, e.P, e.Hann, m->v_att, d_len, jmax, da, 2 * dh, rows_per_sent, n_act, done,
               d.XS + de, xs, alpha};
   aa.energy = d.En;
+  aa.EQ = d.EQ;
   if (ts) {
     aa.ctx_hi = d.XSh + de;
     aa.ctx_lo = d.XSl + de;
@@ -452,7 +462,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // small kernels of one bucket overlap with another bucket's GEMMs (every
   // bucket is still one batch of <= max_batch sentences).
   const char *lanes_env = getenv("AMUN_LANES");
-  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 6;
+  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 8;
   if (o.profile) n_lanes = 1;  // per-launch event timing wants one ordered stream
   n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
   const char *no_graph = getenv("AMUN_NO_GRAPH");
@@ -982,9 +992,12 @@ void hook_step(amun_model *m, const float *s, const int32_t *y_prev, int R, cons
   build_rows_kernel<<<R, 256, 0, c.st>>>(d.XS, xs, m->E_trg, y_prev ? d_y : nullptr, d_s, de, dh, de + 2 * dh);
   AMUN_CHECK_LAUNCH();
   if (!y_prev) {  // attention only (nnet.py:132-141)
-    gemm(c, ga(R, da, d.XS + de + 2 * dh, xs, dh, m->W_att_s, da), EpiStore{d.Q, da, nullptr, 0, 0});
+    EpiStore eq{d.Q, da, nullptr, 0, 0};
+    eq.ex2 = d.EQ;
+    gemm(c, ga(R, da, d.XS + de + 2 * dh, xs, dh, m->W_att_s, da), eq);
     AttnArgs aa{d.Q, da, e.P, e.Hann, m->v_att, d_len, J, da, 2 * dh, R, nullptr, nullptr, d.XS + de, xs, d_alpha};
     aa.energy = d.En;
+    aa.EQ = d.EQ;
     launch_attention(aa, R, c.st);
   } else {
     LogitOut lo{false, 0, 0, nullptr, nullptr, nullptr, nullptr};

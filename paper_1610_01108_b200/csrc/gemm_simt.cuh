@@ -233,10 +233,16 @@ struct EpiStore {
   int act;
   long long c_zs;
   float *hi = nullptr, *lo = nullptr;  // optional 3xTF32 split copies (ldc, no z)
+  float *ex2 = nullptr;  // optional e^{2v} (attention query rows: factored tanh, kernels.cu)
   __device__ void operator()(int m, int n, float v, int z) const {
     if (bias) v += bias[n];
     if (act == 1) v = tanhf(v);
     if (C) C[z * c_zs + (long long)m * ldc + n] = v;
+    if (ex2) {
+      float y;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(v * 2.8853900817779268f));
+      ex2[(long long)m * ldc + n] = y;
+    }
     if (hi) {
       const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
       hi[(long long)m * ldc + n] = h;
@@ -336,7 +342,7 @@ struct EpiEncB {
 
 // Logit epilogue, fused mode: per (row, N-tile) partial log-sum-exp and the
 // tile's top-kk (logit desc, token asc).  Full logits never reach HBM.
-//   pmax/psum: [ntiles][M]   cval/ctok: [M][ntiles][kk]
+//   pmax/psum: [M][ntiles]   cval/ctok: [M][ntiles][kk]
 struct EpiLogitTopK {
   static constexpr bool kTile = true;
   const float *bias;
@@ -366,8 +372,8 @@ struct EpiLogitTopK {
         if (ok[q]) se += expf(v[q] - mx);
       se = warp_sum(se);
       if (lane == 0) {
-        pmax[(long long)nt * M + m] = mx;
-        psum[(long long)nt * M + m] = se;
+        pmax[(long long)m * ntiles + nt] = mx;
+        psum[(long long)m * ntiles + nt] = se;
       }
       // kk passes of "best key strictly below the previous pick"
       double lv = INFINITY;

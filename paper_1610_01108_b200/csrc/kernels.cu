@@ -132,7 +132,7 @@ constexpr float kFactorSafe = 20.f;  // |p|, |q| below this: e^{2p} e^{2q} canno
 // the direct formula (warp-uniform branch).
 template <int KA>
 __global__ void __launch_bounds__(32 * kEnergyWarps, 3) attn_energy_kernel(AttnArgs a) {
-  extern __shared__ float qs[];  // [k][da] query rows, [k][da] e^{2q}, [da] v, then [k] "large" flags
+  extern __shared__ float vs[];  // [da] v, then [k] "large query row" flags
   const int b = blockIdx.y;
   if (a.n_act && a.done[b]) return;
   const int J = a.len[b];
@@ -140,89 +140,73 @@ __global__ void __launch_bounds__(32 * kEnergyWarps, 3) attn_energy_kernel(AttnA
   if (j0 >= J) return;
   const int k = a.rows_per_sent;
   const int na = a.n_act ? a.n_act[b] : k;
-  float *eq = qs + k * a.da;
-  float *vs = eq + k * a.da;
   int *qbig = reinterpret_cast<int *>(vs + a.da);
-  for (int i = threadIdx.x; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
-  {
-    // query rows: batches of 4 independent loads per thread before any use
-    const int n = na * a.da;
-    for (int i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {
-      float x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * blockDim.x;
-        const int r = i / a.da, c = i - r * a.da;
-        x[u] = i < n ? __ldg(a.Q + (long long)(b * k + r) * a.ldq + c) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i < n) {
-          qs[i] = x[u];
-          eq[i] = tc_exp2(x[u] * kTwoLog2e);
-        }
-      }
-    }
-  }
-  __syncthreads();
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  int anybig = 0;
+  const int j = j0 + warp;
+  // this warp's P row first: its latency overlaps the prologue below
+  const float *pj = a.P + ((long long)b * a.jmax + min(j, J - 1)) * a.da;
+  float ep[32];
+#pragma unroll
+  for (int u = 0; u < 32; ++u) {
+    const int i = lane + 32 * u;
+    ep[u] = i < a.da ? __ldg(pj + i) : 0.f;
+  }
+  for (int i = threadIdx.x; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
   for (int r = warp; r < na; r += kEnergyWarps) {
+    const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
     float m = 0.f;
-    for (int c = lane; c < a.da; c += 32) m = fmaxf(m, fabsf(qs[r * a.da + c]));
+    for (int c = lane; c < a.da; c += 32) m = fmaxf(m, fabsf(__ldg(qr + c)));
     m = warp_max(m);
     if (lane == 0) qbig[r] = m > kFactorSafe;
   }
   __syncthreads();
+  if (j >= J) return;
+  int anybig = 0;
   for (int r = 0; r < na; ++r) anybig |= qbig[r];
-  for (int j = j0 + warp; j < min(J, j0 + kEnergyPos); j += kEnergyWarps) {
-    const float *pj = a.P + ((long long)b * a.jmax + j) * a.da;
-    float ep[32];
-    float pm = 0.f;
+  float pm = 0.f;
+#pragma unroll
+  for (int u = 0; u < 32; ++u) {
+    pm = fmaxf(pm, fabsf(ep[u]));
+    ep[u] = tc_exp2(ep[u] * kTwoLog2e);
+  }
+  const bool pbig = warp_max(pm) > kFactorSafe;
+  if (!pbig && !anybig && na == KA && a.da == 1024) {
+    // exact row count, full-width rows: KA independent accumulation chains
+    // per lane; e^{2q} rows come from the query GEMM epilogue (L1-resident)
+    const float *eqr[KA];
+#pragma unroll
+    for (int r = 0; r < KA; ++r) eqr[r] = a.EQ + (long long)(b * k + r) * a.ldq + lane;
+    float acc[KA];
+#pragma unroll
+    for (int r = 0; r < KA; ++r) acc[r] = 0.f;
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
-      const int i = lane + 32 * u;
-      const float p = i < a.da ? __ldg(pj + i) : 0.f;
-      pm = fmaxf(pm, fabsf(p));
-      ep[u] = tc_exp2(p * kTwoLog2e);
+      const float vi = vs[lane + 32 * u];
+#pragma unroll
+      for (int r = 0; r < KA; ++r)
+        acc[r] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], __ldg(eqr[r] + 32 * u), 1.0f)), 1.0f), acc[r]);
     }
-    const bool pbig = warp_max(pm) > kFactorSafe;
-    if (!pbig && !anybig && na == KA && a.da == 1024) {
-      // exact row count, full-width rows: KA independent accumulation
-      // chains per lane, no predication in the inner loop
-      float acc[KA];
 #pragma unroll
-      for (int r = 0; r < KA; ++r) acc[r] = 0.f;
-#pragma unroll
+    for (int r = 0; r < KA; ++r) {
+      const float sum = warp_sum(acc[r]);
+      if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = sum;
+    }
+  } else {
+    for (int r = 0; r < na; ++r) {
+      float s0 = 0.f;
+      const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
+      const float *er = a.EQ + (long long)(b * k + r) * a.ldq;
+      const bool direct = pbig || qbig[r];
       for (int u = 0; u < 32; ++u) {
         const int i = lane + 32 * u;
-        const float vi = vs[i];
-#pragma unroll
-        for (int r = 0; r < KA; ++r)
-          acc[r] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], eq[r * 1024 + i], 1.0f)), 1.0f), acc[r]);
+        if (i < a.da)
+          s0 = fmaf(vs[i],
+                    direct ? tanh_attn(__ldg(pj + i) + __ldg(qr + i))
+                           : 1.0f - __fdividef(2.0f, fmaf(ep[u], __ldg(er + i), 1.0f)),
+                    s0);
       }
-#pragma unroll
-      for (int r = 0; r < KA; ++r) {
-        const float sum = warp_sum(acc[r]);
-        if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = sum;
-      }
-    } else {
-      for (int r = 0; r < na; ++r) {
-        float s0 = 0.f;
-        const float *qr = qs + r * a.da;
-        const float *er = eq + r * a.da;
-        const bool direct = pbig || qbig[r];
-        for (int u = 0; u < 32; ++u) {
-          const int i = lane + 32 * u;
-          if (i < a.da)
-            s0 = fmaf(vs[i],
-                      direct ? tanh_attn(__ldg(pj + i) + qr[i]) : 1.0f - __fdividef(2.0f, fmaf(ep[u], er[i], 1.0f)),
-                      s0);
-        }
-        const float sum = warp_sum(s0);
-        if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = sum;
-      }
+      const float sum = warp_sum(s0);
+      if (lane == 0) a.energy[(long long)(b * k + r) * a.jmax + j] = sum;
     }
   }
 }
@@ -348,8 +332,8 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   const int k = a.rows_per_sent;
   const size_t smem = sizeof(float) * (size_t)k * a.jmax;
   const size_t smem_ctx = sizeof(float) * (((size_t)k * a.jmax + 3) & ~size_t(3)) + sizeof(float4) * kCtxRows * kCtxCols;
-  const size_t smem_q = sizeof(float) * (2 * (size_t)k * a.da + a.da) + sizeof(int) * (size_t)k;
-  if (a.energy && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && smem_ctx <= 200 * 1024 && smem_q <= 200 * 1024) {
+  const size_t smem_q = sizeof(float) * (size_t)a.da + sizeof(int) * (size_t)k;
+  if (a.energy && a.EQ && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && smem_ctx <= 200 * 1024 && smem_q <= 200 * 1024) {
     const int B = R / k;
     const dim3 eg(ceil_div(a.jmax, kEnergyPos), B);
     switch (k) {  // exact beam width: no predicated-off rows in the inner loop
@@ -600,10 +584,10 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       for (int u = 0; u < kPT; ++u) {
         const int tt = lane + 32 * u;
         const bool ok = tt < sa.ntiles;
-        pm[u] = ok ? sa.pmax[(long long)tt * sa.M + r] : -INFINITY;
-        ps[u] = ok ? sa.psum[(long long)tt * sa.M + r] : 0.f;
+        pm[u] = ok ? sa.pmax[(long long)r * sa.ntiles + tt] : -INFINITY;
+        ps[u] = ok ? sa.psum[(long long)r * sa.ntiles + tt] : 0.f;
       }
-      for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, sa.pmax[(long long)tt * sa.M + r]);
+      for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, sa.pmax[(long long)r * sa.ntiles + tt]);
 #pragma unroll
       for (int u = 0; u < kPT; ++u) mx = fmaxf(mx, pm[u]);
       mx = warp_max(mx);
@@ -612,7 +596,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
 #pragma unroll
       for (int u = 0; u < kPT; ++u) s += (double)(ps[u] * expf(pm[u] - mx));
       for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) {
-        long long o = (long long)tt * sa.M + r;
+        long long o = (long long)r * sa.ntiles + tt;
         s += (double)(sa.psum[o] * expf(sa.pmax[o] - mx));
       }
       s = warp_sum_d(s);
@@ -799,24 +783,67 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   __syncthreads();
 
   // ---- phase 4: gather next-step decoder rows [E_trg[y] | . | s'_parent]
+  // (float4 granules, 8 independent loads in flight per thread)
   const int newna = s_newna, nfin = s_nfin;
+  const bool vec = (mr.de % 4 == 0) && (mr.dh % 4 == 0) && (mr.ldxs % 4 == 0) && (mr.s_off % 4 == 0);
   for (int m = 0; m < n_models; ++m) {
     float *XS = mr.XS[m];
     float *XSh = mr.XSh ? mr.XSh[m] : nullptr;
     float *XSl = mr.XSl ? mr.XSl[m] : nullptr;
     const float *Sn = mr.Sn[m];
     const float *E = mr.E_trg[m];
-    for (int i = 0; i < newna; ++i) {
-      const long long ro = (long long)(b * k + i) * mr.ldxs;
-      const float *ey = E + (long long)ch_tok[i] * mr.de;
-      const float *sp = Sn + (long long)(b * k + ch_par[i]) * mr.dh;
-      for (int c = threadIdx.x; c < mr.de; c += blockDim.x) {
-        XS[ro + c] = ey[c];
-        store_split(XSh, XSl, ro + c, ey[c]);
+    if (vec) {
+      const int qe = mr.de / 4, qrow = (mr.de + mr.dh) / 4;
+      const int total = newna * qrow;
+      for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
+        float4 v[8];
+        long long dst[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + u * blockDim.x;
+          dst[u] = -1;
+          if (idx < total) {
+            const int i = idx / qrow, c4 = idx - i * qrow;
+            const long long ro = (long long)(b * k + i) * mr.ldxs;
+            if (c4 < qe) {
+              v[u] = __ldg(reinterpret_cast<const float4 *>(E + (long long)ch_tok[i] * mr.de) + c4);
+              dst[u] = ro + 4 * c4;
+            } else {
+              v[u] = __ldg(reinterpret_cast<const float4 *>(Sn + (long long)(b * k + ch_par[i]) * mr.dh) + (c4 - qe));
+              dst[u] = ro + mr.s_off + 4 * (c4 - qe);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (dst[u] < 0) continue;
+          *reinterpret_cast<float4 *>(XS + dst[u]) = v[u];
+          if (XSh) {
+            const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            float h4[4], l4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              h4[e] = __uint_as_float(__float_as_uint(e4[e]) & 0xFFFFE000u);
+              l4[e] = e4[e] - h4[e];
+            }
+            *reinterpret_cast<float4 *>(XSh + dst[u]) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+            *reinterpret_cast<float4 *>(XSl + dst[u]) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+          }
+        }
       }
-      for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) {
-        XS[ro + mr.s_off + c] = sp[c];
-        store_split(XSh, XSl, ro + mr.s_off + c, sp[c]);
+    } else {
+      for (int i = 0; i < newna; ++i) {
+        const long long ro = (long long)(b * k + i) * mr.ldxs;
+        const float *ey = E + (long long)ch_tok[i] * mr.de;
+        const float *sp = Sn + (long long)(b * k + ch_par[i]) * mr.dh;
+        for (int c = threadIdx.x; c < mr.de; c += blockDim.x) {
+          XS[ro + c] = ey[c];
+          store_split(XSh, XSl, ro + c, ey[c]);
+        }
+        for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) {
+          XS[ro + mr.s_off + c] = sp[c];
+          store_split(XSh, XSl, ro + mr.s_off + c, sp[c]);
+        }
       }
     }
     if (mr.fin_states) {

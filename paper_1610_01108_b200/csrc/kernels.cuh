@@ -27,6 +27,7 @@ struct AttnArgs {
   float *alpha;  // optional [R][jmax]
   float *ctx_hi = nullptr, *ctx_lo = nullptr;  // optional 3xTF32 split (same layout as ctx)
   float *energy = nullptr;  // scratch [R][jmax]: enables the two-phase sentence kernels
+  const float *EQ = nullptr;  // e^{2q} rows (same layout as Q), from the query GEMM epilogue
 };
 // returns the number of kernels launched
 int launch_attention(const AttnArgs &a, int R, cudaStream_t st);

@@ -382,8 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           stamp(8);
           const int m = un.row0 + c0 + ri;
           if (q == 0 && c0 + ri < un.nr && nt < a.ntiles && !(a.debug_flags & 64)) {
-            a.pmax[(long long)nt * a.M + m] = mx;
-            a.psum[(long long)nt * a.M + m] = se;
+            a.pmax[(long long)m * a.ntiles + nt] = mx;
+            a.psum[(long long)m * a.ntiles + nt] = se;
             const long long base = ((long long)m * a.ntiles + nt) * a.kk;
 #pragma unroll
             for (int i = 0; i < KK; ++i)
@@ -432,7 +432,7 @@ EncodeTiledFn encode_fn() {
 int logit_pairs(int units) {
   static int cap = [] {
     const char *e = getenv("AMUN_LOGIT_PAIRS");
-    return e ? std::max(1, atoi(e)) : 74;
+    return e ? std::max(1, atoi(e)) : 40;
   }();
   const int per = ceil_div(units, std::min(cap, 74));
   return ceil_div(units, per);

@@ -10,7 +10,7 @@ struct LogitTcArgs {
   int M, N, K;         // rows (hypotheses), vocabulary, d_emb
   const float *bias;   // b_logit [N]
   int kk, ntiles;      // candidates kept per (row, tile); ceil(N / tile_n)
-  float *pmax, *psum;  // [ntiles][M]
+  float *pmax, *psum;  // [M][ntiles]
   float *cval;         // [M][ntiles][kk]
   int *ctok;
   int debug_flags = 0;  // microbenchmark knobs: 1 skip A loads, 2 skip B loads, 4 skip MMA, 8 skip epilogue

@@ -56,8 +56,8 @@ int main() {
     std::vector<float> m0, s0, v0;
     for (int t = 0; t < ntiles; ++t)
       for (int r = 0; r < R0; ++r) {
-        m0.push_back(m[(size_t)t * R + r]);
-        s0.push_back(s[(size_t)t * R + r]);
+        m0.push_back(m[(size_t)r * ntiles + t]);
+        s0.push_back(s[(size_t)r * ntiles + t]);
       }
     v0.assign(v.begin(), v.begin() + (size_t)R0 * ntiles * kk);
     if (ref_m.empty()) {

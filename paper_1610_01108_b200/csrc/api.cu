@@ -1,6 +1,7 @@
 // C-ABI of the B200 decoder (include/amun_b200.h): device model handle,
 // length-bucketed batched beam-search decode, and the per-step parity hooks.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -59,33 +60,48 @@ enum { G_WZ = 0, G_WR, G_WH, G_UZ, G_UR, G_UH, G_BZ, G_BR, G_BH };
 
 static float *upload(amun_model *m, const std::vector<float> &h);
 
-// [K, N] row-major host matrix -> device [N, K] (K-major) tf32-exact hi and
-// residual lo copies for the 3xTF32 tensor-core GEMMs.
-static void upload_kmajor_split(amun_model *m, const float *W, int K, int N, float **hi_out, float **lo_out) {
-  std::vector<float> hi((size_t)N * K), lo((size_t)N * K);
-  for (int k = 0; k < K; ++k)
-    for (int n = 0; n < N; ++n) {
-      float x = W[(size_t)k * N + n];
-      uint32_t u;
-      std::memcpy(&u, &x, 4);
-      u &= 0xFFFFE000u;
-      float h;
-      std::memcpy(&h, &u, 4);
-      hi[(size_t)n * K + k] = h;
-      lo[(size_t)n * K + k] = x - h;
-    }
-  *hi_out = upload(m, hi);
-  *lo_out = upload(m, lo);
-}
-
-static float *upload(amun_model *m, const std::vector<float> &h) {
-  float *d = nullptr;
-  AMUN_CUDA(cudaMalloc(&d, h.size() * sizeof(float)));
+template <class T>
+static T *upload_t(amun_model *m, const std::vector<T> &h) {
+  T *d = nullptr;
+  AMUN_CUDA(cudaMalloc(&d, h.size() * sizeof(T)));
   m->allocs.push_back(d);
-  AMUN_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
-  m->bytes += (int64_t)(h.size() * sizeof(float));
+  AMUN_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  m->bytes += (int64_t)(h.size() * sizeof(T));
   return d;
 }
+
+// [K, N] row-major host matrix -> device [N, Kp] (K-major, row pitch Kp)
+// 3xFP16 hi/lo copies for the tensor-core GEMMs (common.cuh split_h): the
+// matrix is scaled by 2^sw with max|W| 2^sw < 2^14 (fp16 max 65504, and lo
+// stays normal for |W| >= 2^-17 max|W|), hi = fp16(W'), lo = fp16(W' - hi).
+// Source row k lands in column kmap(k) (the padded decoder-row layout);
+// unused columns are zero.  Returns the epilogue's inverse scale
+// 2^-(sw + kXShift).
+template <class KMap>
+static float upload_kmajor_split(amun_model *m, const float *W, int K, int N, int Kp, KMap kmap, __half **hi_out,
+                                 __half **lo_out) {
+  float mx = 0.f;
+  for (size_t i = 0; i < (size_t)K * N; ++i) mx = std::max(mx, std::fabs(W[i]));
+  int e = 0;
+  if (mx > 0.f) std::frexp(mx, &e);  // mx < 2^e
+  const int sw = mx > 0.f ? 14 - e : 0;
+  const float sc = std::ldexp(1.f, sw);
+  std::vector<__half> hi((size_t)N * Kp, __float2half_rn(0.f)), lo((size_t)N * Kp, __float2half_rn(0.f));
+  for (int k = 0; k < K; ++k) {
+    const size_t kc = (size_t)kmap(k);
+    for (int n = 0; n < N; ++n) {
+      const float x = W[(size_t)k * N + n] * sc;
+      const __half h = __float2half_rn(x);
+      hi[(size_t)n * Kp + kc] = h;
+      lo[(size_t)n * Kp + kc] = __float2half_rn(x - __half2float(h));
+    }
+  }
+  *hi_out = upload_t(m, hi);
+  *lo_out = upload_t(m, lo);
+  return std::ldexp(1.f, -(sw + kXShift));
+}
+
+static float *upload(amun_model *m, const std::vector<float> &h) { return upload_t(m, h); }
 
 extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const float *const *t,
                                  int32_t n_tensors, amun_model **out) {
@@ -107,6 +123,12 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
   const int de = dims->d_emb, dh = dims->d_h, da = dims->d_att, V = dims->v_trg, Vs = dims->v_src;
   const int din = de + 2 * dh;  // decoder GRU input [y ; c]
   m->xs_w = de + 3 * dh;
+  m->dep = (de + 7) / 8 * 8;
+  m->xsp = m->dep + 3 * dh;
+  // decoder-row column -> padded fp16 row column ([y | pad | c | s])
+  const int pad = m->dep - de;
+  auto rowmap = [de, pad](int c) { return c < de ? c : c + pad; };
+  auto ident = [](int c) { return c; };
   auto cp = [&](int idx, size_t n) { return std::vector<float>(t[idx], t[idx] + n); };
 
   m->E_src = upload(m, cp(T_E_SRC, (size_t)Vs * de));
@@ -161,11 +183,16 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     m->Wg = upload(m, Wg);
     m->bg = upload(m, bg);
     m->Uh_dec = upload(m, cp(T_DEC + G_UH, (size_t)dh * dh));
-    m->tc_gemm = (de % 4 == 0) && (dh % 4 == 0) && (da % 4 == 0);
+    // tensor-core path: 16-byte fp16 row pitches and activations inside
+    // the split's range (|x| <= max(1, max|E_trg|) <= 2^(15 - kXShift))
+    float emax = 0.f;
+    for (size_t i = 0; i < (size_t)V * de; ++i) emax = std::max(emax, std::fabs(t[T_E_TRG][i]));
+    m->tc_ok = (dh % 8 == 0) && (da % 8 == 0) && emax <= std::ldexp(1.f, 15 - kXShift);
+    m->tc_gemm = m->tc_ok;
     if (m->tc_gemm) {
-      upload_kmajor_split(m, Wg.data(), din + dh, 3 * dh, &m->Wg_hi, &m->Wg_lo);
-      upload_kmajor_split(m, t[T_DEC + G_UH], dh, dh, &m->Uhd_hi, &m->Uhd_lo);
-      upload_kmajor_split(m, t[T_W_ATT_S], dh, da, &m->Wq_hi, &m->Wq_lo);
+      m->us_g = upload_kmajor_split(m, Wg.data(), din + dh, 3 * dh, m->xsp, rowmap, &m->Wg_hi, &m->Wg_lo);
+      m->us_u = upload_kmajor_split(m, t[T_DEC + G_UH], dh, dh, dh, ident, &m->Uhd_hi, &m->Uhd_lo);
+      m->us_q = upload_kmajor_split(m, t[T_W_ATT_S], dh, da, dh, ident, &m->Wq_hi, &m->Wq_lo);
     }
   }
   {  // deep output: rows [y ; c ; s'] = [W_out_y ; W_out_c ; W_out_s]
@@ -175,27 +202,12 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     std::memcpy(&Wo[(size_t)(de + 2 * dh) * de], t[T_W_OUT_S], (size_t)dh * de * sizeof(float));
     m->Wout = upload(m, Wo);
     m->b_out = upload(m, cp(T_B_OUT, de));
-    if (m->tc_gemm) upload_kmajor_split(m, Wo.data(), de + 3 * dh, de, &m->Wo_hi, &m->Wo_lo);
+    if (m->tc_gemm) m->us_o = upload_kmajor_split(m, Wo.data(), de + 3 * dh, de, m->xsp, rowmap, &m->Wo_hi, &m->Wo_lo);
   }
   m->W_logit = upload(m, cp(T_W_LOGIT, (size_t)de * V));
   m->b_logit = upload(m, cp(T_B_LOGIT, V));
-  if (de % 4 == 0) {  // TMA needs 16-byte row pitch: logit rows [V, de] hi/lo
-    std::vector<float> hi((size_t)V * de), lo((size_t)V * de);
-    const float *W = t[T_W_LOGIT];
-    for (int k = 0; k < de; ++k)
-      for (int v = 0; v < V; ++v) {
-        float x = W[(size_t)k * V + v];
-        uint32_t u;
-        std::memcpy(&u, &x, 4);
-        u &= 0xFFFFE000u;
-        float h;
-        std::memcpy(&h, &u, 4);
-        hi[(size_t)v * de + k] = h;
-        lo[(size_t)v * de + k] = x - h;
-      }
-    m->Wl_hi = upload(m, hi);
-    m->Wl_lo = upload(m, lo);
-  }
+  if (m->tc_ok)  // logit rows [V, dep] (K-major, padded to a 16-byte pitch)
+    m->us_l = upload_kmajor_split(m, t[T_W_LOGIT], de, V, m->dep, ident, &m->Wl_hi, &m->Wl_lo);
   AMUN_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
   *out = m;
   m = nullptr;

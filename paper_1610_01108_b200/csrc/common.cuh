@@ -1,6 +1,7 @@
 // Shared helpers for the sm_100a decoder kernels.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -78,13 +79,28 @@ __device__ __forceinline__ Key warp_best(Key k) {
 
 constexpr int kMaxRowCand = 16;
 
-// 3xTF32 operand split: hi = tf32-exact (low 13 mantissa bits cleared),
-// lo = x - hi (exact).  Writes both when `hi` is non-null.
-__device__ __forceinline__ void store_split(float *hi, float *lo, long long off, float x) {
+// 3xFP16 operand split for the tensor-core GEMMs (kind::f16, fp32
+// accumulate): activations are scaled by 2^kXShift (exact), then
+// hi = fp16(x'), lo = fp16(x' - hi) (x' - hi is exact in fp32), so hi + lo
+// carries ~22 significant bits, like the 3xTF32 split, at twice the MMA rate
+// and half the bytes.  The scale keeps lo out of the fp16 subnormal range for
+// |x| >= 2^-13; decoder activations are bounded by max(1, max|E_trg|) and the
+// model loader only enables the tensor-core path when that is <= 2^(15 -
+// kXShift).  The GEMM epilogues multiply the accumulator by
+// 2^-(kXShift + weight shift).
+constexpr int kXShift = 10;
+constexpr float kXScale = 1024.f;
+__device__ __forceinline__ void split_h(float x, __half &h, __half &l) {
+  const float xs = x * kXScale;
+  h = __float2half_rn(xs);
+  l = __float2half_rn(xs - __half2float(h));
+}
+__device__ __forceinline__ void store_split(__half *hi, __half *lo, long long off, float x) {
   if (hi) {
-    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    __half h, l;
+    split_h(x, h, l);
     hi[off] = h;
-    lo[off] = x - h;
+    lo[off] = l;
   }
 }  // fused logit epilogue keeps <= 16 per row/tile
 

@@ -151,9 +151,10 @@ struct DecBufs {
   float *XS, *Sn, *Q, *Z, *RH, *XH, *T, *L;
   float *En = nullptr;  // attention energies [R][jmax]
   float *EQ = nullptr;  // e^{2q} of the attention query rows [R][da]
-  float *T_hi = nullptr, *T_lo = nullptr;  // 3xTF32 split of t (tensor-core logits)
-  // 3xTF32 splits of the tensor-core GEMM A operands
-  float *XSh = nullptr, *XSl = nullptr, *RHh = nullptr, *RHl = nullptr, *Snh = nullptr, *Snl = nullptr;
+  __half *T_hi = nullptr, *T_lo = nullptr;  // 3xFP16 split of t [R][dep] (tensor-core logits)
+  // 3xFP16 splits of the tensor-core GEMM activation operands; XSh/XSl use
+  // the padded row layout [y | pad | c | s] (pitch xsp, pad columns zero)
+  __half *XSh = nullptr, *XSl = nullptr, *RHh = nullptr, *RHl = nullptr, *Snh = nullptr, *Snl = nullptr;
 };
 
 void carve_enc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
@@ -181,19 +182,19 @@ void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, int jmax, boo
   d.T = cv.take<float>((size_t)R * de);
   d.L = full_logits ? cv.take<float>((size_t)R * m->d.v_trg) : nullptr;
   if (!full_logits && m->Wl_hi) {
-    d.T_hi = cv.take<float>((size_t)R * de);
-    d.T_lo = cv.take<float>((size_t)R * de);
+    d.T_hi = cv.take<__half>((size_t)R * m->dep);
+    d.T_lo = cv.take<__half>((size_t)R * m->dep);
   }
 }
 
 void carve_dec_tc(Carver &cv, DecBufs &d, const amun_model *m, int R) {
   const int dh = m->d.d_h;
-  d.XSh = cv.take<float>((size_t)R * m->xs_w);
-  d.XSl = cv.take<float>((size_t)R * m->xs_w);
-  d.RHh = cv.take<float>((size_t)R * dh);
-  d.RHl = cv.take<float>((size_t)R * dh);
-  d.Snh = cv.take<float>((size_t)R * dh);
-  d.Snl = cv.take<float>((size_t)R * dh);
+  d.XSh = cv.take<__half>((size_t)R * m->xsp);
+  d.XSl = cv.take<__half>((size_t)R * m->xsp);
+  d.RHh = cv.take<__half>((size_t)R * dh);
+  d.RHl = cv.take<__half>((size_t)R * dh);
+  d.Snh = cv.take<__half>((size_t)R * dh);
+  d.Snl = cv.take<__half>((size_t)R * dh);
 }
 
 // nnet.py:110-130 for B padded sentences: input projection (embedding
@@ -256,13 +257,13 @@ int tc_target_ctas() {
 }
 
 void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
-  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, xs = m->xs_w;
-  const int s_off = de + 2 * dh;
-  ts.q = make_sk_maps(d.XSh + s_off, d.XSl + s_off, dh, xs, nullptr, nullptr, 0, 0, Rmax, m->Wq_hi, m->Wq_lo, da,
-                      dh);
-  ts.g = make_sk_maps(d.XSh, d.XSl, xs, xs, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi, m->Wg_lo, 3 * dh, xs);
-  ts.u = make_sk_maps(d.RHh, d.RHl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Uhd_hi, m->Uhd_lo, dh, dh);
-  ts.o = make_sk_maps(d.XSh, d.XSl, de + 2 * dh, xs, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi, m->Wo_lo, de, xs);
+  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, xp = m->xsp, dep = m->dep;
+  const int s_off = dep + 2 * dh;  // padded fp16 row layout
+  ts.q = make_sk_maps(d.XSh + s_off, d.XSl + s_off, dh, xp, nullptr, nullptr, 0, 0, Rmax, m->Wq_hi, m->Wq_lo, da,
+                      dh, m->us_q);
+  ts.g = make_sk_maps(d.XSh, d.XSl, xp, xp, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi, m->Wg_lo, 3 * dh, xp, m->us_g);
+  ts.u = make_sk_maps(d.RHh, d.RHl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Uhd_hi, m->Uhd_lo, dh, dh, m->us_u);
+  ts.o = make_sk_maps(d.XSh, d.XSl, s_off, xp, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi, m->Wo_lo, de, xp, m->us_o);
   const int t = tc_target_ctas();
   ts.sq = sk_fit_splits(ts.q, t);
   ts.sg = sk_fit_splits(ts.g, t);
@@ -295,8 +296,9 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
   aa.energy = d.En;
   aa.EQ = d.EQ;
   if (ts) {
-    aa.ctx_hi = d.XSh + de;
-    aa.ctx_lo = d.XSl + de;
+    aa.ctx_hi = d.XSh + m->dep;
+    aa.ctx_lo = d.XSl + m->dep;
+    aa.ldctx_h = m->xsp;
   }
   int na_launch = 1;
   c.run(AMUN_K_ATTN, [&] { na_launch = launch_attention(aa, R, c.st); });
@@ -332,6 +334,7 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     if (lo.tc) {
       e.hi = d.T_hi;
       e.lo = d.T_lo;
+      e.ldh = m->dep;
     }
     if (ts) {
       gemm_tc(c, ts->o, R, ts->so, e);
@@ -345,7 +348,7 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
   }
   c.cls = AMUN_K_LOGIT;
   if (lo.tc) {
-    LogitTcArgs ta{R, V, de, m->b_logit, lo.kk, lo.ntiles, lo.pmax, lo.psum, lo.cval, lo.ctok};
+    LogitTcArgs ta{R, V, de, m->b_logit, lo.kk, lo.ntiles, m->us_l, lo.pmax, lo.psum, lo.cval, lo.ctok};
     c.run(AMUN_K_LOGIT, [&] { launch_logits_tc(*lo.tc, ta, c.st); });
     return;
   }
@@ -484,7 +487,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     BeamState bs{};
     float **p_XS;
     const float **p_Sn, **p_E, **p_S0, **p_L;
-    float **p_fin, **p_XSh, **p_XSl;
+    float **p_fin;
+    __half **p_XSh, **p_XSl;
     LogitTcMaps tc_maps{};
     int *h_probe = nullptr;  // pinned ring of n_done probes
     std::vector<cudaEvent_t> probe_ev;
@@ -569,14 +573,14 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.p_S0 = cv.take<const float *>(n_models);
       L.p_L = cv.take<const float *>(n_models);
       L.p_fin = cv.take<float *>(n_models);
-      L.p_XSh = cv.take<float *>(n_models);
-      L.p_XSl = cv.take<float *>(n_models);
+      L.p_XSh = cv.take<__half *>(n_models);
+      L.p_XSl = cv.take<__half *>(n_models);
       if (!pass) L.mem.alloc(cv.off, L.st);
     }
     if (use_tc) {
       static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
       if (logits_tc_tile_n() != kBN) throw Error(AMUN_ERR_UNSUPPORTED, "logit tile width mismatch");
-      L.tc_maps = make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, de, m0->Wl_hi, m0->Wl_lo, V);
+      L.tc_maps = make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, m0->Wl_hi, m0->Wl_lo, m0->dep, V);
     }
     if (use_tcg)
       for (int m = 0; m < n_models; ++m) tc_step_maps(ms[m], L.db[m], Rmax, L.tsteps[m]);
@@ -601,6 +605,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     h2d(c, (const void **)L.p_fin, hf.data(), n_models);
     h2d(c, (const void **)L.p_XSh, hxh.data(), n_models);
     h2d(c, (const void **)L.p_XSl, hxl.data(), n_models);
+    if (use_tcg)  // pad columns of the fp16 rows must read as zero
+      for (int m = 0; m < n_models; ++m) {
+        AMUN_CUDA(cudaMemsetAsync(L.db[m].XSh, 0, sizeof(__half) * (size_t)Rmax * ms[m]->xsp, L.st));
+        AMUN_CUDA(cudaMemsetAsync(L.db[m].XSl, 0, sizeof(__half) * (size_t)Rmax * ms[m]->xsp, L.st));
+      }
     AMUN_CUDA(cudaMallocHost(&L.h_probe, sizeof(int) * kProbeSlots));
     L.probe_ev.resize(kProbeSlots);
     for (auto &e : L.probe_ev) AMUN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -678,6 +687,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     if (use_tcg) {
       L.mr.XSh = L.p_XSh;
       L.mr.XSl = L.p_XSl;
+      L.mr.ldxh = m0->xsp;
+      L.mr.hpad = m0->dep - de;
     }
     c.run(AMUN_K_SELECT, [&] { launch_init_beam(L.bs, L.mr, L.p_S0, L.st); });
     L.lo = LogitOut{fused, kk, ntiles, L.pmax, L.psum, L.cval, L.ctok};

@@ -20,16 +20,18 @@ struct amun_model {
   float *Uh_dec = nullptr;                 // [dh, dh]
   float *Wout = nullptr, *b_out = nullptr; // [de+3dh, de], [de]
   float *W_logit = nullptr, *b_logit = nullptr;  // [de, V], [V]
-  // tensor-core copies of the output projection: logit rows [V, de] split
-  // into tf32-exact hi and residual lo (3xTF32); null when de % 4 != 0
-  float *Wl_hi = nullptr, *Wl_lo = nullptr;
-  // K-major [N, K] hi/lo copies of the decoder-step weights for the split-K
-  // tensor-core GEMMs (query, GRU phase A, GRU phase B, deep output)
-  bool tc_gemm = false;
-  float *Wq_hi = nullptr, *Wq_lo = nullptr;    // W_att_s^T [da, dh]
-  float *Wg_hi = nullptr, *Wg_lo = nullptr;    // Wg^T      [3dh, de+3dh]
-  float *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
-  float *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, de+3dh]
+  // tensor-core (3xFP16, common.cuh split_h) copies, K-major [N, Kpitch]
+  // fp16 hi/lo, with the epilogue inverse scales us_*; the decoder-row
+  // weights use the padded row layout [y | pad to dep | c | s] (pitch xsp)
+  bool tc_ok = false;    // dims / activation range allow the tensor-core path
+  bool tc_gemm = false;  // decoder-step GEMMs on tensor cores
+  int dep = 0, xsp = 0;  // d_emb rounded up to 8; padded decoder-row pitch
+  __half *Wl_hi = nullptr, *Wl_lo = nullptr;    // W_logit^T [V, dep]
+  __half *Wq_hi = nullptr, *Wq_lo = nullptr;    // W_att_s^T [da, dh]
+  __half *Wg_hi = nullptr, *Wg_lo = nullptr;    // Wg^T      [3dh, xsp]
+  __half *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
+  __half *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, xsp]
+  float us_l = 1.f, us_q = 1.f, us_g = 1.f, us_u = 1.f, us_o = 1.f;
   int64_t bytes = 0;
   std::vector<void *> allocs;
   cudaStream_t stream = nullptr;

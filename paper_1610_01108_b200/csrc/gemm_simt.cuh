@@ -232,7 +232,8 @@ struct EpiStore {
   const float *bias;
   int act;
   long long c_zs;
-  float *hi = nullptr, *lo = nullptr;  // optional 3xTF32 split copies (ldc, no z)
+  __half *hi = nullptr, *lo = nullptr;  // optional 3xFP16 split copies (row pitch ldh, no z)
+  int ldh = 0;
   float *ex2 = nullptr;  // optional e^{2v} (attention query rows: factored tanh, kernels.cu)
   __device__ void operator()(int m, int n, float v, int z) const {
     if (bias) v += bias[n];
@@ -243,11 +244,7 @@ struct EpiStore {
       asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(v * 2.8853900817779268f));
       ex2[(long long)m * ldc + n] = y;
     }
-    if (hi) {
-      const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-      hi[(long long)m * ldc + n] = h;
-      lo[(long long)m * ldc + n] = v - h;
-    }
+    store_split(hi, lo, (long long)m * ldh + n, v);
   }
 };
 
@@ -259,7 +256,7 @@ struct EpiGruA {
   const float *S;     // current state rows, stride lds
   int lds, dh;
   float *Z, *RH, *XH;  // [M, dh] each
-  float *RHh = nullptr, *RHl = nullptr;  // optional 3xTF32 split of r*s
+  __half *RHh = nullptr, *RHl = nullptr;  // optional 3xFP16 split of r*s
   __device__ void operator()(int m, int n, float v, int) const {
     v += bias[n];
     if (n < dh) {
@@ -283,7 +280,7 @@ struct EpiGruB {
   int lds, dh;
   const float *Z, *XH;
   float *Sn;
-  float *Snh = nullptr, *Snl = nullptr;  // optional 3xTF32 split of s'
+  __half *Snh = nullptr, *Snl = nullptr;  // optional 3xFP16 split of s'
   __device__ void operator()(int m, int n, float v, int) const {
     long long o = (long long)m * dh + n;
     float ht = tanhf(v + XH[o]);

@@ -11,8 +11,10 @@
 // TMEM columns, as one or two MMAs of N <= 256).  Every weight byte is read
 // once per launch; the activation K-slice is re-read once per 128 features.
 //
-// Precision: 3xTF32 (W_hi X_hi + W_hi X_lo + W_lo X_hi, fp32 accumulate in
-// TMEM), the FP32-equivalent scheme of logits_tc.cu.
+// Precision: 3xFP16 (W_hi X_hi + W_hi X_lo + W_lo X_hi on kind::f16, fp32
+// accumulate in TMEM) over power-of-two scaled operands (common.cuh
+// split_h), the FP32-equivalent scheme of logits_tc.cu; the reduction
+// multiplies by the inverse scale before the epilogue.
 //
 // Grid (S, N/128) with clusters of (S, 1, 1): the S CTAs of a cluster split
 // K and each holds a 128 x R fp32 partial in TMEM.  After the mainloop each
@@ -35,8 +37,8 @@
 
 namespace amun {
 
-// Tile configuration: BK fp32 K elements per swizzled smem row (16 -> 64 B
-// rows / SWIZZLE_64B, 32 -> 128 B rows / SWIZZLE_128B), pipeline depth, rows
+// Tile configuration: BK fp16 K elements per swizzled smem row (32 -> 64 B
+// rows / SWIZZLE_64B, 64 -> 128 B rows / SWIZZLE_128B), pipeline depth, rows
 // per pass (TMEM columns; the smem reduction buffer is PR x 512 B) and CG,
 // the CTA group: 1 = one CTA per 128 features, 2 = a CTA pair per 256
 // features (tcgen05 cta_group::2: M = 256, each CTA stages its 128 weight
@@ -45,7 +47,7 @@ template <int BK_, int STAGES_, int PR_ = 320, int CG_ = 1>
 struct SkCfg {
   static constexpr int kBK = BK_;
   static constexpr int kCG = CG_;
-  static constexpr int kRowBytes = BK_ * 4;
+  static constexpr int kRowBytes = BK_ * 2;
   static constexpr int kPR = PR_;
   static constexpr int kBoxR = 16;  // activation rows per TMA box
   static constexpr int kStages = STAGES_;
@@ -59,11 +61,12 @@ struct SkCfg {
   static_assert(kPR % (16 * CG_) == 0, "pass rows");
   static_assert(kSmem <= 232448, "shared memory per CTA");
 };
-using SkDefault = SkCfg<32, 3, 320, 2>;
+using SkDefault = SkCfg<64, 3, 320, 2>;
 
 struct SkMaps {
   CUtensorMap wh, wl, x1h, x1l, x2h, x2l;
   int N, k1, k2;
+  float unscale;
 };
 
 struct SkArgs {
@@ -72,6 +75,7 @@ struct SkArgs {
   int k_off2;    // weight K coordinate where segment 2 starts
   int kb_per_split;
   int splits;
+  float unscale;  // 2^-(activation shift + weight shift)
   int debug;  // microbenchmark knobs: 1 skip weight loads, 2 skip activation loads, 4 skip MMA
 };
 
@@ -192,13 +196,13 @@ __global__ void __launch_bounds__(C::kThreads, 1)
       }
     } else if (warp == 1) {
       if (lane == 0 && member == 0) {
-        const uint32_t id0 = tc::idesc_tf32(128 * CG, ps.n[0]);
-        const uint32_t id1 = tc::idesc_tf32(128 * CG, ps.nsub == 2 ? ps.n[1] : 16 * CG);
+        const uint32_t id0 = tc::idesc_f16(128 * CG, ps.n[0]);
+        const uint32_t id1 = tc::idesc_f16(128 * CG, ps.nsub == 2 ? ps.n[1] : 16 * CG);
         auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t id, uint32_t acc) {
           if constexpr (CG == 2)
-            tc::mma_tf32_pair(d, ad, bd, id, acc);
+            tc::mma_f16_pair(d, ad, bd, id, acc);
           else
-            tc::mma_tf32(d, ad, bd, id, acc);
+            tc::mma_f16(d, ad, bd, id, acc);
         };
         for (int i = 0; i < nkb; ++i) {
           const int it = it0 + i;
@@ -207,8 +211,8 @@ __global__ void __launch_bounds__(C::kThreads, 1)
           tc::tc_fence_after();
           const uint32_t base = tc::smem_u32(smem + s * C::kStageBytes);
 #pragma unroll
-          for (int k2 = 0; k2 < ((a.debug & 4) ? 0 : C::kBK / 8); ++k2) {
-            const uint32_t koff = k2 * 32;  // 8 tf32 = 32 bytes along K (inside the swizzle row)
+          for (int k2 = 0; k2 < ((a.debug & 4) ? 0 : C::kBK / 16); ++k2) {
+            const uint32_t koff = k2 * 32;  // 16 fp16 = 32 bytes along K (inside the swizzle row)
             const uint64_t awh = tc::desc_kmajor<C::kRowBytes>(base + koff);
             const uint64_t awl = tc::desc_kmajor<C::kRowBytes>(base + C::kWBytes + koff);
             const uint32_t xb = base + 2 * C::kWBytes + koff;
@@ -291,6 +295,10 @@ __global__ void __launch_bounds__(C::kThreads, 1)
           acc.z += p[s].z;
           acc.w += p[s].w;
         }
+      acc.x *= a.unscale;
+      acc.y *= a.unscale;
+      acc.z *= a.unscale;
+      acc.w *= a.unscale;
       const int n = n0 + 4 * q;
       const int m = row0 + r;
       if (n + 0 < a.N) epi(m, n + 0, acc.x, 0);
@@ -315,20 +323,21 @@ __global__ void __launch_bounds__(C::kThreads, 1)
 // Activation segment s: hi/lo [rows, k_s] with row pitch lda_s (elements),
 // Rmax rows allocated; weight hi/lo: [N, Kb = k1 + k2] K-major.
 template <class C = SkDefault>
-SkMaps make_sk_maps(const float *x1h, const float *x1l, int k1, int lda1, const float *x2h, const float *x2l, int k2,
-                    int lda2, int Rmax, const float *wh, const float *wl, int N, int Kb) {
+SkMaps make_sk_maps(const __half *x1h, const __half *x1l, int k1, int lda1, const __half *x2h, const __half *x2l,
+                    int k2, int lda2, int Rmax, const __half *wh, const __half *wl, int N, int Kb, float unscale) {
   SkMaps m;
-  m.x1h = make_tma_2d_f32(x1h, k1, Rmax, lda1, C::kBK, C::kBoxR);
-  m.x1l = make_tma_2d_f32(x1l, k1, Rmax, lda1, C::kBK, C::kBoxR);
+  m.x1h = make_tma_2d_f16(x1h, k1, Rmax, lda1, C::kBK, C::kBoxR);
+  m.x1l = make_tma_2d_f16(x1l, k1, Rmax, lda1, C::kBK, C::kBoxR);
   if (x2h) {
-    m.x2h = make_tma_2d_f32(x2h, k2, Rmax, lda2, C::kBK, C::kBoxR);
-    m.x2l = make_tma_2d_f32(x2l, k2, Rmax, lda2, C::kBK, C::kBoxR);
+    m.x2h = make_tma_2d_f16(x2h, k2, Rmax, lda2, C::kBK, C::kBoxR);
+    m.x2l = make_tma_2d_f16(x2l, k2, Rmax, lda2, C::kBK, C::kBoxR);
   } else {
     m.x2h = m.x1h;
     m.x2l = m.x1l;
   }
-  m.wh = make_tma_2d_f32(wh, Kb, N, Kb, C::kBK, 128);
-  m.wl = make_tma_2d_f32(wl, Kb, N, Kb, C::kBK, 128);
+  m.wh = make_tma_2d_f16(wh, Kb, N, Kb, C::kBK, 128);
+  m.wl = make_tma_2d_f16(wl, Kb, N, Kb, C::kBK, 128);
+  m.unscale = unscale;
   m.N = N;
   m.k1 = k1;
   m.k2 = x2h ? k2 : 0;
@@ -358,6 +367,7 @@ void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaS
   a.k_off2 = maps.k1;
   a.kb_per_split = ceil_div(a.nk1 + a.nk2, splits);
   a.splits = splits;
+  a.unscale = maps.unscale;
   a.debug = debug;
   auto kern = gemm_sk_kernel<C, Epi>;
   static bool attr[64] = {};

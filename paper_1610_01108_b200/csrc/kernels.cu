@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
       const int c = c0 + u * blockDim.x;
       if (c < a.dh2) {
         a.ctx[(long long)r * a.ldctx + c] = acc[u];
-        store_split(a.ctx_hi, a.ctx_lo, (long long)r * a.ldctx + c, acc[u]);
+        store_split(a.ctx_hi, a.ctx_lo, (long long)r * a.ldctx_h + c, acc[u]);
       }
     }
   }
@@ -303,10 +303,11 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
         const float4 o4 = part[r * kCtxCols + ct];
         const float vals[4] = {acc[r].x + o4.x, acc[r].y + o4.y, acc[r].z + o4.z, acc[r].w + o4.w};
         const long long o = (long long)(b * k + r0 + r) * a.ldctx + c;
+        const long long oh = (long long)(b * k + r0 + r) * a.ldctx_h + c;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           a.ctx[o + u] = vals[u];
-          store_split(a.ctx_hi, a.ctx_lo, o + u, vals[u]);
+          store_split(a.ctx_hi, a.ctx_lo, oh + u, vals[u]);
         }
       }
     }
@@ -407,11 +408,12 @@ __global__ void init_beam_kernel(BeamState bs, ModelRows mr, const float *const 
   }
   for (int m = 0; m < mr.n_models; ++m) {
     float *XS = mr.XS[m];
-    float *XSh = mr.XSh ? mr.XSh[m] : nullptr;
-    float *XSl = mr.XSl ? mr.XSl[m] : nullptr;
+    __half *XSh = mr.XSh ? mr.XSh[m] : nullptr;
+    __half *XSl = mr.XSl ? mr.XSl[m] : nullptr;
     const float *E = mr.E_trg[m];
     for (int i = 0; i < k; ++i) {
       const long long ro = (long long)(b * k + i) * mr.ldxs;
+      const long long roh = (long long)(b * k + i) * mr.ldxh;
       for (int c = threadIdx.x; c < mr.ldxs; c += blockDim.x) {
         float v = 0.f;
         if (i == 0) {
@@ -419,7 +421,7 @@ __global__ void init_beam_kernel(BeamState bs, ModelRows mr, const float *const 
           else if (c >= mr.s_off && c < mr.s_off + mr.dh) v = S0[m][(long long)b * mr.dh + (c - mr.s_off)];
         }
         XS[ro + c] = v;
-        store_split(XSh, XSl, ro + c, v);
+        store_split(XSh, XSl, roh + c + (c >= mr.de ? mr.hpad : 0), v);
       }
     }
   }
@@ -788,8 +790,8 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   const bool vec = (mr.de % 4 == 0) && (mr.dh % 4 == 0) && (mr.ldxs % 4 == 0) && (mr.s_off % 4 == 0);
   for (int m = 0; m < n_models; ++m) {
     float *XS = mr.XS[m];
-    float *XSh = mr.XSh ? mr.XSh[m] : nullptr;
-    float *XSl = mr.XSl ? mr.XSl[m] : nullptr;
+    __half *XSh = mr.XSh ? mr.XSh[m] : nullptr;
+    __half *XSl = mr.XSl ? mr.XSl[m] : nullptr;
     const float *Sn = mr.Sn[m];
     const float *E = mr.E_trg[m];
     if (vec) {
@@ -797,7 +799,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       const int total = newna * qrow;
       for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
         float4 v[8];
-        long long dst[8];
+        long long dst[8], dsth[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int idx = base + u * blockDim.x;
@@ -805,12 +807,15 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
           if (idx < total) {
             const int i = idx / qrow, c4 = idx - i * qrow;
             const long long ro = (long long)(b * k + i) * mr.ldxs;
+            const long long roh = (long long)(b * k + i) * mr.ldxh;
             if (c4 < qe) {
               v[u] = __ldg(reinterpret_cast<const float4 *>(E + (long long)ch_tok[i] * mr.de) + c4);
               dst[u] = ro + 4 * c4;
+              dsth[u] = roh + 4 * c4;
             } else {
               v[u] = __ldg(reinterpret_cast<const float4 *>(Sn + (long long)(b * k + ch_par[i]) * mr.dh) + (c4 - qe));
               dst[u] = ro + mr.s_off + 4 * (c4 - qe);
+              dsth[u] = roh + mr.s_off + mr.hpad + 4 * (c4 - qe);
             }
           }
         }
@@ -818,31 +823,30 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         for (int u = 0; u < 8; ++u) {
           if (dst[u] < 0) continue;
           *reinterpret_cast<float4 *>(XS + dst[u]) = v[u];
-          if (XSh) {
-            const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-            float h4[4], l4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              h4[e] = __uint_as_float(__float_as_uint(e4[e]) & 0xFFFFE000u);
-              l4[e] = e4[e] - h4[e];
-            }
-            *reinterpret_cast<float4 *>(XSh + dst[u]) = make_float4(h4[0], h4[1], h4[2], h4[3]);
-            *reinterpret_cast<float4 *>(XSl + dst[u]) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+          if (XSh) {  // 4 halves = 8 bytes (ldxh, hpad and s_off are multiples of 4)
+            __half h4[4], l4[4];
+            split_h(v[u].x, h4[0], l4[0]);
+            split_h(v[u].y, h4[1], l4[1]);
+            split_h(v[u].z, h4[2], l4[2]);
+            split_h(v[u].w, h4[3], l4[3]);
+            *reinterpret_cast<uint2 *>(XSh + dsth[u]) = *reinterpret_cast<const uint2 *>(h4);
+            *reinterpret_cast<uint2 *>(XSl + dsth[u]) = *reinterpret_cast<const uint2 *>(l4);
           }
         }
       }
     } else {
       for (int i = 0; i < newna; ++i) {
         const long long ro = (long long)(b * k + i) * mr.ldxs;
+        const long long roh = (long long)(b * k + i) * mr.ldxh;
         const float *ey = E + (long long)ch_tok[i] * mr.de;
         const float *sp = Sn + (long long)(b * k + ch_par[i]) * mr.dh;
         for (int c = threadIdx.x; c < mr.de; c += blockDim.x) {
           XS[ro + c] = ey[c];
-          store_split(XSh, XSl, ro + c, ey[c]);
+          store_split(XSh, XSl, roh + c, ey[c]);
         }
         for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) {
           XS[ro + mr.s_off + c] = sp[c];
-          store_split(XSh, XSl, ro + mr.s_off + c, sp[c]);
+          store_split(XSh, XSl, roh + mr.s_off + mr.hpad + c, sp[c]);
         }
       }
     }

@@ -25,7 +25,8 @@ struct AttnArgs {
   float *ctx;
   int ldctx;
   float *alpha;  // optional [R][jmax]
-  float *ctx_hi = nullptr, *ctx_lo = nullptr;  // optional 3xTF32 split (same layout as ctx)
+  __half *ctx_hi = nullptr, *ctx_lo = nullptr;  // optional 3xFP16 split (row pitch ldctx_h)
+  int ldctx_h = 0;
   float *energy = nullptr;  // scratch [R][jmax]: enables the two-phase sentence kernels
   const float *EQ = nullptr;  // e^{2q} rows (same layout as Q), from the query GEMM epilogue
 };
@@ -60,8 +61,11 @@ struct ModelRows {  // per-model decoder row buffers (device arrays of pointers)
   const float *const *E_trg;
   float *const *fin_states;  // optional [B][fin_cap][dh]
   int ldxs, de, dh, s_off, n_models;
-  float *const *XSh = nullptr;  // optional 3xTF32 split copies of XS (per model)
-  float *const *XSl = nullptr;
+  // optional 3xFP16 split copies of XS (per model) in the padded layout:
+  // row pitch ldxh, XS column c at c + (c >= de ? hpad : 0)
+  __half *const *XSh = nullptr;
+  __half *const *XSl = nullptr;
+  int ldxh = 0, hpad = 0;
 };
 
 // XS rows of every sentence: slot 0 <- [E_trg[EOS] | 0 | s0_b], others 0;

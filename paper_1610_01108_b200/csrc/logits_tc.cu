@@ -4,11 +4,14 @@
 //
 //   logits[R, V] = t[R, K] * W_logit[K, V] + b_logit,  K = d_emb
 //
-// Precision: 3xTF32 on tcgen05.mma kind::tf32.  Both operands are split into
-// tf32-exact hi and residual lo parts (t by the deep-output epilogue, the
-// weights once at model load) and the MMAs accumulate hi*hi + hi*lo + lo*hi
-// in fp32 in TMEM — FP32-equivalent accuracy (BF16/TF32 flip the
-// beam set in 1-4% of steps, FP32 and 3xTF32 in none).
+// Precision: 3xFP16 on tcgen05.mma kind::f16.  Both operands are scaled by a
+// power of two and split into fp16 hi and residual lo parts (t by the
+// deep-output epilogue, common.cuh split_h; the weights once at model load)
+// and the MMAs accumulate hi*hi + hi*lo + lo*hi in fp32 in TMEM — ~22
+// significant bits per operand like 3xTF32, FP32-equivalent accuracy (SURVEY
+// §0.4: BF16/TF32 flip the beam set in 1-4% of steps, FP32 and 3xTF32 in
+// none), at twice the tf32 MMA rate and half its operand bytes.  The epilogue
+// multiplies by the inverse scale.
 //
 // Swap-AB on CTA pairs (tcgen05 cta_group::2): the vocabulary is the MMA's
 // M dimension (256 logit rows per pair, 128 per CTA = one TMEM lane each)
@@ -33,8 +36,8 @@ namespace amun {
 
 namespace {
 
-constexpr int kBK = 32;                     // fp32 K elements per 128-byte swizzled row
-constexpr int kRowB = kBK * 4;
+constexpr int kBK = 64;                     // fp16 K elements per 128-byte swizzled row
+constexpr int kRowB = kBK * 2;
 constexpr int kStages = 3;
 constexpr int kUnitRows = 160;              // hypothesis rows per work unit (one MMA, N <= 160)
 constexpr int kXRows = kUnitRows / 2;       // rows staged by each CTA of the pair
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Unit un(u, npass, a.M);
         const int buf = ti & 1;
         const uint32_t acc = tmem + buf * kAccCols;
-        const uint32_t idesc = tc::idesc_tf32(256, un.n);
+        const uint32_t idesc = tc::idesc_f16(256, un.n);
         if (ti >= 2) {
           tc::mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1);  // both epilogues drained this buffer
           tc::tc_fence_after();
@@ -248,16 +251,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tc_fence_after();
           const uint32_t base = tc::smem_u32(smem + s * kStageB);
 #pragma unroll
-          for (int k2 = 0; k2 < ((a.debug_flags & 4) ? 0 : kBK / 8); ++k2) {
+          for (int k2 = 0; k2 < ((a.debug_flags & 4) ? 0 : kBK / 16); ++k2) {
             const uint32_t koff = k2 * 32;
             const uint64_t awh = tc::desc_kmajor_sw128(base + koff);
             const uint64_t awl = tc::desc_kmajor_sw128(base + kWB + koff);
             const uint64_t bh = tc::desc_kmajor_sw128(base + 2 * kWB + koff);
             const uint64_t bl = tc::desc_kmajor_sw128(base + 2 * kWB + kXB + koff);
             const uint32_t acc0 = (kb | k2) != 0;
-            tc::mma_tf32_pair(acc, awh, bh, idesc, acc0);
-            tc::mma_tf32_pair(acc, awh, bl, idesc, 1);
-            tc::mma_tf32_pair(acc, awl, bh, idesc, 1);
+            tc::mma_f16_pair(acc, awh, bh, idesc, acc0);
+            tc::mma_f16_pair(acc, awh, bl, idesc, 1);
+            tc::mma_f16_pair(acc, awl, bh, idesc, 1);
           }
           tc::mma_commit_pair_mc(&empty[s], (uint16_t)(kMask << leader));
         }
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tmem_ld_32x32(tmem + ab * kAccCols + ((uint32_t)(lg * 32) << 16) + c0, v);
           float *dst = buf + lg * kTrQ + lane;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) dst[i * kTrRow] = v[i] + bias_f;
+          for (int i = 0; i < 32; ++i) dst[i * kTrRow] = fmaf(v[i], a.unscale, bias_f);
         }
         stamp(1);
         asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
@@ -483,13 +486,28 @@ CUtensorMap make_tma_2d_f32(const float *ptr, int inner, int outer, int row_stri
   return m;
 }
 
-LogitTcMaps make_logit_maps(const float *t_hi, const float *t_lo, int R, int K, int ldt, const float *w_hi,
-                            const float *w_lo, int V) {
+CUtensorMap make_tma_2d_f16(const __half *ptr, int inner, int outer, int row_stride_elems, int box_inner,
+                            int box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)row_stride_elems * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half *>(ptr), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           box_inner * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(2, "cuTensorMapEncodeTiled (f16) failed: " + std::to_string((int)r));
+  return m;
+}
+
+LogitTcMaps make_logit_maps(const __half *t_hi, const __half *t_lo, int R, int K, int ldt, const __half *w_hi,
+                            const __half *w_lo, int ldw, int V) {
   LogitTcMaps m;
-  m.a_hi = make_tma_2d_f32(t_hi, K, R, ldt, kBK, kBoxR);
-  m.a_lo = make_tma_2d_f32(t_lo, K, R, ldt, kBK, kBoxR);
-  m.b_hi = make_tma_2d_f32(w_hi, K, V, K, kBK, 128);
-  m.b_lo = make_tma_2d_f32(w_lo, K, V, K, kBK, 128);
+  m.a_hi = make_tma_2d_f16(t_hi, K, R, ldt, kBK, kBoxR);
+  m.a_lo = make_tma_2d_f16(t_lo, K, R, ldt, kBK, kBoxR);
+  m.b_hi = make_tma_2d_f16(w_hi, K, V, ldw, kBK, 128);
+  m.b_lo = make_tma_2d_f16(w_lo, K, V, ldw, kBK, 128);
   return m;
 }
 

@@ -1,8 +1,9 @@
-// Tensor-core (tcgen05, 3xTF32) logit projection with fused log-softmax
+// Tensor-core (tcgen05, 3xFP16) logit projection with fused log-softmax
 // partials and per-row top-k; see logits_tc.cu.
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 namespace amun {
 
@@ -10,6 +11,7 @@ struct LogitTcArgs {
   int M, N, K;         // rows (hypotheses), vocabulary, d_emb
   const float *bias;   // b_logit [N]
   int kk, ntiles;      // candidates kept per (row, tile); ceil(N / tile_n)
+  float unscale;       // 2^-(activation shift + weight shift) of the 3xFP16 operands
   float *pmax, *psum;  // [M][ntiles]
   float *cval;         // [M][ntiles][kk]
   int *ctok;
@@ -26,9 +28,12 @@ int logits_tc_tile_n();
 // 128 B -> SW128)
 CUtensorMap make_tma_2d_f32(const float *ptr, int inner, int outer, int row_stride_elems, int box_inner,
                             int box_outer);
-// t_hi/t_lo: [R, ldt] (first K columns used); w_hi/w_lo: [V, K] (logit rows)
-LogitTcMaps make_logit_maps(const float *t_hi, const float *t_lo, int R, int K, int ldt, const float *w_hi,
-                            const float *w_lo, int V);
+// fp16 2D tensor map (row pitch must be a multiple of 8 elements)
+CUtensorMap make_tma_2d_f16(const __half *ptr, int inner, int outer, int row_stride_elems, int box_inner,
+                            int box_outer);
+// t_hi/t_lo: [R, ldt] (first K columns used); w_hi/w_lo: [V, ldw] (logit rows)
+LogitTcMaps make_logit_maps(const __half *t_hi, const __half *t_lo, int R, int K, int ldt, const __half *w_hi,
+                            const __half *w_lo, int ldw, int V);
 void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st);
 
 }  // namespace amun

@@ -187,7 +187,7 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     // the split's range (|x| <= max(1, max|E_trg|) <= 2^(15 - kXShift))
     float emax = 0.f;
     for (size_t i = 0; i < (size_t)V * de; ++i) emax = std::max(emax, std::fabs(t[T_E_TRG][i]));
-    m->tc_ok = (dh % 8 == 0) && (da % 8 == 0) && emax <= std::ldexp(1.f, 15 - kXShift);
+    m->tc_ok = (de % 4 == 0) && (dh % 8 == 0) && (da % 8 == 0) && emax <= std::ldexp(1.f, 15 - kXShift);
     m->tc_gemm = m->tc_ok;
     if (m->tc_gemm) {
       m->us_g = upload_kmajor_split(m, Wg.data(), din + dh, 3 * dh, m->xsp, rowmap, &m->Wg_hi, &m->Wg_lo);

@@ -222,6 +222,18 @@ inline int launch_gemm_simt(GemmArgs g, const Epi &epi, int nz, int splits, cuda
   return 2;
 }
 
+// 4 consecutive columns (n % 4 == 0, 16-byte aligned rows): fp16 split copies
+__device__ __forceinline__ void store_split4(__half *hi, __half *lo, long long off, float4 v) {
+  if (!hi) return;
+  __half h[4], l[4];
+  split_h(v.x, h[0], l[0]);
+  split_h(v.y, h[1], l[1]);
+  split_h(v.z, h[2], l[2]);
+  split_h(v.w, h[3], l[3]);
+  *reinterpret_cast<uint2 *>(hi + off) = *reinterpret_cast<const uint2 *>(h);
+  *reinterpret_cast<uint2 *>(lo + off) = *reinterpret_cast<const uint2 *>(l);
+}
+
 // ------------------------------------------------------------------ epilogues
 
 // C = act(acc + bias)    act: 0 identity, 1 tanh
@@ -245,6 +257,38 @@ struct EpiStore {
       ex2[(long long)m * ldc + n] = y;
     }
     store_split(hi, lo, (long long)m * ldh + n, v);
+  }
+  // two-phase 4-column form for the tensor-core reduction (gemm_sk.cuh):
+  // every load of a batch of items is issued before any of its stores
+  struct Pre {
+    float4 b;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    Pre p;
+    p.b = bias ? *reinterpret_cast<const float4 *>(bias + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    v.x += p.b.x;
+    v.y += p.b.y;
+    v.z += p.b.z;
+    v.w += p.b.w;
+    if (act == 1) {
+      v.x = tanhf(v.x);
+      v.y = tanhf(v.y);
+      v.z = tanhf(v.z);
+      v.w = tanhf(v.w);
+    }
+    if (C) *reinterpret_cast<float4 *>(C + (long long)m * ldc + n) = v;
+    if (ex2) {
+      float4 y;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.x) : "f"(v.x * 2.8853900817779268f));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.y) : "f"(v.y * 2.8853900817779268f));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.z) : "f"(v.z * 2.8853900817779268f));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.w) : "f"(v.w * 2.8853900817779268f));
+      *reinterpret_cast<float4 *>(ex2 + (long long)m * ldc + n) = y;
+    }
+    store_split4(hi, lo, (long long)m * ldh + n, v);
   }
 };
 
@@ -270,6 +314,34 @@ struct EpiGruA {
       XH[(long long)m * dh + n - 2 * dh] = v;
     }
   }
+  struct Pre {
+    float4 b, s;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    Pre p;
+    p.b = *reinterpret_cast<const float4 *>(bias + n);
+    p.s = (n >= dh && n < 2 * dh) ? *reinterpret_cast<const float4 *>(S + (long long)m * lds + n - dh)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    v.x += p.b.x;
+    v.y += p.b.y;
+    v.z += p.b.z;
+    v.w += p.b.w;
+    if (n < dh) {
+      *reinterpret_cast<float4 *>(Z + (long long)m * dh + n) =
+          make_float4(sigmoid_acc(v.x), sigmoid_acc(v.y), sigmoid_acc(v.z), sigmoid_acc(v.w));
+    } else if (n < 2 * dh) {
+      const long long o = (long long)m * dh + n - dh;
+      const float4 rh = make_float4(sigmoid_acc(v.x) * p.s.x, sigmoid_acc(v.y) * p.s.y, sigmoid_acc(v.z) * p.s.z,
+                                    sigmoid_acc(v.w) * p.s.w);
+      *reinterpret_cast<float4 *>(RH + o) = rh;
+      store_split4(RHh, RHl, o, rh);
+    } else {
+      *reinterpret_cast<float4 *>(XH + (long long)m * dh + n - 2 * dh) = v;
+    }
+  }
 };
 
 // Decoder GRU phase B (nnet.py:69-70): h~ = tanh(xW_h + b_h + (r*h)U_h),
@@ -289,6 +361,27 @@ struct EpiGruB {
     const float sn = (1.0f - zz) * s + zz * ht;
     Sn[o] = sn;
     store_split(Snh, Snl, o, sn);
+  }
+  struct Pre {
+    float4 xh, z, s;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    const long long o = (long long)m * dh + n;
+    Pre p;
+    p.xh = *reinterpret_cast<const float4 *>(XH + o);
+    p.z = *reinterpret_cast<const float4 *>(Z + o);
+    p.s = *reinterpret_cast<const float4 *>(S + (long long)m * lds + n);
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    const long long o = (long long)m * dh + n;
+    float4 sn;
+    sn.x = (1.0f - p.z.x) * p.s.x + p.z.x * tanhf(v.x + p.xh.x);
+    sn.y = (1.0f - p.z.y) * p.s.y + p.z.y * tanhf(v.y + p.xh.y);
+    sn.z = (1.0f - p.z.z) * p.s.z + p.z.z * tanhf(v.z + p.xh.z);
+    sn.w = (1.0f - p.z.w) * p.s.w + p.z.w * tanhf(v.w + p.xh.w);
+    *reinterpret_cast<float4 *>(Sn + o) = sn;
+    store_split4(Snh, Snl, o, sn);
   }
 };
 

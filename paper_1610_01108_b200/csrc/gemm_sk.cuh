@@ -51,7 +51,7 @@ struct SkCfg {
   static constexpr int kPR = PR_;
   static constexpr int kBoxR = 16;  // activation rows per TMA box
   static constexpr int kStages = STAGES_;
-  static constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 TMEM drain; all reduce
+  static constexpr int kThreads = 384;  // warp 0 TMA, warp 1 MMA, warps 2-5 TMEM drain; all 12 reduce
   static constexpr int kWBytes = 128 * kRowBytes;            // one of hi/lo weight tiles
   static constexpr int kXBytes = (kPR / CG_) * kRowBytes;    // one of hi/lo activation tiles (this CTA's rows)
   static constexpr int kStageBytes = 2 * kWBytes + 2 * kXBytes;
@@ -76,7 +76,7 @@ struct SkArgs {
   int kb_per_split;
   int splits;
   float unscale;  // 2^-(activation shift + weight shift)
-  int debug;  // microbenchmark knobs: 1 skip weight loads, 2 skip activation loads, 4 skip MMA
+  int debug;  // microbenchmark knobs: 1 skip weight loads, 2 skip activation loads, 4 skip MMA, 8 skip reduction
 };
 
 // Row layout of one pass: one MMA of N0 columns, or two (N0 + N1) when the
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(C::kThreads, 1)
         else
           tc::mma_commit(tfull);  // this pass's partial is complete in TMEM
       }
-    } else {
+    } else if (warp < 6) {
       // drain TMEM -> red[row][feature]; thread = feature (TMEM lane)
       const int lg = warp & 3;
       const int f = lg * 32 + lane;
@@ -278,33 +278,49 @@ __global__ void __launch_bounds__(C::kThreads, 1)
     const int re = min(nr, rb + per);
     const int items = max(0, re - rb) * 32;
     const uint32_t red_base = tc::smem_u32(red);
-    for (int idx = threadIdx.x; idx < items; idx += C::kThreads) {
-      const int r = rb + idx / 32;
-      const int q = idx % 32;
-      const uint32_t off = red_base + (uint32_t)(r * 128 + 4 * q) * 4u;
-      float4 p[C::kMaxSplits];
+    // items of (row, 4 features); kU items per thread per batch: all DSMEM
+    // and epilogue loads of a batch are issued before its stores
+    constexpr int kU = 2;
+    for (int base = threadIdx.x; base < ((a.debug & 8) ? 0 : items); base += kU * C::kThreads) {
+      float4 acc[kU];
+      bool ok[kU];
+      int mm[kU], nn[kU];
 #pragma unroll
-      for (int s = 0; s < C::kMaxSplits; ++s)
-        if (s < S) p[s] = tc::ld_dsmem_v4(tc::mapa_shared(off, (uint32_t)(member + CG * s)));
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < kU; ++u) {
+        const int idx = base + u * C::kThreads;
+        const int r = rb + idx / 32;
+        const int q = idx % 32;
+        nn[u] = n0 + 4 * q;
+        mm[u] = row0 + r;
+        ok[u] = idx < items && nn[u] < a.N;
+        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (idx < items) {
+          const uint32_t off = red_base + (uint32_t)(r * 128 + 4 * q) * 4u;
+          float4 p[C::kMaxSplits];
 #pragma unroll
-      for (int s = 0; s < C::kMaxSplits; ++s)
-        if (s < S) {
-          acc.x += p[s].x;
-          acc.y += p[s].y;
-          acc.z += p[s].z;
-          acc.w += p[s].w;
+          for (int s = 0; s < C::kMaxSplits; ++s)
+            if (s < S) p[s] = tc::ld_dsmem_v4(tc::mapa_shared(off, (uint32_t)(member + CG * s)));
+#pragma unroll
+          for (int s = 0; s < C::kMaxSplits; ++s)
+            if (s < S) {
+              acc[u].x += p[s].x;
+              acc[u].y += p[s].y;
+              acc[u].z += p[s].z;
+              acc[u].w += p[s].w;
+            }
+          acc[u].x *= a.unscale;
+          acc[u].y *= a.unscale;
+          acc[u].z *= a.unscale;
+          acc[u].w *= a.unscale;
         }
-      acc.x *= a.unscale;
-      acc.y *= a.unscale;
-      acc.z *= a.unscale;
-      acc.w *= a.unscale;
-      const int n = n0 + 4 * q;
-      const int m = row0 + r;
-      if (n + 0 < a.N) epi(m, n + 0, acc.x, 0);
-      if (n + 1 < a.N) epi(m, n + 1, acc.y, 0);
-      if (n + 2 < a.N) epi(m, n + 2, acc.z, 0);
-      if (n + 3 < a.N) epi(m, n + 3, acc.w, 0);
+      }
+      typename Epi::Pre pre[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (ok[u]) pre[u] = epi.load4(mm[u], nn[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (ok[u]) epi.store4(mm[u], nn[u], acc[u], pre[u]);
     }
     tc::fence_proxy_async();
     tc::tc_fence_before();

@@ -1,6 +1,8 @@
 // Microbenchmark of the decoder-step tensor-core GEMM (gemm_sk.cuh; not part
-// of the product): sweeps tile configurations and split counts on the GRU
-// phase-A / query / deep-output shapes, L2 flushed before every launch.
+// of the product): the GRU phase-A / query / GRU phase-B / deep-output shapes
+// at several split counts, L2 flushed before every launch, with the
+// attribution knobs (debug: 1 skip weight loads, 2 skip activation loads,
+// 4 skip MMA, 8 skip reduction + epilogue).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lcuda \
 //     tools/bench_sk.cu paper_1610_01108_b200/csrc/logits_tc.cu -o build/bench_sk
 #include <cmath>
@@ -16,47 +18,63 @@ using namespace amun;
 struct Shape {
   const char *name;
   int N, k1, k2;
+  bool grub;  // GRU phase-B epilogue instead of a plain store
 };
 
 static unsigned g_seed = 1;
-static float *dev_rand(size_t n) {
-  std::vector<float> h(n);
+static __half *dev_rand_h(size_t n) {
+  std::vector<__half> h(n);
   srand(g_seed++);
-  for (auto &x : h) x = (rand() / (float)RAND_MAX - 0.5f) * 0.2f;
-  float *d;
-  cudaMalloc(&d, n * sizeof(float));
-  cudaMemcpy(d, h.data(), n * sizeof(float), cudaMemcpyHostToDevice);
+  for (auto &x : h) x = __float2half_rn((rand() / (float)RAND_MAX - 0.5f) * 100.f);
+  __half *d;
+  cudaMalloc(&d, n * sizeof(__half));
+  cudaMemcpy(d, h.data(), n * sizeof(__half), cudaMemcpyHostToDevice);
   return d;
 }
-
-static std::vector<float> g_ref;
+static float *dev_zero(size_t n) {
+  float *d;
+  cudaMalloc(&d, n * sizeof(float));
+  cudaMemset(d, 0, n * sizeof(float));
+  return d;
+}
 
 template <class C>
 void run(const char *cname, const Shape &sh, int R, float *flush, size_t flush_n, int debug) {
   const int K = sh.k1 + sh.k2;
   g_seed = 1;
-  float *xh = dev_rand((size_t)R * sh.k1), *xl = dev_rand((size_t)R * sh.k1);
-  float *x2h = sh.k2 ? dev_rand((size_t)R * sh.k2) : nullptr, *x2l = sh.k2 ? dev_rand((size_t)R * sh.k2) : nullptr;
-  float *wh = dev_rand((size_t)sh.N * K), *wl = dev_rand((size_t)sh.N * K);
-  float *out;
-  cudaMalloc(&out, sizeof(float) * R * sh.N);
-  SkMaps maps = make_sk_maps<C>(xh, xl, sh.k1, sh.k1, x2h, x2l, sh.k2, sh.k2, R, wh, wl, sh.N, K);
+  __half *xh = dev_rand_h((size_t)R * sh.k1), *xl = dev_rand_h((size_t)R * sh.k1);
+  __half *x2h = sh.k2 ? dev_rand_h((size_t)R * sh.k2) : nullptr, *x2l = sh.k2 ? dev_rand_h((size_t)R * sh.k2) : nullptr;
+  __half *wh = dev_rand_h((size_t)sh.N * K), *wl = dev_rand_h((size_t)sh.N * K);
+  float *out = dev_zero((size_t)R * sh.N), *S = dev_zero((size_t)R * sh.N), *Z = dev_zero((size_t)R * sh.N),
+        *XH = dev_zero((size_t)R * sh.N);
+  __half *oh, *ol;
+  cudaMalloc(&oh, sizeof(__half) * R * sh.N);
+  cudaMalloc(&ol, sizeof(__half) * R * sh.N);
+  SkMaps maps = make_sk_maps<C>(xh, xl, sh.k1, sh.k1, x2h, x2l, sh.k2, sh.k2, R, wh, wl, sh.N, K, 1.f / 1024);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int nt = ceil_div(sh.N, 128 * C::kCG) * C::kCG;
-  for (int S : {1, 2, 3, 4, 5, 6, 8}) {
-    const int splits = sk_splits<C>(maps, S * nt);
-    if (splits != S) continue;
+  for (int S_ : {1, 2, 3, 4, 6, 8}) {
+    const int splits = sk_splits<C>(maps, S_ * nt);
+    if (splits != S_) continue;
     if (C::kCG * splits > 16) continue;
-    const int maxc = sk_max_active_clusters<C, EpiStore>(splits);
     EpiStore epi{out, sh.N, nullptr, 0, 0};
+    EpiGruB eb{S, sh.N, sh.N, Z, XH, out};
+    eb.Snh = oh;
+    eb.Snl = ol;
+    auto launch = [&] {
+      if (sh.grub)
+        launch_gemm_sk<C>(maps, R, splits, eb, 0, debug);
+      else
+        launch_gemm_sk<C>(maps, R, splits, epi, 0, debug);
+    };
     float tot = 0.f, warm = 0.f;
     const int it = 10;
     for (int i = 0; i < it + 2; ++i) {
       cudaMemsetAsync(flush, i, flush_n * sizeof(float));
       cudaEventRecord(e0);
-      launch_gemm_sk<C>(maps, R, splits, epi, 0, debug);
+      launch();
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -64,23 +82,18 @@ void run(const char *cname, const Shape &sh, int R, float *flush, size_t flush_n
       if (i >= 2) tot += ms;
     }
     cudaEventRecord(e0);
-    for (int i = 0; i < it; ++i) launch_gemm_sk<C>(maps, R, splits, epi, 0, debug);
+    for (int i = 0; i < it; ++i) launch();
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&warm, e0, e1);
     cudaError_t err = cudaGetLastError();
-    std::vector<float> got((size_t)R * sh.N);
-    cudaMemcpy(got.data(), out, got.size() * sizeof(float), cudaMemcpyDeviceToHost);
-    if (g_ref.empty()) g_ref = got;
-    double md = 0;
-    for (size_t i = 0; i < got.size(); ++i) md = std::max(md, (double)std::fabs(got[i] - g_ref[i]));
     const double flops = 3.0 * 2.0 * R * (double)K * sh.N;
-    const double wbytes = 8.0 * K * sh.N;
+    const double wbytes = 4.0 * K * sh.N;
     const double us = 1000.0 * tot / it;
-    printf("%-8s %-14s R=%d S=%d ctas=%3d maxclusters=%3d dbg=%d  cold %7.1f us (%5.0f TF/s 3xTF32, W %5.0f GB/s)  "
-           "warm %7.1f us  maxdiff %.2e %s\n",
-           sh.name, cname, R, splits, splits * nt, maxc, debug, us, flops / us * 1e-6, wbytes / us * 1e-3,
-           1000.0 * warm / it, md, cudaGetErrorString(err));
+    printf("%-8s %-14s R=%d S=%d ctas=%3d dbg=%2d  cold %7.1f us (%5.0f TF/s issued f16, W %5.0f GB/s)  "
+           "warm %7.1f us  %s\n",
+           sh.name, cname, R, splits, splits * nt, debug, us, flops / us * 1e-6, wbytes / us * 1e-3,
+           1000.0 * warm / it, cudaGetErrorString(err));
   }
   cudaFree(xh);
   cudaFree(xl);
@@ -91,6 +104,11 @@ void run(const char *cname, const Shape &sh, int R, float *flush, size_t flush_n
   cudaFree(wh);
   cudaFree(wl);
   cudaFree(out);
+  cudaFree(S);
+  cudaFree(Z);
+  cudaFree(XH);
+  cudaFree(oh);
+  cudaFree(ol);
 }
 
 int main(int argc, char **argv) {
@@ -99,12 +117,10 @@ int main(int argc, char **argv) {
   const size_t flush_n = 256u << 20 >> 2;
   float *flush;
   cudaMalloc(&flush, flush_n * sizeof(float));
-  Shape shapes[] = {{"gru_a", 3072, 3572, 0}, {"query", 1024, 1024, 0}, {"deep_out", 500, 2548, 1024}};
-  for (auto &sh : shapes) {
-    g_ref.clear();
-    run<SkCfg<32, 2, 320, 1>>("bk32 st2 cg1", sh, R, flush, flush_n, debug);
-    run<SkCfg<32, 3, 320, 2>>("bk32 st3 cg2", sh, R, flush, flush_n, debug);
-    run<SkCfg<16, 5, 320, 2>>("bk16 st5 cg2", sh, R, flush, flush_n, debug);
-  }
+  Shape shapes[] = {{"gru_a", 3072, 3576, 0, false},
+                    {"query", 1024, 1024, 0, false},
+                    {"gru_b", 1024, 1024, 0, true},
+                    {"deep_out", 500, 2552, 1024, false}};
+  for (auto &sh : shapes) run<SkDefault>("bk64 st3 cg2", sh, R, flush, flush_n, debug);
   return 0;
 }

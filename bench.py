@@ -311,7 +311,8 @@ def main() -> None:
                                   max_len_offset=wl.max_len_offset, devices=(local,), max_batch=wl.batch),
                      [model], vocab, vocab, None, None, None, 0, 0.0)
         lines = W.lines_of(local_sents)
-        eng.translate_corpus(lines[:8])
+        for _ in range(max(args.warmup, 1)):  # same W warm-up steps as the device leg
+            eng.translate_corpus(lines)
         barrier()
         torch.cuda.synchronize()
         e2e_ms = 0.0

@@ -6,6 +6,7 @@
 #include <climits>
 #include <deque>
 #include <memory>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -47,6 +48,55 @@ struct DevMem {  // owning stream-ordered device allocation
     if (p) cudaFreeAsync(p, st);
   }
 };
+
+// Per-device pool of decode-lane resources reused across amun_decode calls:
+// stream, workspace (grown on demand), pinned probe ring and probe events.
+// Creating them per call (pinned allocation, stream-ordered workspace
+// allocation, event creation) cost tens of ms of host time per call.
+struct LaneRes {
+  cudaStream_t st = nullptr;
+  void *mem = nullptr;
+  size_t cap = 0;
+  int *h_probe = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+constexpr int kProbeSlots = 64;
+std::mutex g_lane_mu;
+std::vector<LaneRes *> g_lane_pool[64];
+
+LaneRes *lane_acquire(int dev) {
+  {
+    std::lock_guard<std::mutex> g(g_lane_mu);
+    auto &v = g_lane_pool[dev & 63];
+    if (!v.empty()) {
+      LaneRes *r = v.back();
+      v.pop_back();
+      return r;
+    }
+  }
+  std::unique_ptr<LaneRes> r(new LaneRes());
+  AMUN_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
+  AMUN_CUDA(cudaMallocHost(&r->h_probe, sizeof(int) * kProbeSlots));
+  r->ev.resize(kProbeSlots);
+  for (auto &e : r->ev) AMUN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return r.release();
+}
+void lane_release(int dev, LaneRes *r) {
+  std::lock_guard<std::mutex> g(g_lane_mu);
+  g_lane_pool[dev & 63].push_back(r);
+}
+// workspace of at least n bytes on the lane's stream
+void *lane_mem(LaneRes *r, size_t n) {
+  n = std::max<size_t>(n, 256);
+  if (r->cap < n) {
+    if (r->mem) AMUN_CUDA(cudaFreeAsync(r->mem, r->st));
+    r->mem = nullptr;
+    r->cap = 0;
+    AMUN_CUDA(cudaMallocAsync(&r->mem, n, r->st));
+    r->cap = n;
+  }
+  return r->mem;
+}
 
 // Launch context: stream, launch counter, byte counters, and (when
 // profiling) CUDA-event pairs around every launch, bucketed by kernel class.
@@ -470,12 +520,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
   const char *no_graph = getenv("AMUN_NO_GRAPH");
   const bool graphs_ok = o.profile == 0 && !(no_graph && no_graph[0] == '1');
-  constexpr int kProbeEvery = 8, kMaxAhead = 16, kProbeSlots = 64;
+  constexpr int kProbeEvery = 8, kMaxAhead = 16;
 
   struct Lane {
     cudaStream_t st = nullptr;
     std::unique_ptr<Ctx> c;
-    DevMem mem;
     std::vector<EncBufs> eb;
     std::vector<DecBufs> db;
     std::vector<float *> fin_states;
@@ -490,8 +539,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     float **p_fin;
     __half **p_XSh, **p_XSl;
     LogitTcMaps tc_maps{};
+    LaneRes *res = nullptr;  // pooled stream / workspace / probe ring
+    int dev = 0;
+    void *mem = nullptr;
     int *h_probe = nullptr;  // pinned ring of n_done probes
-    std::vector<cudaEvent_t> probe_ev;
+    cudaEvent_t *probe_ev = nullptr;
     std::deque<std::pair<int, int>> pending;  // (step, slot)
     int probe_next = 0;
     // current bucket
@@ -504,16 +556,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     int64_t step_launches = 0;
     ~Lane() {
       if (gexec) cudaGraphExecDestroy(gexec);
-      for (auto e : probe_ev) cudaEventDestroy(e);
-      if (h_probe) cudaFreeHost(h_probe);
       c.reset();
-      if (mem.p) {  // free on this lane's stream before the stream goes away
-        cudaFreeAsync(mem.p, st);
-        mem.p = nullptr;
-      }
-      if (st) {
+      if (res) {  // back to the pool once this call's work on the stream is done
         cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
+        lane_release(dev, res);
       }
     }
   };
@@ -521,7 +567,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   for (int li = 0; li < n_lanes; ++li) {
     lanes.emplace_back(new Lane());
     Lane &L = *lanes.back();
-    AMUN_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+    L.dev = m0->device;
+    L.res = lane_acquire(L.dev);
+    L.st = L.res->st;
+    L.h_probe = L.res->h_probe;
+    L.probe_ev = L.res->ev.data();
     L.c.reset(new Ctx(L.st));
     L.c->prof = (uint32_t)o.profile;
     L.eb.resize(n_models);
@@ -530,7 +580,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.tsteps.resize(n_models);
     for (int pass = 0; pass < 2; ++pass) {
       Carver cv;
-      cv.base = pass ? static_cast<char *>(L.mem.p) : nullptr;
+      cv.base = pass ? static_cast<char *>(L.mem) : nullptr;
       for (int m = 0; m < n_models; ++m) {
         carve_enc(cv, L.eb[m], ms[m], Bmax, jmax_all);
         carve_dec(cv, L.db[m], ms[m], Rmax, jmax_all, !fused);
@@ -575,7 +625,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.p_fin = cv.take<float *>(n_models);
       L.p_XSh = cv.take<__half *>(n_models);
       L.p_XSl = cv.take<__half *>(n_models);
-      if (!pass) L.mem.alloc(cv.off, L.st);
+      if (!pass) L.mem = lane_mem(L.res, cv.off);
     }
     if (use_tc) {
       static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
@@ -610,9 +660,6 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
         AMUN_CUDA(cudaMemsetAsync(L.db[m].XSh, 0, sizeof(__half) * (size_t)Rmax * ms[m]->xsp, L.st));
         AMUN_CUDA(cudaMemsetAsync(L.db[m].XSl, 0, sizeof(__half) * (size_t)Rmax * ms[m]->xsp, L.st));
       }
-    AMUN_CUDA(cudaMallocHost(&L.h_probe, sizeof(int) * kProbeSlots));
-    L.probe_ev.resize(kProbeSlots);
-    for (auto &e : L.probe_ev) AMUN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
 
   cudaEvent_t ev0, ev1;
@@ -783,9 +830,19 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     d2h(c, steps.data(), bs.steps, B);
     d2h(c, fin_n.data(), bs.fin_n, B);
     d2h(c, score.data(), bs.score, R);
-    d2h(c, fin_score.data(), bs.fin_score, (size_t)B * fin_cap);
-    d2h(c, fin_t.data(), bs.fin_t, (size_t)B * fin_cap);
-    d2h(c, fin_par.data(), bs.fin_par, (size_t)B * fin_cap);
+    AMUN_CUDA(cudaStreamSynchronize(L.st));
+    // finished lists: only the used prefix of every sentence's row
+    const int fmax = *std::max_element(fin_n.begin(), fin_n.end());
+    if (fmax > 0) {
+      auto rows2d = [&](void *dst, const void *src, size_t esz) {
+        AMUN_CUDA(cudaMemcpy2DAsync(dst, fin_cap * esz, src, fin_cap * esz, fmax * esz, B, cudaMemcpyDeviceToHost,
+                                    L.st));
+        c.d2h += (int64_t)(fmax * esz * B);
+      };
+      rows2d(fin_score.data(), bs.fin_score, sizeof(double));
+      rows2d(fin_t.data(), bs.fin_t, sizeof(int));
+      rows2d(fin_par.data(), bs.fin_par, sizeof(int));
+    }
     d2h(c, bp_tok.data(), bs.bp_tok, (size_t)B * capm * k);
     d2h(c, bp_par.data(), bs.bp_par, (size_t)B * capm * k);
     std::vector<float> act_states, fin_st;

@@ -13,25 +13,27 @@ using namespace amun;
 int main(int argc, char **argv) {
   const int R = argc > 1 ? atoi(argv[1]) : 320, K = 500, V = 30000, kk = 5;
   const int ntiles = (V + 127) / 128;
-  std::vector<float> h((size_t)std::max(R, V) * K);
-  for (auto &x : h) x = (rand() / (float)RAND_MAX - 0.5f) * 0.2f;
-  float *thi, *tlo, *whi, *wlo, *bias, *pmax, *psum, *cval;
+  const int Kp = (K + 7) / 8 * 8;
+  std::vector<__half> h((size_t)std::max(R, V) * Kp);
+  for (auto &x : h) x = __float2half_rn((rand() / (float)RAND_MAX - 0.5f) * 100.f);
+  __half *thi, *tlo, *whi, *wlo;
+  float *bias, *pmax, *psum, *cval;
   int *ctok;
-  cudaMalloc(&thi, sizeof(float) * R * K);
-  cudaMalloc(&tlo, sizeof(float) * R * K);
-  cudaMalloc(&whi, sizeof(float) * (size_t)V * K);
-  cudaMalloc(&wlo, sizeof(float) * (size_t)V * K);
+  cudaMalloc(&thi, sizeof(__half) * R * Kp);
+  cudaMalloc(&tlo, sizeof(__half) * R * Kp);
+  cudaMalloc(&whi, sizeof(__half) * (size_t)V * Kp);
+  cudaMalloc(&wlo, sizeof(__half) * (size_t)V * Kp);
   cudaMalloc(&bias, sizeof(float) * V);
   cudaMalloc(&pmax, sizeof(float) * ntiles * R);
   cudaMalloc(&psum, sizeof(float) * ntiles * R);
   cudaMalloc(&cval, sizeof(float) * ntiles * R * kk);
   cudaMalloc(&ctok, sizeof(int) * ntiles * R * kk);
-  cudaMemcpy(thi, h.data(), sizeof(float) * R * K, cudaMemcpyHostToDevice);
-  cudaMemcpy(tlo, h.data(), sizeof(float) * R * K, cudaMemcpyHostToDevice);
-  cudaMemcpy(whi, h.data(), sizeof(float) * (size_t)V * K, cudaMemcpyHostToDevice);
-  cudaMemcpy(wlo, h.data(), sizeof(float) * (size_t)V * K, cudaMemcpyHostToDevice);
+  cudaMemcpy(thi, h.data(), sizeof(__half) * R * Kp, cudaMemcpyHostToDevice);
+  cudaMemcpy(tlo, h.data(), sizeof(__half) * R * Kp, cudaMemcpyHostToDevice);
+  cudaMemcpy(whi, h.data(), sizeof(__half) * (size_t)V * Kp, cudaMemcpyHostToDevice);
+  cudaMemcpy(wlo, h.data(), sizeof(__half) * (size_t)V * Kp, cudaMemcpyHostToDevice);
   cudaMemset(bias, 0, sizeof(float) * V);
-  LogitTcMaps maps = make_logit_maps(thi, tlo, R, K, K, whi, wlo, V);
+  LogitTcMaps maps = make_logit_maps(thi, tlo, R, K, Kp, whi, wlo, Kp, V);
   const char *names[] = {"full", "no A loads", "no B loads", "no A/B loads", "no MMA", "no epilogue",
                          "loads only (no MMA, no epi)", "MMA only (no loads, no epi)", "no top-k", "no sum pass",
                          "no stores", "no topk/sum/stores", "no merge", "no topk/sum/merge/stores"};
@@ -40,7 +42,7 @@ int main(int argc, char **argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int v = 0; v < 14; ++v) {
-    LogitTcArgs a{R, V, K, bias, kk, ntiles, pmax, psum, cval, ctok};
+    LogitTcArgs a{R, V, K, bias, kk, ntiles, 1.f / (1 << 20), pmax, psum, cval, ctok};
     a.debug_flags = flags[v];
     for (int i = 0; i < 3; ++i) launch_logits_tc(maps, a, 0);
     cudaEventRecord(e0);
@@ -57,7 +59,7 @@ int main(int argc, char **argv) {
     long long *dclk;
     cudaMalloc(&dclk, sizeof(long long) * 64 * 16);
     cudaMemset(dclk, 0, sizeof(long long) * 64 * 16);
-    LogitTcArgs a{R, V, K, bias, kk, ntiles, pmax, psum, cval, ctok};
+    LogitTcArgs a{R, V, K, bias, kk, ntiles, 1.f / (1 << 20), pmax, psum, cval, ctok};
     a.debug_clock = dclk;
     launch_logits_tc(maps, a, 0);
     cudaDeviceSynchronize();

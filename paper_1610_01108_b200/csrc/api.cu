@@ -130,6 +130,14 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
   auto rowmap = [de, pad](int c) { return c < de ? c : c + pad; };
   auto ident = [](int c) { return c; };
   auto cp = [&](int idx, size_t n) { return std::vector<float>(t[idx], t[idx] + n); };
+  {  // tensor-core path: 16-byte fp16 row pitches and activations inside the
+     // split's range (decoder rows |x| <= max(1, max|E_trg|) <= 2^(15 - kXShift);
+     // encoder states and annotations are GRU outputs in (-1, 1))
+    float emax = 0.f;
+    for (size_t i = 0; i < (size_t)V * de; ++i) emax = std::max(emax, std::fabs(t[T_E_TRG][i]));
+    for (size_t i = 0; i < (size_t)Vs * de; ++i) emax = std::max(emax, std::fabs(t[T_E_SRC][i]));
+    m->tc_ok = (de % 4 == 0) && (dh % 8 == 0) && (da % 8 == 0) && emax <= std::ldexp(1.f, 15 - kXShift);
+  }
 
   m->E_src = upload(m, cp(T_E_SRC, (size_t)Vs * de));
   m->E_trg = upload(m, cp(T_E_TRG, (size_t)V * de));
@@ -146,6 +154,7 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     }
     m->Wenc = upload(m, W);
     m->benc = upload(m, b);
+    if (m->tc_ok) m->us_x = upload_kmajor_split(m, W.data(), de, 6 * dh, m->dep, ident, &m->Wenc_hi, &m->Wenc_lo);
   }
   {  // encoder recurrent weights: Uzr [2][dh][2dh], Uh [2][dh][dh]
     std::vector<float> Uzr((size_t)2 * dh * 2 * dh), Uh((size_t)2 * dh * dh);
@@ -159,8 +168,14 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     }
     m->Uzr = upload(m, Uzr);
     m->Uh = upload(m, Uh);
+    if (m->tc_ok) {  // both directions stacked along K: [2dh, 2dh] and [2dh, dh]
+      m->us_ea = upload_kmajor_split(m, Uzr.data(), 2 * dh, 2 * dh, 2 * dh, ident, &m->Uzr_hi, &m->Uzr_lo);
+      m->us_eb = upload_kmajor_split(m, Uh.data(), 2 * dh, dh, 2 * dh, ident, &m->Uh_hi, &m->Uh_lo);
+    }
   }
   m->W_att_h = upload(m, cp(T_W_ATT_H, (size_t)2 * dh * da));
+  if (m->tc_ok)
+    m->us_p = upload_kmajor_split(m, t[T_W_ATT_H], 2 * dh, da, 2 * dh, ident, &m->Watth_hi, &m->Watth_lo);
   m->W_init = upload(m, cp(T_W_INIT, (size_t)2 * dh * dh));
   m->b_init = upload(m, cp(T_B_INIT, dh));
   m->W_att_s = upload(m, cp(T_W_ATT_S, (size_t)dh * da));
@@ -183,11 +198,6 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     m->Wg = upload(m, Wg);
     m->bg = upload(m, bg);
     m->Uh_dec = upload(m, cp(T_DEC + G_UH, (size_t)dh * dh));
-    // tensor-core path: 16-byte fp16 row pitches and activations inside
-    // the split's range (|x| <= max(1, max|E_trg|) <= 2^(15 - kXShift))
-    float emax = 0.f;
-    for (size_t i = 0; i < (size_t)V * de; ++i) emax = std::max(emax, std::fabs(t[T_E_TRG][i]));
-    m->tc_ok = (de % 4 == 0) && (dh % 8 == 0) && (da % 8 == 0) && emax <= std::ldexp(1.f, 15 - kXShift);
     m->tc_gemm = m->tc_ok;
     if (m->tc_gemm) {
       m->us_g = upload_kmajor_split(m, Wg.data(), din + dh, 3 * dh, m->xsp, rowmap, &m->Wg_hi, &m->Wg_lo);

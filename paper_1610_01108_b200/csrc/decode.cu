@@ -195,6 +195,10 @@ void gemm(Ctx &c, const GemmArgs &g, const Epi &e, int nz = 1, bool allow_split 
 // Encoder buffers of one model for a bucket of B sentences, jmax positions.
 struct EncBufs {
   float *XP, *Hann, *P, *Hs, *Zs, *RHs, *Hmean, *S0;
+  // tensor-core encoder (3xFP16 splits): block rows [2B][2dh] of the states
+  // (HH) and of r*h (RR), and the split annotations [B*jmax][2dh] (Ha)
+  __half *HHh = nullptr, *HHl = nullptr, *RRh = nullptr, *RRl = nullptr, *Hah = nullptr, *Hal = nullptr;
+  __half *Xh = nullptr, *Xl = nullptr;  // gathered source embeddings [B*jmax][dep] (input projection)
 };
 // Decoder row buffers of one model for R hypothesis rows.
 struct DecBufs {
@@ -217,6 +221,65 @@ void carve_enc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
   e.RHs = cv.take<float>((size_t)2 * B * dh);
   e.Hmean = cv.take<float>((size_t)B * 2 * dh);
   e.S0 = cv.take<float>((size_t)B * dh);
+}
+
+void carve_enc_tc(Carver &cv, EncBufs &e, const amun_model *m, int B, int jmax) {
+  const int dh = m->d.d_h;
+  e.HHh = cv.take<__half>((size_t)2 * B * 2 * dh);
+  e.HHl = cv.take<__half>((size_t)2 * B * 2 * dh);
+  e.RRh = cv.take<__half>((size_t)2 * B * 2 * dh);
+  e.RRl = cv.take<__half>((size_t)2 * B * 2 * dh);
+  e.Hah = cv.take<__half>((size_t)B * jmax * 2 * dh);
+  e.Hal = cv.take<__half>((size_t)B * jmax * 2 * dh);
+  e.Xh = cv.take<__half>((size_t)B * jmax * m->dep);
+  e.Xl = cv.take<__half>((size_t)B * jmax * m->dep);
+}
+
+// 3xFP16 split of the gathered source embeddings E_src[ids] (nnet.py:113,
+// 167-174), zero pad columns [de, dep): the input-projection A operand.
+__global__ void gather_split_kernel(const float *__restrict__ E, const int *__restrict__ ids, int de, int dep,
+                                    __half *xh, __half *xl) {
+  const long long r = blockIdx.x;
+  const float *src = E + (long long)ids[r] * de;
+  for (int c = threadIdx.x; c < dep; c += blockDim.x) {
+    __half h = __float2half_rn(0.f), l = h;
+    if (c < de) split_h(__ldg(src + c), h, l);
+    xh[r * dep + c] = h;
+    xl[r * dep + c] = l;
+  }
+}
+
+// Tensor-core encoder GEMMs of one model: recurrence phase A / B over the
+// 2B block rows, and precomp_att over the split annotations; split counts
+// from (N, K) only.
+struct TcEnc {
+  SkMaps x, a, b, p;
+  int sx = 1, sa = 1, sb = 1, sp = 1;
+};
+
+int enc_target_ctas() {
+  static int v = [] {
+    const char *e = getenv("AMUN_ENC_CTAS");
+    return e ? std::max(1, atoi(e)) : 64;
+  }();
+  return v;
+}
+
+void tc_enc_maps(const amun_model *m, const EncBufs &e, int Bmax, int jmax, TcEnc &te) {
+  const int dh = m->d.d_h, da = m->d.d_att;
+  te.a = make_sk_maps(e.HHh, e.HHl, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0, 2 * Bmax, m->Uzr_hi, m->Uzr_lo, 2 * dh,
+                      2 * dh, m->us_ea);
+  te.b = make_sk_maps(e.RRh, e.RRl, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0, 2 * Bmax, m->Uh_hi, m->Uh_lo, dh, 2 * dh,
+                      m->us_eb);
+  te.p = make_sk_maps(e.Hah, e.Hal, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0, Bmax * jmax, m->Watth_hi, m->Watth_lo,
+                      da, 2 * dh, m->us_p);
+  te.x = make_sk_maps(e.Xh, e.Xl, m->dep, m->dep, nullptr, nullptr, 0, 0, Bmax * jmax, m->Wenc_hi, m->Wenc_lo,
+                      6 * dh, m->dep, m->us_x);
+  const int t = enc_target_ctas();
+  te.sx = sk_fit_splits(te.x, t);
+  te.sa = sk_fit_splits(te.a, t);
+  te.sb = sk_fit_splits(te.b, t);
+  te.sp = sk_fit_splits(te.p, t);
 }
 
 void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, int jmax, bool full_logits) {
@@ -251,16 +314,44 @@ void carve_dec_tc(Carver &cv, DecBufs &d, const amun_model *m, int R) {
 // gather fused into the A-load), the bi-GRU recurrence (both directions per
 // launch), precomp_att, masked mean and the initial decoder state.
 void encode_bucket(Ctx &c, const amun_model *m, const EncBufs &e, const int *d_ids, const int *d_len, int B,
-                   int jmax) {
+                   int jmax, const TcEnc *te = nullptr) {
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att;
   c.cls = AMUN_K_ENCODER;
-  {
+  if (te) {  // input projection on tensor cores (embedding gather + split first)
+    c.run(AMUN_K_ENCODER, [&] {
+      gather_split_kernel<<<B * jmax, 128, 0, c.st>>>(m->E_src, d_ids, de, m->dep, e.Xh, e.Xl);
+      AMUN_CHECK_LAUNCH();
+    });
+    EpiStore ex{e.XP, 6 * dh, m->benc, 0, 0};
+    c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(te->x, B * jmax, te->sx, ex, c.st); });
+  } else {
     GemmArgs g = ga(B * jmax, 6 * dh, m->E_src, de, de, m->Wenc, 6 * dh);
     g.rows0 = d_ids;
     gemm(c, g, EpiStore{e.XP, 6 * dh, m->benc, 0, 0}, 1, false);
   }
   AMUN_CUDA(cudaMemsetAsync(e.Hs, 0, sizeof(float) * 2 * B * dh, c.st));
   AMUN_CUDA(cudaMemsetAsync(e.Hann, 0, sizeof(float) * (size_t)B * jmax * 2 * dh, c.st));
+  if (te) {
+    // block rows start as zeros (h0 = 0; the off-diagonal halves stay zero)
+    const size_t blk = sizeof(__half) * (size_t)2 * B * 2 * dh, ann = sizeof(__half) * (size_t)B * jmax * 2 * dh;
+    AMUN_CUDA(cudaMemsetAsync(e.HHh, 0, blk, c.st));
+    AMUN_CUDA(cudaMemsetAsync(e.HHl, 0, blk, c.st));
+    AMUN_CUDA(cudaMemsetAsync(e.RRh, 0, blk, c.st));
+    AMUN_CUDA(cudaMemsetAsync(e.RRl, 0, blk, c.st));
+    AMUN_CUDA(cudaMemsetAsync(e.Hah, 0, ann, c.st));
+    AMUN_CUDA(cudaMemsetAsync(e.Hal, 0, ann, c.st));
+    for (int t = 0; t < jmax; ++t) {
+      EpiEncA2 ea{e.XP, e.Hs, d_len, jmax, dh, t, B, e.Zs, e.RHs, e.RRh, e.RRl};
+      c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(te->a, 2 * B, te->sa, ea, c.st); });
+      EpiEncB2 eb{e.XP, e.Hs, d_len, jmax, dh, t, B, e.Zs, e.Hann, e.HHh, e.HHl, e.Hah, e.Hal};
+      c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(te->b, 2 * B, te->sb, eb, c.st); });
+    }
+    EpiStore ep{e.P, da, nullptr, 0, 0};
+    c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(te->p, B * jmax, te->sp, ep, c.st); });
+    c.run(AMUN_K_ENCODER, [&] { launch_masked_mean(e.Hann, d_len, B, jmax, 2 * dh, e.Hmean, c.st); });
+    gemm(c, ga(B, dh, e.Hmean, 2 * dh, 2 * dh, m->W_init, dh), EpiStore{e.S0, dh, m->b_init, 1, 0});
+    return;
+  }
   for (int t = 0; t < jmax; ++t) {
     GemmArgs a = ga(B, 2 * dh, e.Hs, dh, dh, m->Uzr, 2 * dh);
     a.a_zs = (long long)B * dh;
@@ -476,6 +567,9 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   const char *no_tcg = getenv("AMUN_NO_TC_GEMM");
   bool use_tcg = !(no_tc && no_tc[0] == '1') && !(no_tcg && no_tcg[0] == '1');
   for (auto *m : ms) use_tcg = use_tcg && m->tc_gemm;
+  const char *no_tce = getenv("AMUN_NO_TC_ENC");
+  bool use_tce = !(no_tc && no_tc[0] == '1') && !(no_tce && no_tce[0] == '1');
+  for (auto *m : ms) use_tce = use_tce && m->Uzr_hi;
   const int kk = std::min(k, V);
   const int ntiles = ceil_div(V, kBN);
 
@@ -529,6 +623,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     std::vector<DecBufs> db;
     std::vector<float *> fin_states;
     std::vector<TcStep> tsteps;
+    std::vector<TcEnc> tencs;
     int *d_ids, *d_len, *d_cap, *d_sl, *d_sl_off, *d_sl_len;
     float *pmax, *psum, *cval;
     int *ctok, *cand_tok;
@@ -578,11 +673,13 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.db.resize(n_models);
     L.fin_states.assign(n_models, nullptr);
     L.tsteps.resize(n_models);
+    L.tencs.resize(n_models);
     for (int pass = 0; pass < 2; ++pass) {
       Carver cv;
       cv.base = pass ? static_cast<char *>(L.mem) : nullptr;
       for (int m = 0; m < n_models; ++m) {
         carve_enc(cv, L.eb[m], ms[m], Bmax, jmax_all);
+        if (use_tce) carve_enc_tc(cv, L.eb[m], ms[m], Bmax, jmax_all);
         carve_dec(cv, L.db[m], ms[m], Rmax, jmax_all, !fused);
         if (!use_tc) L.db[m].T_hi = L.db[m].T_lo = nullptr;
         if (use_tcg) {
@@ -634,6 +731,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     if (use_tcg)
       for (int m = 0; m < n_models; ++m) tc_step_maps(ms[m], L.db[m], Rmax, L.tsteps[m]);
+    if (use_tce)
+      for (int m = 0; m < n_models; ++m) tc_enc_maps(ms[m], L.eb[m], Bmax, jmax_all, L.tencs[m]);
     std::vector<const void *> hx(n_models), hs(n_models), he(n_models), h0(n_models), hl(n_models), hf(n_models),
         hxh(n_models), hxl(n_models);
     for (int m = 0; m < n_models; ++m) {
@@ -725,7 +824,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       h2d(c, L.d_sl_off, slo.data(), B);
       h2d(c, L.d_sl_len, sll.data(), B);
     }
-    for (int m = 0; m < n_models; ++m) encode_bucket(c, ms[m], L.eb[m], L.d_ids, L.d_len, B, jmax);
+    for (int m = 0; m < n_models; ++m)
+      encode_bucket(c, ms[m], L.eb[m], L.d_ids, L.d_len, B, jmax, use_tce ? &L.tencs[m] : nullptr);
     L.bs.B = B;
     L.bs.k = k;
     L.bs.cap_max = L.capm;

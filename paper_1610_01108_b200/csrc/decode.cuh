@@ -32,6 +32,14 @@ struct amun_model {
   __half *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
   __half *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, xsp]
   float us_l = 1.f, us_q = 1.f, us_g = 1.f, us_u = 1.f, us_o = 1.f;
+  // encoder: recurrent weights of both directions stacked along K (the
+  // recurrence runs both directions as one block-structured GEMM, rows
+  // [fwd sentences ; bwd sentences]) and W_att_h^T for precomp_att
+  __half *Uzr_hi = nullptr, *Uzr_lo = nullptr;      // [2dh, 2dh]  (N = z|r, K = fwd|bwd state)
+  __half *Uh_hi = nullptr, *Uh_lo = nullptr;        // [dh, 2dh]
+  __half *Watth_hi = nullptr, *Watth_lo = nullptr;  // [da, 2dh]
+  __half *Wenc_hi = nullptr, *Wenc_lo = nullptr;    // [6dh, dep] input projection, both directions
+  float us_ea = 1.f, us_eb = 1.f, us_p = 1.f, us_x = 1.f;
   int64_t bytes = 0;
   std::vector<void *> allocs;
   cudaStream_t stream = nullptr;

@@ -433,6 +433,98 @@ struct EpiEncB {
 // Logit epilogue, fused mode: per (row, N-tile) partial log-sum-exp and the
 // tile's top-kk (logit desc, token asc).  Full logits never reach HBM.
 //   pmax/psum: [M][ntiles]   cval/ctok: [M][ntiles][kk]
+// Tensor-core encoder recurrence (gemm_sk.cuh, decode.cu encode_bucket):
+// both directions in one GEMM over 2B rows m = dir * B + b, with block rows
+// [h_fwd | 0] / [0 | h_bwd] against K-stacked weights [U_fwd ; U_bwd].  Same
+// arithmetic as EpiEncA / EpiEncB per (b, n, dir); additionally keeps the
+// 3xFP16 splits of r*h (phase-B input) and of h (next step's phase-A input,
+// and the annotation rows for precomp_att).
+struct EpiEncA2 {
+  const float *XP;
+  const float *Hs;  // [2B][dh]
+  const int *len;
+  int jmax, dh, t, B;
+  float *Z, *RH;            // [2B][dh]
+  __half *RRh, *RRl;        // [2B][2dh] block rows
+  struct Pre {
+    float4 xp, hs;
+    int L;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    Pre p;
+    const int dir = m >= B, b = m - dir * B;
+    p.L = len[b];
+    if (t < p.L) {
+      const int pos = dir == 0 ? t : p.L - 1 - t;
+      p.xp = *reinterpret_cast<const float4 *>(XP + ((long long)b * jmax + pos) * 6 * dh + dir * 3 * dh + n);
+      p.hs = n >= dh ? *reinterpret_cast<const float4 *>(Hs + (long long)m * dh + n - dh) : make_float4(0, 0, 0, 0);
+    }
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    if (t >= p.L) return;
+    const int dir = m >= B;
+    v.x += p.xp.x;
+    v.y += p.xp.y;
+    v.z += p.xp.z;
+    v.w += p.xp.w;
+    const long long o = (long long)m * dh;
+    if (n < dh) {
+      *reinterpret_cast<float4 *>(Z + o + n) =
+          make_float4(sigmoid_acc(v.x), sigmoid_acc(v.y), sigmoid_acc(v.z), sigmoid_acc(v.w));
+    } else {
+      const int j = n - dh;
+      const float4 rh = make_float4(sigmoid_acc(v.x) * p.hs.x, sigmoid_acc(v.y) * p.hs.y, sigmoid_acc(v.z) * p.hs.z,
+                                    sigmoid_acc(v.w) * p.hs.w);
+      *reinterpret_cast<float4 *>(RH + o + j) = rh;
+      store_split4(RRh, RRl, (long long)m * 2 * dh + dir * dh + j, rh);
+    }
+  }
+};
+struct EpiEncB2 {
+  const float *XP;
+  float *Hs;
+  const int *len;
+  int jmax, dh, t, B;
+  const float *Z;
+  float *Hann;               // [B][jmax][2dh]
+  __half *HHh, *HHl;         // [2B][2dh] block rows (next phase-A input)
+  __half *Hah, *Hal;         // [B][jmax][2dh] split annotations (precomp_att input)
+  struct Pre {
+    float4 xp, z, hs;
+    int L;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    Pre p;
+    const int dir = m >= B, b = m - dir * B;
+    p.L = len[b];
+    if (t < p.L) {
+      const int pos = dir == 0 ? t : p.L - 1 - t;
+      const long long o = (long long)m * dh + n;
+      p.xp = *reinterpret_cast<const float4 *>(XP + ((long long)b * jmax + pos) * 6 * dh + dir * 3 * dh + 2 * dh + n);
+      p.z = *reinterpret_cast<const float4 *>(Z + o);
+      p.hs = *reinterpret_cast<const float4 *>(Hs + o);
+    }
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    if (t >= p.L) return;
+    const int dir = m >= B, b = m - dir * B;
+    const int pos = dir == 0 ? t : p.L - 1 - t;
+    const long long o = (long long)m * dh + n;
+    float4 h;
+    h.x = (1.0f - p.z.x) * p.hs.x + p.z.x * tanhf(v.x + p.xp.x);
+    h.y = (1.0f - p.z.y) * p.hs.y + p.z.y * tanhf(v.y + p.xp.y);
+    h.z = (1.0f - p.z.z) * p.hs.z + p.z.z * tanhf(v.z + p.xp.z);
+    h.w = (1.0f - p.z.w) * p.hs.w + p.z.w * tanhf(v.w + p.xp.w);
+    *reinterpret_cast<float4 *>(Hs + o) = h;
+    const long long ao = ((long long)b * jmax + pos) * 2 * dh + dir * dh + n;
+    *reinterpret_cast<float4 *>(Hann + ao) = h;
+    store_split4(HHh, HHl, (long long)m * 2 * dh + dir * dh + n, h);
+    store_split4(Hah, Hal, ao, h);
+  }
+};
+
 struct EpiLogitTopK {
   static constexpr bool kTile = true;
   const float *bias;

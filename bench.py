@@ -264,41 +264,66 @@ def main() -> None:
     toks = allreduce(float(toks_local), "sum")
     value = toks / (ms_step / 1000.0)
 
-    # ---- roofline of the dominant kernel (logits + fused LSE/top-k)
+    # ---- roofline per tensor-core kernel class, headline = the dominant one
+    # (largest share of the eager pass).  Algorithmic work per launch
+    # (SURVEY §8(d)): FLOP = 2 x rows x (fp32 GEMM shape of
+    # the reference op); rows = average hypothesis rows per launch of the
+    # pass.  The kernels issue three fp16 MMAs per product (3xFP16 split),
+    # reported as "issued_frac".  Bytes = fp32-equivalent weight bytes once
+    # per launch (the hi/lo fp16 pair the kernel reads has the same size).
     peaks = {}
     pk = REPO / "MEASURED_PEAKS.json"
     if pk.exists():
         peaks = json.loads(pk.read_text())
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    de, V = W.D_EMB, W.V_TRG
-    # algorithmic bytes per launch: W_logit + b_logit in fp32
-    # once, the R input rows t (d_emb fp32 each) and R x beam (score, id)
-    # outputs; averaged over the launches of one step (one per bucket-step).
+    tc_peak = peaks.get("bf16_tflops", 2250.0)  # kind::f16 runs at the bf16 dense rate
+    de, dh, da, V = W.D_EMB, W.D_H, W.D_ATT, W.V_TRG
     lens = sorted(len(s) for s in local_sents)
-    tot_bytes = n_launch = 0
+    rows_sum = n_launch = 0
     for b in range(0, len(lens), wl.batch):
         chunk = lens[b:b + wl.batch]
         steps_b = max(wl.max_len_factor * L + wl.max_len_offset for L in chunk)
-        rows_b = len(chunk) * wl.beam
-        tot_bytes += steps_b * (de * V * 4 + V * 4 + rows_b * (de * 4 + wl.beam * 8))
+        rows_sum += steps_b * len(chunk) * wl.beam
         n_launch += steps_b
-    logit_bytes = tot_bytes / max(1, n_launch)
-    logit_launches = kcount.get("logits", 0)
-    logit_ms = kms.get("logits", 0.0)
-    avg_ms = logit_ms / max(1, logit_launches)
-    achieved = logit_bytes / (avg_ms / 1000.0) / 1e9 if avg_ms else 0.0
+    rows = rows_sum / max(1, n_launch)
+    shapes = {  # (K, N) of the fp32 GEMM each class computes per hypothesis row
+        "query": [(dh, da)],
+        "gru_a": [(de + 2 * dh, 3 * dh), (dh, 2 * dh)],  # x W_{z,r,h} + s U_{z,r}
+        "gru_b": [(dh, dh)],                            # (r*s) U_h
+        "deep_out": [(de + 3 * dh, de)],
+        "logits": [(de, V)],
+    }
+    classes = {}
+    for cls, kn in shapes.items():
+        n = kcount.get(cls, 0)
+        if not n:
+            continue
+        avg_ms = kms[cls] / n
+        flop = sum(2.0 * rows * k * nn for k, nn in kn)
+        wbytes = sum(4.0 * k * nn for k, nn in kn)
+        ach = flop / (avg_ms / 1e3) / 1e12
+        classes[cls] = {"launches": int(n), "avg_launch_ms": round(avg_ms, 4), "gflop_per_launch": round(flop / 1e9, 3),
+                        "achieved_tflops": round(ach, 1), "frac": round(ach / tc_peak, 4),
+                        "issued_frac": round(3 * ach / tc_peak, 4),
+                        "weight_gbs": round(wbytes / (avg_ms / 1e3) / 1e9, 1),
+                        "share_of_step": round(kms[cls] / max(prof.device_ms, 1e-9), 3)}
+    dom = max(classes, key=lambda c: kms[c])
+    d = classes[dom]
     traffic = None
-    tf = REPO / "profiles" / "logit_traffic.json"
+    tf = REPO / "profiles" / f"{dom}_traffic.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
-    roofline = {"kernel": "logits (GEMM + fused log-softmax partials + per-row top-k)", "bound": "hbm",
-                "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": int(logit_bytes), "avg_launch_ms": round(avg_ms, 4),
-                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if pk.exists() else "fallback",
-                "share_of_step": round(logit_ms / max(prof.device_ms, 1e-9), 3),
-                "timing": "CUDA events around every logits launch in an eager pass right after the timed "
-                          "(graph-replay) region",
+    roofline = {"kernel": dom, "bound": "tensor", "achieved": d["achieved_tflops"], "peak": tc_peak,
+                "unit": "TFLOP/s", "frac": d["frac"], "traffic": traffic,
+                "issued_frac": d["issued_frac"], "avg_launch_ms": d["avg_launch_ms"],
+                "gflop_per_launch": d["gflop_per_launch"], "rows_per_launch": round(rows, 1),
+                "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops; kind::f16 runs at the bf16 rate)"
+                if pk.exists() else "fallback (nominal dense bf16)",
+                "share_of_step": d["share_of_step"],
+                "timing": "CUDA events around every launch in an eager single-lane pass right after the timed "
+                          "(graph-replay, 8-lane) region",
+                "tensor_core_classes": classes,
+                "hbm_peak_gbs": hbm_peak,
                 "kernel_ms_per_step": breakdown,
                 "launches_per_step": {k: int(v) for k, v in prof.kernel_count.items()}}
 

@@ -83,6 +83,8 @@ typedef struct {
   int64_t h2d_bytes, d2h_bytes;  /* host<->device bytes moved by the call */
   double kernel_ms[AMUN_K_CLASSES];     /* profile: summed launch durations */
   int64_t kernel_count[AMUN_K_CLASSES]; /* profile: launches per class */
+  double host_setup_ms;     /* host time before the first device event (buckets, lanes, workspace) */
+  double host_post_ms;      /* host time after the last device event (result assembly) */
 } amun_result;
 
 /* ---- library / device ------------------------------------------------ */

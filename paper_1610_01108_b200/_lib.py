@@ -8,6 +8,7 @@ calls raise instead of computing anything on the host.
 from __future__ import annotations
 
 import ctypes
+import time
 import os
 import threading
 from pathlib import Path
@@ -49,7 +50,7 @@ class Result(ctypes.Structure):
                 ("tok_offsets", ctypes.POINTER(ctypes.c_int64)), ("tokens", _i32p), ("states", _f32p),
                 ("decoder_steps", _i64), ("kernel_launches", _i64), ("device_ms", ctypes.c_double),
                 ("h2d_bytes", _i64), ("d2h_bytes", _i64), ("kernel_ms", ctypes.c_double * 8),
-                ("kernel_count", _i64 * 8)]
+                ("kernel_count", _i64 * 8), ("host_setup_ms", ctypes.c_double), ("host_post_ms", ctypes.c_double)]
 
 KERNEL_CLASSES = ("encoder", "query", "attention", "gru_a", "gru_b", "deep_out", "logits", "select")
 
@@ -251,6 +252,8 @@ class DecodeOut:
         self.decoder_steps = res.decoder_steps
         self.kernel_launches = res.kernel_launches
         self.device_ms = res.device_ms
+        self.host_setup_ms = res.host_setup_ms
+        self.host_post_ms = res.host_post_ms
         self.h2d_bytes = res.h2d_bytes
         self.d2h_bytes = res.d2h_bytes
         self.kernel_ms = {k: res.kernel_ms[i] for i, k in enumerate(KERNEL_CLASSES)}
@@ -284,10 +287,14 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
     opts = DecodeOpts(beam_size, max_len_factor, max_len_offset, int(length_normalize), n_best, int(want_states),
                       max_batch, int(force_full_logits), int(profile))
     res = ctypes.POINTER(Result)()
+    t_call = time.perf_counter()
     check(lib.amun_decode(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(sentences),
                           None if sl_ids is None else _ptr(sl_ids, _i32p),
                           None if sl_len is None else _ptr(sl_len, _i32p), ctypes.byref(opts), ctypes.byref(res)))
+    t_ret = time.perf_counter()
     try:
-        return DecodeOut(res.contents, want_states)
+        out = DecodeOut(res.contents, want_states)
     finally:
         lib.amun_result_free(res)
+    out.call_ms = 1e3 * (t_ret - t_call)  # the C call, wall (vs device_ms inside it)
+    return out

@@ -3,10 +3,12 @@
 // final ranking.  Mirrors search.py:116-216 for a batch of sentences, the
 // way engine.py:181-221 fans sentences out — but as one device batch.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <deque>
 #include <memory>
 #include <mutex>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -59,6 +61,9 @@ struct LaneRes {
   size_t cap = 0;
   int *h_probe = nullptr;
   std::vector<cudaEvent_t> ev;
+  cudaGraphExec_t gexec = nullptr;  // step graph, updated in place per bucket
+  float *ws = nullptr;              // SIMT split-K partials
+  size_t ws_floats = 0;
 };
 constexpr int kProbeSlots = 64;
 std::mutex g_lane_mu;
@@ -75,6 +80,13 @@ LaneRes *lane_acquire(int dev) {
     }
   }
   std::unique_ptr<LaneRes> r(new LaneRes());
+  {  // keep freed pool memory mapped: stream syncs must not trim the pool
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   AMUN_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
   AMUN_CUDA(cudaMallocHost(&r->h_probe, sizeof(int) * kProbeSlots));
   r->ev.resize(kProbeSlots);
@@ -113,10 +125,17 @@ struct Ctx {
   int64_t kcount[AMUN_K_CLASSES] = {0};
   float *ws = nullptr;  // split-K partials (stream-ordered, grown on demand)
   size_t ws_floats = 0;
+  float **ws_keep = nullptr;  // when set, the buffer outlives the Ctx (pooled lane)
+  size_t *ws_keep_n = nullptr;
   explicit Ctx(cudaStream_t s) : st(s) {}
   ~Ctx() {
     for (auto e : pool) cudaEventDestroy(e);
-    if (ws) cudaFreeAsync(ws, st);
+    if (ws_keep) {
+      *ws_keep = ws;
+      *ws_keep_n = ws_floats;
+    } else if (ws) {
+      cudaFreeAsync(ws, st);
+    }
   }
   void ensure_ws(size_t n) {
     if (n <= ws_floats) return;
@@ -532,6 +551,7 @@ void d2h(Ctx &c, T *dst, const T *src, size_t n) {
 
 amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_ids, const int32_t *src_len,
                         int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o) {
+  const auto t_enter = std::chrono::steady_clock::now();
   amun_model *m0 = ms[0];
   AMUN_CUDA(cudaSetDevice(m0->device));
   const int n_models = (int)ms.size();
@@ -648,14 +668,23 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     LogitOut lo{};
     SelectArgs sa{};
     cudaGraphExec_t gexec = nullptr;
+    bool gstale = false;
     int64_t step_launches = 0;
     ~Lane() {
-      if (gexec) cudaGraphExecDestroy(gexec);
+      static const bool dbg = getenv("AMUN_DEBUG_TEARDOWN") != nullptr;
+      auto t0 = std::chrono::steady_clock::now();
+      if (res) res->gexec = gexec;  // kept (stale) for the next call to update
       c.reset();
+      auto t1 = std::chrono::steady_clock::now();
       if (res) {  // back to the pool once this call's work on the stream is done
         cudaStreamSynchronize(st);
         lane_release(dev, res);
       }
+      auto t2 = std::chrono::steady_clock::now();
+      if (dbg)
+        fprintf(stderr, "lane teardown: ctx %.2f ms, sync+release %.2f ms\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
     }
   };
   std::vector<std::unique_ptr<Lane>> lanes;
@@ -667,7 +696,13 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.st = L.res->st;
     L.h_probe = L.res->h_probe;
     L.probe_ev = L.res->ev.data();
+    L.gexec = L.res->gexec;
+    L.gstale = true;
     L.c.reset(new Ctx(L.st));
+    L.c->ws = L.res->ws;
+    L.c->ws_floats = L.res->ws_floats;
+    L.c->ws_keep = &L.res->ws;
+    L.c->ws_keep_n = &L.res->ws_floats;
     L.c->prof = (uint32_t)o.profile;
     L.eb.resize(n_models);
     L.db.resize(n_models);
@@ -772,6 +807,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
   } evg{ev0, ev1};
   AMUN_CUDA(cudaEventRecord(ev0, lanes[0]->st));
+  const auto t_ev0 = std::chrono::steady_clock::now();
   for (int li = 1; li < n_lanes; ++li) AMUN_CUDA(cudaStreamWaitEvent(lanes[li]->st, ev0, 0));
 
   std::vector<std::vector<HostHyp>> out_hyps(n_sent);
@@ -798,10 +834,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.active = true;
     L.stop = false;
     L.pending.clear();
-    if (L.gexec) {
-      cudaGraphExecDestroy(L.gexec);
-      L.gexec = nullptr;
-    }
+    L.gstale = true;  // the step graph is re-captured at step 1 and updated in place
     const int B = L.B, jmax = L.jmax;
     std::vector<int> ids((size_t)B * jmax, 0), lens(B), caps(B), slo(B), sll(B), slv;
     for (int i = 0; i < B; ++i) {
@@ -869,7 +902,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // without decoding to the cap.
   auto enqueue_step = [&](Lane &L) {
     Ctx &c = *L.c;
-    if (graphs_ok && L.capm > 2 && L.t == 1 && !L.gexec) {
+    if (graphs_ok && L.capm > 2 && L.t == 1 && (!L.gexec || L.gstale)) {
       const int64_t before = c.launches;
       cudaGraph_t graph = nullptr;
       AMUN_CUDA(cudaStreamBeginCapture(L.st, cudaStreamCaptureModeThreadLocal));
@@ -883,11 +916,24 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       AMUN_CUDA(cudaStreamEndCapture(L.st, &graph));
       L.step_launches = c.launches - before;
       c.launches = before;
-      cudaError_t ie = cudaGraphInstantiate(&L.gexec, graph, 0);
+      // same topology as the previous bucket's graph (only kernel arguments
+      // differ): update the executable graph instead of re-instantiating
+      bool updated = false;
+      if (L.gexec) {
+        cudaGraphExecUpdateResultInfo info{};
+        updated = cudaGraphExecUpdate(L.gexec, graph, &info) == cudaSuccess;
+        if (!updated) {
+          (void)cudaGetLastError();
+          cudaGraphExecDestroy(L.gexec);
+          L.gexec = nullptr;
+        }
+      }
+      cudaError_t ie = updated ? cudaSuccess : cudaGraphInstantiate(&L.gexec, graph, 0);
       cudaGraphDestroy(graph);
       AMUN_CUDA(ie);
+      L.gstale = false;
     }
-    if (L.gexec) {
+    if (L.gexec && !L.gstale) {
       AMUN_CUDA(cudaGraphLaunch(L.gexec, L.st));
       c.launches += L.step_launches;
     } else {
@@ -1039,6 +1085,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   }
   AMUN_CUDA(cudaEventRecord(ev1, lanes[0]->st));
   AMUN_CUDA(cudaEventSynchronize(ev1));
+  const auto t_ev1 = std::chrono::steady_clock::now();
   float ms_elapsed = 0.f;
   AMUN_CUDA(cudaEventElapsedTime(&ms_elapsed, ev0, ev1));
   Ctx c(nullptr);  // totals over lanes
@@ -1095,6 +1142,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     r->kernel_ms[i] = c.kms[i];
     r->kernel_count[i] = c.kcount[i];
   }
+  using ms_d = std::chrono::duration<double, std::milli>;
+  r->host_setup_ms = ms_d(t_ev0 - t_enter).count();
+  lanes.clear();  // lane teardown (back to the pool) counts as host post-processing
+  r->host_post_ms = ms_d(std::chrono::steady_clock::now() - t_ev1).count();
   return r;
 }
 

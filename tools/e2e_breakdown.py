@@ -29,5 +29,35 @@ for it in range(3):
     t2 = time.perf_counter()
     res = eng.translate_corpus(lines)
     t3 = time.perf_counter()
-    print(f"decode wall {1e3*(t1-t0):.1f} ms (device {out.device_ms:.1f}), hyps {1e3*(t2-t1):.1f} ms, "
+    print(f"decode wall {1e3*(t1-t0):.1f} ms (C call {out.call_ms:.1f}, device {out.device_ms:.1f}, host setup {out.host_setup_ms:.1f}, "
+          f"post {out.host_post_ms:.1f}), hyps {1e3*(t2-t1):.1f} ms, "
           f"translate_corpus wall {1e3*(t3-t2):.1f} ms, d2h {out.d2h_bytes/1e6:.1f} MB", flush=True)
+
+if len(sys.argv) > 1 and sys.argv[1] == "profile":
+    _orig = eng._decode
+    _t = {}
+
+    def _timed(*a, **k):
+        t0 = time.perf_counter()
+        r = _orig(*a, **k)
+        _t["dec"] = 1e3 * (time.perf_counter() - t0)
+        return r
+
+    eng._decode = _timed
+    import gc
+    for _ in range(6):
+        t0 = time.perf_counter()
+        eng.translate_corpus(lines)
+        print(f"translate_corpus {1e3 * (time.perf_counter() - t0):.1f} ms: _decode {_t['dec']:.1f} "
+              f"(device {eng.last_stats['device_ms'][0]:.1f}); gc counts {gc.get_count()}", flush=True)
+    import cProfile, pstats
+    for _ in range(5):
+        t0 = time.perf_counter()
+        eng.translate_corpus(lines)
+        print(f"translate_corpus {1e3 * (time.perf_counter() - t0):.1f} ms (device {eng.last_stats['device_ms']})",
+              flush=True)
+    pr = cProfile.Profile()
+    pr.enable()
+    eng.translate_corpus(lines)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(18)

@@ -62,6 +62,7 @@ struct LaneRes {
   int *h_probe = nullptr;
   std::vector<cudaEvent_t> ev;
   cudaGraphExec_t gexec = nullptr;  // step graph, updated in place per bucket
+  std::vector<uintptr_t> gkey;      // what the graph was captured for (models, options)
   float *ws = nullptr;              // SIMT split-K partials
   size_t ws_floats = 0;
 };
@@ -696,6 +697,21 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.st = L.res->st;
     L.h_probe = L.res->h_probe;
     L.probe_ev = L.res->ev.data();
+    // a pooled step graph is only updated in place for the same models and
+    // options (same kernels and cluster shapes; buckets differ in arguments
+    // and grid sizes only); otherwise it is rebuilt
+    {
+      std::vector<uintptr_t> key;
+      for (auto *m : ms) key.push_back(reinterpret_cast<uintptr_t>(m));
+      for (int v : {k, (int)use_tc, (int)use_tcg, (int)fused, (int)(sl_ids != nullptr), (int)o.want_states, Bmax,
+                    jmax_all, cap_all})
+        key.push_back((uintptr_t)(unsigned)v);
+      if (L.res->gexec && L.res->gkey != key) {
+        cudaGraphExecDestroy(L.res->gexec);
+        L.res->gexec = nullptr;
+      }
+      L.res->gkey = key;
+    }
     L.gexec = L.res->gexec;
     L.gstale = true;
     L.c.reset(new Ctx(L.st));

@@ -214,8 +214,9 @@ def test_batch_composition_invariance(gpu, full):
 
 
 def test_tensor_core_logits_match_cuda_core_path(gpu, full, monkeypatch):
-    """tcgen05 3xTF32 logit kernel vs the FP32 CUDA-core kernel on the same
-    decode: identical tokens, scores equal to FP32 rounding."""
+    """tcgen05 3xFP16 kernels (logits, decoder-step GEMMs, encoder) vs the
+    FP32 CUDA-core kernels on the same decode: identical tokens, scores equal
+    to FP32 rounding."""
     s = golden_full()["sets"]["cfg2_strat64"]
     sub = dict(s, src=s["src"][:32])
     a = _decode_set(full, sub)
@@ -251,3 +252,20 @@ def test_fused_and_full_logit_paths_agree(gpu, full):
         ha, hb = a.hyps(i)[0], b.hyps(i)[0]
         assert ha[0] == hb[0]
         assert abs(ha[1] - hb[1]) <= 1e-6 * abs(ha[1])
+
+
+@pytest.mark.parametrize("knob", ["AMUN_NO_TC_ENC", "AMUN_NO_TC_GEMM"])
+def test_tensor_core_encoder_and_step_gemms_match_cuda_core(gpu, full, monkeypatch, knob):
+    """One tensor-core subsystem at a time swapped for its FP32 CUDA-core
+    version (encoder: input projection, bi-GRU recurrence, precomp_att;
+    step: query / GRU / deep-output GEMMs): same tokens, scores within FP32
+    rounding of each other."""
+    s = golden_full()["sets"]["cfg2_strat64"]
+    sub = dict(s, src=s["src"][:24])
+    a = _decode_set(full, sub)
+    monkeypatch.setenv(knob, "1")
+    b = _decode_set(full, sub)
+    for i in range(24):
+        ha, hb = a.hyps(i)[0], b.hyps(i)[0]
+        assert ha[0] == hb[0], (knob, i)
+        assert abs(ha[1] - hb[1]) <= 1e-5 * abs(hb[1]), (knob, i, ha[1], hb[1])

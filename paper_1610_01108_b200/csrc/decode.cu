@@ -827,6 +827,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   for (int li = 1; li < n_lanes; ++li) AMUN_CUDA(cudaStreamWaitEvent(lanes[li]->st, ev0, 0));
 
   std::vector<std::vector<HostHyp>> out_hyps(n_sent);
+  unsigned long long *sel_dbg = nullptr;  // AMUN_DEBUG_SELECT: select-kernel phase cycles
+  if (getenv("AMUN_DEBUG_SELECT")) {
+    AMUN_CUDA(cudaMalloc(&sel_dbg, 8 * sizeof(unsigned long long)));
+    AMUN_CUDA(cudaMemset(sel_dbg, 0, 8 * sizeof(unsigned long long)));
+  }
   int64_t total_steps = 0;
   size_t next_bucket = 0;
 
@@ -907,6 +912,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     sa.sl_len = L.d_sl_len;
     sa.cand_lp = L.cand_lp;
     sa.cand_tok = L.cand_tok;
+    sa.dbg = sel_dbg;
   };
 
   // Enqueue one decoder step.  Step 0 runs eagerly (it also sizes lazily
@@ -1102,6 +1108,14 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   AMUN_CUDA(cudaEventRecord(ev1, lanes[0]->st));
   AMUN_CUDA(cudaEventSynchronize(ev1));
   const auto t_ev1 = std::chrono::steady_clock::now();
+  if (sel_dbg) {
+    unsigned long long h[8];
+    AMUN_CUDA(cudaMemcpy(h, sel_dbg, sizeof(h), cudaMemcpyDeviceToHost));
+    const double n = (double)std::max(1ull, h[4]);
+    fprintf(stderr, "select phases (cycles per CTA): rows %.0f | sentence top-k %.0f | update %.0f | gather %.0f (%llu CTAs)\n",
+            h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4]);
+    cudaFree(sel_dbg);
+  }
   float ms_elapsed = 0.f;
   AMUN_CUDA(cudaEventElapsedTime(&ms_elapsed, ev0, ev1));
   Ctx c(nullptr);  // totals over lanes

@@ -487,6 +487,7 @@ struct LaneList {
 template <int KMAX, class Out>
 __device__ __forceinline__ void warp_merge(const LaneList<KMAX> &L, int kk, Out out) {
   int h = 0;
+  __syncwarp();  // lanes reconverge after the lane-divergent scans: plain shuffles below
   for (int j = 0; j < kk; ++j) {
     Key mine = L.get(h);
     Key best = warp_best(mine);
@@ -529,6 +530,7 @@ __device__ __forceinline__ void warp_topk(int n, int kk, Get get, Out out) {
       }
     }
     int h = 0;
+    __syncwarp();
     for (int j = 0; j < kk; ++j) {
       Key mine = L.get(h);
       Key best = warp_best(mine);
@@ -562,8 +564,12 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   int *ch_par = ch_tok + k;                             // [k]
   int *fin_par = ch_par + k;                            // [k] finished this step: parent
   int *fin_idx = fin_par + k;                           // [k]
+  // phase-1 row candidates [k][kk] (log-prob, token), consumed by phase 2
+  double *c_lp = reinterpret_cast<double *>(smraw + (((size_t)k * (sizeof(double) + 4 * sizeof(int)) + 15) & ~size_t(15)));
+  int *c_tok = reinterpret_cast<int *>(c_lp + (size_t)k * sa.kk);
   __shared__ int s_nch, s_newna, s_nfin;
 
+  long long clk0 = clock64();
   const int b = blockIdx.x;
   if (bs.done[b]) return;
   const int t = bs.steps[b];  // this sentence's step index (graph-replay safe: no host-side t)
@@ -575,8 +581,8 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   // ---- phase 1: per active row, log-sum-exp and top-kk candidates
   for (int i = warp; i < na; i += nw) {
     const int r = b * k + i;
-    double *out_lp = sa.cand_lp + ((long long)b * k + i) * kk;
-    int *out_tok = sa.cand_tok + ((long long)b * k + i) * kk;
+    double *out_lp = c_lp + (size_t)i * kk;
+    int *out_tok = c_tok + (size_t)i * kk;
     if constexpr (FUSED) {
       // per-tile partial (max, sum) pairs, kept in registers (<= 8 per lane)
       constexpr int kPT = 8;
@@ -707,13 +713,42 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     }
   }
   __syncthreads();
+  if (sa.dbg && threadIdx.x == 0) { const long long c = clock64(); atomicAdd(sa.dbg + 0, (unsigned long long)(c - clk0)); clk0 = c; }
 
   // ---- phase 2: sentence top-k over na*kk candidates, key (score desc,
   // token asc, parent asc) with f64 scores (search.py:169-170, :75-91)
-  if (warp == 0) {
+  if (warp == 0 && na * kk <= 32) {
+    // one candidate per lane: its rank is the number of candidates that beat
+    // it in the total (score desc, token asc, parent asc) order; ranks < k
+    // are the selection, in order (no lists, no divergent shuffles)
     const int n = na * kk;
-    const double *clp = sa.cand_lp + (long long)b * k * kk;
-    const int *ctk = sa.cand_tok + (long long)b * k * kk;
+    Key me{-INFINITY, -1, -1};
+    if (lane < n) {
+      const int par = lane / kk;
+      me = Key{bs.score[b * k + par] + c_lp[lane], c_tok[lane], par};
+    }
+    const bool valid = lane < n && me.tok >= 0;
+    int rank = 0, nvalid = 0;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const double ov = __shfl_sync(0xffffffffu, me.v, j);
+      const int ot = __shfl_sync(0xffffffffu, me.tok, j);
+      const int op = __shfl_sync(0xffffffffu, me.par, j);
+      if (j < n && ot >= 0) {
+        ++nvalid;
+        rank += key_better(ov, ot, op, me.v, me.tok, me.par);
+      }
+    }
+    if (valid && rank < k) {
+      ch_v[rank] = me.v;
+      ch_tok[rank] = me.tok;
+      ch_par[rank] = me.par;
+    }
+    if (lane == 0) s_nch = min(k, nvalid);
+  } else if (warp == 0) {
+    const int n = na * kk;
+    const double *clp = c_lp;
+    const int *ctk = c_tok;
     int nch = 0;
     warp_topk<KMAX>(
         n, k,
@@ -733,6 +768,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     if (lane == 0) s_nch = nch;
   }
   __syncthreads();
+  if (sa.dbg && threadIdx.x == 0) { const long long c = clock64(); atomicAdd(sa.dbg + 1, (unsigned long long)(c - clk0)); clk0 = c; }
 
   // ---- phase 3: beam update (search.py:172-198)
   if (threadIdx.x == 0) {
@@ -783,6 +819,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     s_nfin = nfin;
   }
   __syncthreads();
+  if (sa.dbg && threadIdx.x == 0) { const long long c = clock64(); atomicAdd(sa.dbg + 2, (unsigned long long)(c - clk0)); clk0 = c; }
 
   // ---- phase 4: gather next-step decoder rows [E_trg[y] | . | s'_parent]
   // (float4 granules, 8 independent loads in flight per thread)
@@ -858,6 +895,8 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       }
     }
   }
+  __syncthreads();
+  if (sa.dbg && threadIdx.x == 0) { atomicAdd(sa.dbg + 3, (unsigned long long)(clock64() - clk0)); atomicAdd(sa.dbg + 4, 1ull); }
 }
 
 template <int KMAX, bool FUSED>
@@ -871,7 +910,8 @@ static void launch_select_t(const SelectArgs &sa, const BeamState &bs, const Mod
 
 void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, cudaStream_t st) {
   if (mr.n_models > kMaxModels) throw Error(4, "at most 8 ensemble members are supported on the device path");
-  size_t smem = (size_t)bs.k * (sizeof(double) + 4 * sizeof(int));
+  size_t smem = (((size_t)bs.k * (sizeof(double) + 4 * sizeof(int)) + 15) & ~size_t(15)) +
+                (size_t)bs.k * sa.kk * (sizeof(double) + sizeof(int));
   const int need = std::max(bs.k, sa.kk);  // list sizes used in phases 1 and 2
   if (sa.fused) {
     if (need <= 1) launch_select_t<1, true>(sa, bs, mr, smem, st);

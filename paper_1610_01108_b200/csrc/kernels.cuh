@@ -84,6 +84,7 @@ struct SelectArgs {
   const int *sl_ids, *sl_off, *sl_len;  // optional per-sentence shortlists
   double *cand_lp;  // scratch [B*k*kk]
   int *cand_tok;
+  unsigned long long *dbg = nullptr;  // profiling: summed clock64 per phase [6] (env AMUN_DEBUG_SELECT)
 };
 // search.py:161-198 for one step of every sentence of the bucket.
 void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, cudaStream_t st);

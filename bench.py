@@ -302,7 +302,12 @@ def main() -> None:
         flop = sum(2.0 * rows * k * nn for k, nn in kn)
         wbytes = sum(4.0 * k * nn for k, nn in kn)
         ach = flop / (avg_ms / 1e3) / 1e12
+        ctas = prof.kernel_ctas.get(cls, 0) / n
         classes[cls] = {"launches": int(n), "avg_launch_ms": round(avg_ms, 4), "gflop_per_launch": round(flop / 1e9, 3),
+                        "ctas_per_launch": round(ctas, 1),
+                        # fraction of the per-SM tensor peak on the SMs the launch occupies
+                        # (production runs 16 bucket lanes concurrently, each launch owns few SMs)
+                        "issued_frac_of_sms_used": round(3 * ach / tc_peak * 148 / ctas, 4) if ctas else None,
                         "achieved_tflops": round(ach, 1), "frac": round(ach / tc_peak, 4),
                         "issued_frac": round(3 * ach / tc_peak, 4),
                         "weight_gbs": round(wbytes / (avg_ms / 1e3) / 1e9, 1),
@@ -315,7 +320,8 @@ def main() -> None:
         traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
     roofline = {"kernel": dom, "bound": "tensor", "achieved": d["achieved_tflops"], "peak": tc_peak,
                 "unit": "TFLOP/s", "frac": d["frac"], "traffic": traffic,
-                "issued_frac": d["issued_frac"], "avg_launch_ms": d["avg_launch_ms"],
+                "issued_frac": d["issued_frac"], "issued_frac_of_sms_used": d["issued_frac_of_sms_used"],
+                "ctas_per_launch": d["ctas_per_launch"], "avg_launch_ms": d["avg_launch_ms"],
                 "gflop_per_launch": d["gflop_per_launch"], "rows_per_launch": round(rows, 1),
                 "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops; kind::f16 runs at the bf16 rate)"
                 if pk.exists() else "fallback (nominal dense bf16)",

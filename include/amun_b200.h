@@ -85,6 +85,7 @@ typedef struct {
   int64_t kernel_count[AMUN_K_CLASSES]; /* profile: launches per class */
   double host_setup_ms;     /* host time before the first device event (buckets, lanes, workspace) */
   double host_post_ms;      /* host time after the last device event (result assembly) */
+  int64_t kernel_ctas[AMUN_K_CLASSES];  /* profile: tensor-core CTAs launched per class */
 } amun_result;
 
 /* ---- library / device ------------------------------------------------ */

@@ -50,7 +50,8 @@ class Result(ctypes.Structure):
                 ("tok_offsets", ctypes.POINTER(ctypes.c_int64)), ("tokens", _i32p), ("states", _f32p),
                 ("decoder_steps", _i64), ("kernel_launches", _i64), ("device_ms", ctypes.c_double),
                 ("h2d_bytes", _i64), ("d2h_bytes", _i64), ("kernel_ms", ctypes.c_double * 8),
-                ("kernel_count", _i64 * 8), ("host_setup_ms", ctypes.c_double), ("host_post_ms", ctypes.c_double)]
+                ("kernel_count", _i64 * 8), ("host_setup_ms", ctypes.c_double), ("host_post_ms", ctypes.c_double),
+                ("kernel_ctas", _i64 * 8)]
 
 KERNEL_CLASSES = ("encoder", "query", "attention", "gru_a", "gru_b", "deep_out", "logits", "select")
 
@@ -258,6 +259,7 @@ class DecodeOut:
         self.d2h_bytes = res.d2h_bytes
         self.kernel_ms = {k: res.kernel_ms[i] for i, k in enumerate(KERNEL_CLASSES)}
         self.kernel_count = {k: res.kernel_count[i] for i, k in enumerate(KERNEL_CLASSES)}
+        self.kernel_ctas = {k: res.kernel_ctas[i] for i, k in enumerate(KERNEL_CLASSES)}
 
     def hyps(self, i: int):
         """[(tokens list, score, finished, states or None)] for sentence i."""

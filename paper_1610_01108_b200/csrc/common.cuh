@@ -32,6 +32,13 @@ struct Error : std::runtime_error {
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// CTAs of the most recent tensor-core launch on this host thread (profiling:
+// the decode driver attributes them to the launch's kernel class)
+inline int &last_launch_ctas() {
+  static thread_local int n = 0;
+  return n;
+}
+
 // Accurate transcendentals (SURVEY §7 hard part (f)): full-precision expf /
 // tanhf, never the .approx forms.
 __device__ __forceinline__ float sigmoid_acc(float x) { return 1.0f / (1.0f + expf(-x)); }

@@ -124,6 +124,7 @@ struct Ctx {
   size_t used = 0;
   double kms[AMUN_K_CLASSES] = {0};
   int64_t kcount[AMUN_K_CLASSES] = {0};
+  int64_t kctas[AMUN_K_CLASSES] = {0};  // tensor-core CTAs launched per class (profiling)
   float *ws = nullptr;  // split-K partials (stream-ordered, grown on demand)
   size_t ws_floats = 0;
   float **ws_keep = nullptr;  // when set, the buffer outlives the Ctx (pooled lane)
@@ -161,7 +162,9 @@ struct Ctx {
       return;
     }
     AMUN_CUDA(cudaEventRecord(next_event(), st));
+    last_launch_ctas() = 0;
     f();
+    kctas[k] += last_launch_ctas();
     AMUN_CUDA(cudaEventRecord(next_event(), st));
     rec_cls.push_back(k);
   }
@@ -1126,6 +1129,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     for (int i = 0; i < AMUN_K_CLASSES; ++i) {
       c.kms[i] += Lp->c->kms[i];
       c.kcount[i] += Lp->c->kcount[i];
+      c.kctas[i] += Lp->c->kctas[i];
     }
   }
 
@@ -1171,6 +1175,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   for (int i = 0; i < AMUN_K_CLASSES; ++i) {
     r->kernel_ms[i] = c.kms[i];
     r->kernel_count[i] = c.kcount[i];
+    r->kernel_ctas[i] = c.kctas[i];
   }
   using ms_d = std::chrono::duration<double, std::milli>;
   r->host_setup_ms = ms_d(t_ev0 - t_enter).count();

@@ -406,6 +406,7 @@ void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaS
   la[0].val.clusterDim.z = 1;
   cfg.attrs = la;
   cfg.numAttrs = 1;
+  last_launch_ctas() = (int)(cfg.gridDim.x * cfg.gridDim.y);
   AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, maps.wh, maps.wl, maps.x1h, maps.x1l, maps.x2h, maps.x2l, a, epi));
 }
 

@@ -464,6 +464,7 @@ void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
   la[0].val.clusterDim.z = 1;
   cfg.attrs = la;
   cfg.numAttrs = 1;
+  last_launch_ctas() = (int)cfg.gridDim.x;
   AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, a));
 }
 

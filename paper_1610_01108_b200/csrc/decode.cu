@@ -426,6 +426,10 @@ void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
   ts.q = make_sk_maps(d.XSh + s_off, d.XSl + s_off, dh, xp, nullptr, nullptr, 0, 0, Rmax, m->Wq_hi, m->Wq_lo, da,
                       dh, m->us_q);
   ts.g = make_sk_maps(d.XSh, d.XSl, xp, xp, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi, m->Wg_lo, 3 * dh, xp, m->us_g);
+  if ((2 * dh) % 256 == 0) {  // h-gate features: the state rows' weights are zero
+    ts.g.n_klim = 2 * dh;
+    ts.g.k_lim = dep + 2 * dh;
+  }
   ts.u = make_sk_maps(d.RHh, d.RHl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Uhd_hi, m->Uhd_lo, dh, dh, m->us_u);
   ts.o = make_sk_maps(d.XSh, d.XSl, s_off, xp, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi, m->Wo_lo, de, xp, m->us_o);
   const int t = tc_target_ctas();

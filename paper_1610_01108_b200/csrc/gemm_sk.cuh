@@ -67,6 +67,9 @@ struct SkMaps {
   CUtensorMap wh, wl, x1h, x1l, x2h, x2l;
   int N, k1, k2;
   float unscale;
+  // features >= n_klim only need the first k_lim K elements (their weight
+  // rows beyond are zero: the h-gate block of the decoder state rows)
+  int n_klim = 1 << 30, k_lim = 0;
 };
 
 struct SkArgs {
@@ -76,6 +79,7 @@ struct SkArgs {
   int kb_per_split;
   int splits;
   float unscale;  // 2^-(activation shift + weight shift)
+  int n_klim, nk_lim;  // CTA pairs at features >= n_klim run only the first nk_lim K blocks
   int debug;  // microbenchmark knobs: 1 skip weight loads, 2 skip activation loads, 4 skip MMA, 8 skip reduction
 };
 
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(C::kThreads, 1)
   const int split = (int)crank / CG;
   const int S = a.splits;
   const int n0 = blockIdx.y * 128 * CG + member * 128;  // this CTA's 128 features (TMEM lanes)
-  const int nk = a.nk1 + a.nk2;
+  const int nk = (blockIdx.y * 128 * CG >= a.n_klim) ? min(a.nk1 + a.nk2, a.nk_lim) : a.nk1 + a.nk2;
   const int kb0 = split * a.kb_per_split;
   const int kb1 = min(nk, kb0 + a.kb_per_split);
   const int nkb = max(0, kb1 - kb0);
@@ -384,6 +388,8 @@ void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaS
   a.kb_per_split = ceil_div(a.nk1 + a.nk2, splits);
   a.splits = splits;
   a.unscale = maps.unscale;
+  a.n_klim = maps.n_klim;
+  a.nk_lim = maps.k_lim > 0 ? ceil_div(maps.k_lim, C::kBK) : a.nk1 + a.nk2;
   a.debug = debug;
   auto kern = gemm_sk_kernel<C, Epi>;
   static bool attr[64] = {};

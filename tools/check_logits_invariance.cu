@@ -16,37 +16,37 @@ int main() {
   std::vector<float> h((size_t)V * K);
   srand(3);
   for (auto &x : h) x = (rand() / (float)RAND_MAX - 0.5f) * 0.2f;
-  std::vector<float> hh(h.size()), hl(h.size());
-  for (size_t i = 0; i < h.size(); ++i) {
-    unsigned u;
-    memcpy(&u, &h[i], 4);
-    u &= 0xFFFFE000u;
-    float t;
-    memcpy(&t, &u, 4);
-    hh[i] = t;
-    hl[i] = h[i] - t;
-  }
-  float *thi, *tlo, *whi, *wlo, *bias, *pmax, *psum, *cval;
+  const int Kp = (K + 7) / 8 * 8;  // 16-byte fp16 row pitch
+  std::vector<__half> hh((size_t)V * Kp, __float2half_rn(0.f)), hl(hh.size(), __float2half_rn(0.f));
+  for (int r = 0; r < V; ++r)  // 3xFP16 split of (x * 2^10), as the product does
+    for (int c = 0; c < K; ++c) {
+      const float x = h[(size_t)r * K + c] * 1024.f;
+      const __half a = __float2half_rn(x);
+      hh[(size_t)r * Kp + c] = a;
+      hl[(size_t)r * Kp + c] = __float2half_rn(x - __half2float(a));
+    }
+  __half *thi, *tlo, *whi, *wlo;
+  float *bias, *pmax, *psum, *cval;
   int *ctok;
-  cudaMalloc(&thi, sizeof(float) * Rmax * K);
-  cudaMalloc(&tlo, sizeof(float) * Rmax * K);
-  cudaMalloc(&whi, sizeof(float) * (size_t)V * K);
-  cudaMalloc(&wlo, sizeof(float) * (size_t)V * K);
+  cudaMalloc(&thi, sizeof(__half) * Rmax * Kp);
+  cudaMalloc(&tlo, sizeof(__half) * Rmax * Kp);
+  cudaMalloc(&whi, sizeof(__half) * (size_t)V * Kp);
+  cudaMalloc(&wlo, sizeof(__half) * (size_t)V * Kp);
   cudaMalloc(&bias, sizeof(float) * V);
   cudaMalloc(&pmax, sizeof(float) * ntiles * Rmax);
   cudaMalloc(&psum, sizeof(float) * ntiles * Rmax);
   cudaMalloc(&cval, sizeof(float) * ntiles * Rmax * kk);
   cudaMalloc(&ctok, sizeof(int) * ntiles * Rmax * kk);
-  cudaMemcpy(thi, hh.data(), sizeof(float) * Rmax * K, cudaMemcpyHostToDevice);
-  cudaMemcpy(tlo, hl.data(), sizeof(float) * Rmax * K, cudaMemcpyHostToDevice);
-  cudaMemcpy(whi, hh.data(), sizeof(float) * (size_t)V * K, cudaMemcpyHostToDevice);
-  cudaMemcpy(wlo, hl.data(), sizeof(float) * (size_t)V * K, cudaMemcpyHostToDevice);
+  cudaMemcpy(thi, hh.data(), sizeof(__half) * Rmax * Kp, cudaMemcpyHostToDevice);
+  cudaMemcpy(tlo, hl.data(), sizeof(__half) * Rmax * Kp, cudaMemcpyHostToDevice);
+  cudaMemcpy(whi, hh.data(), sizeof(__half) * (size_t)V * Kp, cudaMemcpyHostToDevice);
+  cudaMemcpy(wlo, hl.data(), sizeof(__half) * (size_t)V * Kp, cudaMemcpyHostToDevice);
   cudaMemcpy(bias, h.data(), sizeof(float) * V, cudaMemcpyHostToDevice);
   std::vector<float> ref_m, ref_s, ref_v;
   const int R0 = 25;
   for (int R : Rs) {
-    LogitTcMaps maps = make_logit_maps(thi, tlo, R, K, K, whi, wlo, V);
-    LogitTcArgs a{R, V, K, bias, kk, ntiles, pmax, psum, cval, ctok};
+    LogitTcMaps maps = make_logit_maps(thi, tlo, R, K, Kp, whi, wlo, Kp, V);
+    LogitTcArgs a{R, V, K, bias, kk, ntiles, 1.f / (1 << 20), pmax, psum, cval, ctok};
     launch_logits_tc(maps, a, 0);
     cudaDeviceSynchronize();
     std::vector<float> m((size_t)ntiles * R), s((size_t)ntiles * R), v((size_t)R * ntiles * kk);

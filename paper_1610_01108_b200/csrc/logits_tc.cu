@@ -39,7 +39,10 @@ namespace {
 constexpr int kBK = 64;                     // fp16 K elements per 128-byte swizzled row
 constexpr int kRowB = kBK * 2;
 constexpr int kStages = 3;
-constexpr int kUnitRows = 160;              // hypothesis rows per work unit (one MMA, N <= 160)
+#ifndef AMUN_LOGIT_UNIT_ROWS
+#define AMUN_LOGIT_UNIT_ROWS 160
+#endif
+constexpr int kUnitRows = AMUN_LOGIT_UNIT_ROWS;              // hypothesis rows per work unit (one MMA, N <= 160)
 constexpr int kXRows = kUnitRows / 2;       // rows staged by each CTA of the pair
 constexpr int kBoxR = 16;                   // activation rows per TMA box
 constexpr int kWB = 128 * kRowB;            // one of hi/lo weight tiles

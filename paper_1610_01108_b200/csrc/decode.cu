@@ -156,6 +156,11 @@ struct Ctx {
   }
   template <class F>
   void run(int k, F &&f) {
+    static const unsigned skip = [] {  // profiling ablation only: outputs are garbage
+      const char *e = getenv("AMUN_ABLATE_CLASSES");
+      return e ? (unsigned)strtoul(e, nullptr, 0) : 0u;
+    }();
+    if (skip & (1u << k)) return;
     ++launches;
     if (!(prof & (1u << k))) {
       f();
@@ -834,6 +839,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   for (int li = 1; li < n_lanes; ++li) AMUN_CUDA(cudaStreamWaitEvent(lanes[li]->st, ev0, 0));
 
   std::vector<std::vector<HostHyp>> out_hyps(n_sent);
+  long long host_launch_ns = 0, host_launch_n = 0;  // host time inside cudaGraphLaunch
   unsigned long long *sel_dbg = nullptr;  // AMUN_DEBUG_SELECT: select-kernel phase cycles
   if (getenv("AMUN_DEBUG_SELECT")) {
     AMUN_CUDA(cudaMalloc(&sel_dbg, 8 * sizeof(unsigned long long)));
@@ -963,7 +969,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.gstale = false;
     }
     if (L.gexec && !L.gstale) {
+      const auto tg0 = std::chrono::steady_clock::now();
       AMUN_CUDA(cudaGraphLaunch(L.gexec, L.st));
+      host_launch_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - tg0).count();
+      ++host_launch_n;
       c.launches += L.step_launches;
     } else {
       launch_step(L);
@@ -1115,6 +1124,9 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   AMUN_CUDA(cudaEventRecord(ev1, lanes[0]->st));
   AMUN_CUDA(cudaEventSynchronize(ev1));
   const auto t_ev1 = std::chrono::steady_clock::now();
+  if (getenv("AMUN_DEBUG_HOST"))
+    fprintf(stderr, "host: %lld graph launches, %.1f ms inside cudaGraphLaunch, decode loop %.1f ms\n", host_launch_n,
+            host_launch_ns / 1e6, std::chrono::duration<double, std::milli>(t_ev1 - t_ev0).count());
   if (sel_dbg) {
     unsigned long long h[8];
     AMUN_CUDA(cudaMemcpy(h, sel_dbg, sizeof(h), cudaMemcpyDeviceToHost));

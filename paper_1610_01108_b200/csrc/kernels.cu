@@ -315,6 +315,159 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
   }
 }
 
+// Fused per-sentence attention (one CTA of 512 threads per sentence):
+// the energies of every position for every beam row (factored tanh as in
+// attn_energy_kernel), the masked softmax in shared memory, and the context
+// (thread = 4 consecutive columns, all rows, positions summed in order).  One
+// launch and 64 CTAs per bucket step instead of two launches of 256 CTAs:
+// fewer, longer-lived CTAs leave the SMs to the tensor-core kernels of the
+// other bucket lanes (the step is throughput-bound with 16 lanes in flight).
+template <int KA>
+__global__ void __launch_bounds__(512, 1) attn_sent_kernel(AttnArgs a) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x;
+  if (a.n_act && a.done[b]) return;
+  const int k = a.rows_per_sent;
+  const int na = a.n_act ? a.n_act[b] : k;
+  const int J = a.len[b];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
+  float *vs = sm;                                    // [da]
+  float *al = vs + a.da;                             // [k][jmax]
+  int *qbig = reinterpret_cast<int *>(al + (size_t)k * a.jmax);  // [k]
+  for (int i = tid; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
+  for (int r = warp; r < na; r += nw) {
+    const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
+    float m = 0.f;
+    for (int c = lane; c < a.da; c += 32) m = fmaxf(m, fabsf(__ldg(qr + c)));
+    m = warp_max(m);
+    if (lane == 0) qbig[r] = m > kFactorSafe;
+  }
+  __syncthreads();
+  int anybig = 0;
+  for (int r = 0; r < na; ++r) anybig |= qbig[r];
+  // ---- energies: warp per source position (nnet.py:135-136)
+  for (int j = warp; j < J; j += nw) {
+    const float *pj = a.P + ((long long)b * a.jmax + j) * a.da;
+    float ep[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int i = lane + 32 * u;
+      ep[u] = i < a.da ? __ldg(pj + i) : 0.f;
+    }
+    float pm = 0.f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      pm = fmaxf(pm, fabsf(ep[u]));
+      ep[u] = tc_exp2(ep[u] * kTwoLog2e);
+    }
+    const bool pbig = warp_max(pm) > kFactorSafe;
+    if (!pbig && !anybig && na == KA && a.da == 1024) {
+      const float *eqr[KA];
+#pragma unroll
+      for (int r = 0; r < KA; ++r) eqr[r] = a.EQ + (long long)(b * k + r) * a.ldq + lane;
+      float acc[KA];
+#pragma unroll
+      for (int r = 0; r < KA; ++r) acc[r] = 0.f;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const float vi = vs[lane + 32 * u];
+#pragma unroll
+        for (int r = 0; r < KA; ++r)
+          acc[r] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], __ldg(eqr[r] + 32 * u), 1.0f)), 1.0f), acc[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < KA; ++r) {
+        const float sum = warp_sum(acc[r]);
+        if (lane == 0) al[r * a.jmax + j] = sum;
+      }
+    } else {
+      for (int r = 0; r < na; ++r) {
+        float s0 = 0.f;
+        const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
+        const float *er = a.EQ + (long long)(b * k + r) * a.ldq;
+        const bool direct = pbig || qbig[r];
+        for (int u = 0; u < 32; ++u) {
+          const int i = lane + 32 * u;
+          if (i < a.da)
+            s0 = fmaf(vs[i],
+                      direct ? tanh_attn(__ldg(pj + i) + __ldg(qr + i))
+                             : 1.0f - __fdividef(2.0f, fmaf(ep[u], __ldg(er + i), 1.0f)),
+                      s0);
+        }
+        const float sum = warp_sum(s0);
+        if (lane == 0) al[r * a.jmax + j] = sum;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- masked softmax over j < J, warp per row (nnet.py:137-139)
+  for (int r = warp; r < na; r += nw) {
+    float *e = al + r * a.jmax;
+    float mx = -INFINITY;
+    for (int j = lane; j < J; j += 32) mx = fmaxf(mx, e[j]);
+    mx = warp_max(mx);
+    float s = 0.f;
+    for (int j = lane; j < J; j += 32) {
+      const float x = expf(e[j] - mx);
+      e[j] = x;
+      s += x;
+    }
+    s = warp_sum(s);
+    const float inv = 1.0f / s;
+    for (int j = lane; j < J; j += 32) {
+      const float x = e[j] * inv;
+      e[j] = x;
+      if (a.alpha) a.alpha[(long long)(b * k + r) * a.jmax + j] = x;
+    }
+  }
+  __syncthreads();
+  // ---- context (nnet.py:141): thread = 4 consecutive columns, every row
+  const int hs = a.dh2 / 4;
+  const float4 *Hb = reinterpret_cast<const float4 *>(a.H + (long long)b * a.jmax * a.dh2);
+  for (int c4 = tid; c4 < hs; c4 += blockDim.x) {
+    float4 acc[KA];
+#pragma unroll
+    for (int r = 0; r < KA; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j0 = 0; j0 < J; j0 += 8) {
+      float4 h[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        h[jj] = j0 + jj < J ? __ldg(Hb + (long long)(j0 + jj) * hs + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        if (j0 + jj >= J) break;
+#pragma unroll
+        for (int r = 0; r < KA; ++r)
+          if (r < na) {
+            const float w = al[r * a.jmax + j0 + jj];
+            acc[r].x = fmaf(w, h[jj].x, acc[r].x);
+            acc[r].y = fmaf(w, h[jj].y, acc[r].y);
+            acc[r].z = fmaf(w, h[jj].z, acc[r].z);
+            acc[r].w = fmaf(w, h[jj].w, acc[r].w);
+          }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < KA; ++r) {
+      if (r >= na) break;
+      const long long o = (long long)(b * k + r) * a.ldctx + 4 * c4;
+      *reinterpret_cast<float4 *>(a.ctx + o) = acc[r];
+      const long long oh = (long long)(b * k + r) * a.ldctx_h + 4 * c4;
+      store_split(a.ctx_hi, a.ctx_lo, oh + 0, acc[r].x);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 1, acc[r].y);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 2, acc[r].z);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 3, acc[r].w);
+    }
+  }
+}
+
+template <int KA>
+static void launch_sent(const AttnArgs &a, int B, size_t smem, cudaStream_t st) {
+  auto kern = attn_sent_kernel<KA>;
+  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<B, 512, smem, st>>>(a);
+}
+
 template <int KA>
 static void launch_energy(const AttnArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
   auto kern = attn_energy_kernel<KA>;
@@ -334,6 +487,29 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   const size_t smem = sizeof(float) * (size_t)k * a.jmax;
   const size_t smem_ctx = sizeof(float) * (((size_t)k * a.jmax + 3) & ~size_t(3)) + sizeof(float4) * kCtxRows * kCtxCols;
   const size_t smem_q = sizeof(float) * (size_t)a.da + sizeof(int) * (size_t)k;
+  static const bool fused = [] {
+    const char *e = getenv("AMUN_ATTN_FUSED");  // 0: two-phase kernels
+    return !(e && e[0] == '0');
+  }();
+  const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)k;
+  if (fused && a.EQ && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && k <= 16 && smem_s <= 200 * 1024 &&
+      (size_t)a.ldctx % 4 == 0 && reinterpret_cast<uintptr_t>(a.ctx) % 16 == 0) {
+    const int B = R / k;
+    switch (k) {  // exact beam width: no predicated-off rows in the inner loops
+      case 1: launch_sent<1>(a, B, smem_s, st); break;
+      case 2: launch_sent<2>(a, B, smem_s, st); break;
+      case 3: launch_sent<3>(a, B, smem_s, st); break;
+      case 4: launch_sent<4>(a, B, smem_s, st); break;
+      case 5: launch_sent<5>(a, B, smem_s, st); break;
+      case 6: launch_sent<6>(a, B, smem_s, st); break;
+      case 8: launch_sent<8>(a, B, smem_s, st); break;
+      case 10: launch_sent<10>(a, B, smem_s, st); break;
+      case 12: launch_sent<12>(a, B, smem_s, st); break;
+      default: launch_sent<16>(a, B, smem_s, st); break;
+    }
+    AMUN_CHECK_LAUNCH();
+    return 1;
+  }
   if (a.energy && a.EQ && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && smem_ctx <= 200 * 1024 && smem_q <= 200 * 1024) {
     const int B = R / k;
     const dim3 eg(ceil_div(a.jmax, kEnergyPos), B);

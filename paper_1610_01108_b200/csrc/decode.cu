@@ -417,10 +417,10 @@ struct TcStep {
 int tc_target_ctas() {
   static int v = [] {
     const char *e = getenv("AMUN_TC_CTAS");
-    // AMUN_TC_CTAS caps CTAs per GEMM launch; the default (16, swept) keeps every
+    // AMUN_TC_CTAS caps CTAs per GEMM launch; the default (12, swept) keeps every
     // decoder GEMM at one K split: each launch is SM-efficient and the
     // concurrent bucket lanes fill the machine
-    return e ? std::max(1, atoi(e)) : 16;
+    return e ? std::max(1, atoi(e)) : 12;
   }();
   return v;
 }
@@ -642,7 +642,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // small kernels of one bucket overlap with another bucket's GEMMs (every
   // bucket is still one batch of <= max_batch sentences).
   const char *lanes_env = getenv("AMUN_LANES");
-  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 16;
+  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 32;
   if (o.profile) n_lanes = 1;  // per-launch event timing wants one ordered stream
   n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
   const char *no_graph = getenv("AMUN_NO_GRAPH");

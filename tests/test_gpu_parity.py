@@ -269,3 +269,39 @@ def test_tensor_core_encoder_and_step_gemms_match_cuda_core(gpu, full, monkeypat
         ha, hb = a.hyps(i)[0], b.hyps(i)[0]
         assert ha[0] == hb[0], (knob, i)
         assert abs(ha[1] - hb[1]) <= 1e-5 * abs(hb[1]), (knob, i, ha[1], hb[1])
+
+
+def test_engine_translate_corpus_matches_beam_search(gpu):
+    """Engine.translate_corpus (batched device decode + vectorised
+    detokenisation) equals per-line beam_search + the reference's
+    detokenisation (engine.py:175-179): final </s> dropped, BPE "@@" pieces
+    joined, n-best order and scores, empty lines, OOV counts."""
+    from paper_1610_01108_b200.engine import Engine, EngineConfig
+    from paper_1610_01108_b200.model import Vocabulary
+    from paper_1610_01108_b200.subword import bpe_join
+
+    m = tiny_model(11, 30, 40, 8)
+    src_vocab = Vocabulary.from_tokens([f"s{i}" for i in range(2, 30)])
+    trg_vocab = Vocabulary.from_tokens([f"t{i}@@" if i % 3 == 0 else f"t{i}" for i in range(2, 40)])
+    cfg = EngineConfig(model_paths=("<memory>",), src_vocab_path="<memory>", trg_vocab_path="<memory>",
+                       beam_size=4, n_best=3, max_len_factor=1, max_len_offset=6, lowercase=False)
+    eng = Engine(cfg, [m], src_vocab, trg_vocab, None, None, None, 0, 0.0)
+    rng = np.random.default_rng(5)
+    lines = [" ".join(f"s{int(i)}" for i in rng.integers(2, 30, size=int(rng.integers(1, 9)))) for _ in range(40)]
+    lines[3] = ""
+    lines[7] = "s4 unknownword s5"
+    res = eng.translate_corpus(lines)
+    opts = DecodeOptions(beam_size=4, n_best=3, max_len_factor=1, max_len_offset=6)
+    for line, r in zip(lines, res):
+        if not line.split():
+            assert r.text == "" and r.score == 0.0
+            continue
+        ids = src_vocab.ids(line.split())
+        want = beam_search([m], ids, opts)
+        texts = []
+        for h in want:
+            toks = h.tokens[:-1] if h.finished and h.tokens and h.tokens[-1] == EOS_ID else h.tokens
+            texts.append(" ".join(bpe_join([trg_vocab.tokens[i] for i in toks])))
+        assert [t for _, t in r.n_best] == texts
+        assert [s for s, _ in r.n_best] == [h.score for h in want]
+        assert r.oov == sum(1 for t in line.split() if t not in src_vocab)

@@ -237,3 +237,29 @@ def test_workload_matches_survey_totals():
     c1 = WORKLOADS["cfg1"].corpus()
     assert sum(map(len, c1)) == 2813
     assert WORKLOADS["cfg2"].corpus() == orc.synthetic_corpus(4000, 2016, 100)
+
+
+def test_engine_vectorised_texts_match_detokenize():
+    """Engine._hyp_texts (flat device output -> strings) equals the
+    per-hypothesis reference detokenisation (engine.py:175-179)."""
+    from types import SimpleNamespace
+
+    from paper_1610_01108_b200.engine import Engine, EngineConfig
+    from paper_1610_01108_b200.model import EOS_ID, Vocabulary
+
+    trg = Vocabulary.from_tokens([f"t{i}@@" if i % 3 == 0 else f"t{i}" for i in range(2, 20)])
+    cfg = EngineConfig(model_paths=("<memory>",), src_vocab_path="<memory>", trg_vocab_path="<memory>")
+    eng = Engine(cfg, [tiny_model(1, 20, 20, 4)], trg, trg, None, None, None, 0, 0.0)
+    rng = np.random.default_rng(3)
+    hyps = []
+    for _ in range(60):
+        toks = [int(t) for t in rng.integers(1, 20, size=int(rng.integers(0, 9)))]
+        fin = bool(rng.integers(0, 2))
+        if fin:
+            toks.append(EOS_ID)
+        hyps.append((toks, fin))
+    flat = np.array([t for toks, _ in hyps for t in toks], np.int32)
+    offs = np.cumsum([0] + [len(t) for t, _ in hyps]).astype(np.int64)
+    res = SimpleNamespace(tokens=flat, tok_offsets=offs, finished=np.array([f for _, f in hyps]),
+                          scores=np.zeros(len(hyps)))
+    assert eng._hyp_texts(res) == [eng._detokenize(t, f) for t, f in hyps]

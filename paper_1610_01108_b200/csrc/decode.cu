@@ -642,7 +642,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // small kernels of one bucket overlap with another bucket's GEMMs (every
   // bucket is still one batch of <= max_batch sentences).
   const char *lanes_env = getenv("AMUN_LANES");
-  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 32;
+  int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 24;
   if (o.profile) n_lanes = 1;  // per-launch event timing wants one ordered stream
   n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
   const char *no_graph = getenv("AMUN_NO_GRAPH");
@@ -847,6 +847,17 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   }
   int64_t total_steps = 0;
   size_t next_bucket = 0;
+  // dispatch order: longest-running buckets first (step count x rows), so
+  // the short ones fill the lanes at the end instead of a long bucket
+  // running alone in the tail (bucket composition, hence every result, is
+  // unchanged)
+  std::vector<int> dispatch(buckets.size());
+  std::iota(dispatch.begin(), dispatch.end(), 0);
+  std::stable_sort(dispatch.begin(), dispatch.end(), [&](int x, int y) {
+    const long long wx = (long long)buckets[x].cap_max * buckets[x].count * (buckets[x].jmax + 8);
+    const long long wy = (long long)buckets[y].cap_max * buckets[y].count * (buckets[y].jmax + 8);
+    return wx > wy;
+  });
 
   auto launch_step = [&](Lane &L) {
     Ctx &c = *L.c;
@@ -1094,7 +1105,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   };
 
   for (auto &Lp : lanes)
-    if (next_bucket < buckets.size()) start_bucket(*Lp, (int)next_bucket++);
+    if (next_bucket < buckets.size()) start_bucket(*Lp, dispatch[next_bucket++]);
   for (;;) {
     bool any = false;
     for (auto &Lp : lanes) {
@@ -1104,7 +1115,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       poll(L, false);
       if (L.stop || L.t >= L.capm) {
         finish_bucket(L);
-        if (next_bucket < buckets.size()) start_bucket(L, (int)next_bucket++);
+        if (next_bucket < buckets.size()) start_bucket(L, dispatch[next_bucket++]);
         continue;
       }
       // bounded run-ahead past the newest probe the host has seen

@@ -65,15 +65,16 @@ struct LaneRes {
   std::vector<uintptr_t> gkey;      // what the graph was captured for (models, options)
   float *ws = nullptr;              // SIMT split-K partials
   size_t ws_floats = 0;
+  int high = 0;                     // stream created with the device's greatest priority
 };
 constexpr int kProbeSlots = 64;
 std::mutex g_lane_mu;
-std::vector<LaneRes *> g_lane_pool[64];
+std::vector<LaneRes *> g_lane_pool[64][2];  // [device][high priority]
 
-LaneRes *lane_acquire(int dev) {
+LaneRes *lane_acquire(int dev, int high) {
   {
     std::lock_guard<std::mutex> g(g_lane_mu);
-    auto &v = g_lane_pool[dev & 63];
+    auto &v = g_lane_pool[dev & 63][high ? 1 : 0];
     if (!v.empty()) {
       LaneRes *r = v.back();
       v.pop_back();
@@ -88,7 +89,12 @@ LaneRes *lane_acquire(int dev) {
       cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
-  AMUN_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
+  {
+    int least = 0, greatest = 0;
+    AMUN_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    r->high = high ? 1 : 0;
+    AMUN_CUDA(cudaStreamCreateWithPriority(&r->st, cudaStreamNonBlocking, high ? greatest : least));
+  }
   AMUN_CUDA(cudaMallocHost(&r->h_probe, sizeof(int) * kProbeSlots));
   r->ev.resize(kProbeSlots);
   for (auto &e : r->ev) AMUN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -96,7 +102,17 @@ LaneRes *lane_acquire(int dev) {
 }
 void lane_release(int dev, LaneRes *r) {
   std::lock_guard<std::mutex> g(g_lane_mu);
-  g_lane_pool[dev & 63].push_back(r);
+  g_lane_pool[dev & 63][r->high].push_back(r);
+}
+
+// lanes [0, n) run on high-priority streams: with longest-first dispatch
+// they carry the longest buckets, whose serial step chains bound the pass
+int high_priority_lanes() {
+  static int v = [] {
+    const char *e = getenv("AMUN_HIGH_LANES");
+    return e ? std::max(0, atoi(e)) : 0;  // swept: no measurable effect on cfg2
+  }();
+  return v;
 }
 // workspace of at least n bytes on the lane's stream
 void *lane_mem(LaneRes *r, size_t n) {
@@ -705,7 +721,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     lanes.emplace_back(new Lane());
     Lane &L = *lanes.back();
     L.dev = m0->device;
-    L.res = lane_acquire(L.dev);
+    L.res = lane_acquire(L.dev, li < high_priority_lanes());
     L.st = L.res->st;
     L.h_probe = L.res->h_probe;
     L.probe_ev = L.res->ev.data();

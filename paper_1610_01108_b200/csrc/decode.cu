@@ -883,7 +883,13 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     c.run(AMUN_K_SELECT, [&] { launch_select(L.sa, L.bs, L.mr, L.st); });
   };
 
+  // AMUN_DEBUG_SCHED: host-side (start, end) of every bucket, printed as a
+  // lane-occupancy profile after the decode
+  static const bool dbg_sched = getenv("AMUN_DEBUG_SCHED") != nullptr;
+  std::vector<std::pair<double, double>> bucket_span(buckets.size(), {0.0, 0.0});
+  auto now_ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enter).count(); };
   auto start_bucket = [&](Lane &L, int bi) {
+    if (dbg_sched) bucket_span[bi].first = now_ms();
     Ctx &c = *L.c;
     const Bucket &bk = buckets[bi];
     L.bucket = bi;
@@ -1030,6 +1036,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   };
 
   auto finish_bucket = [&](Lane &L) {
+    if (dbg_sched) bucket_span[L.bucket].second = now_ms();
     Ctx &c = *L.c;
     const Bucket &bk = buckets[L.bucket];
     const int B = L.B, capm = L.capm, R = L.R;
@@ -1151,6 +1158,23 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   AMUN_CUDA(cudaEventRecord(ev1, lanes[0]->st));
   AMUN_CUDA(cudaEventSynchronize(ev1));
   const auto t_ev1 = std::chrono::steady_clock::now();
+  if (dbg_sched) {
+    double t_end = 0;
+    for (auto &sp : bucket_span) t_end = std::max(t_end, sp.second);
+    fprintf(stderr, "sched: %zu buckets, last finish %.1f ms; active lanes per 10%% of the run:", buckets.size(), t_end);
+    for (int d = 0; d < 10; ++d) {
+      const double t = t_end * (d + 0.5) / 10;
+      int act = 0;
+      for (auto &sp : bucket_span) act += sp.first <= t && t < sp.second;
+      fprintf(stderr, " %d", act);
+    }
+    int longest = 0;
+    for (size_t i = 0; i < buckets.size(); ++i)
+      if (bucket_span[i].second - bucket_span[i].first > bucket_span[longest].second - bucket_span[longest].first) longest = (int)i;
+    fprintf(stderr, "; longest bucket %d: %d steps in %.1f ms (%.2f ms/step)\n", longest, buckets[longest].cap_max,
+            bucket_span[longest].second - bucket_span[longest].first,
+            (bucket_span[longest].second - bucket_span[longest].first) / std::max(1, buckets[longest].cap_max));
+  }
   if (getenv("AMUN_DEBUG_HOST"))
     fprintf(stderr, "host: %lld graph launches, %.1f ms inside cudaGraphLaunch, decode loop %.1f ms\n", host_launch_n,
             host_launch_ns / 1e6, std::chrono::duration<double, std::milli>(t_ev1 - t_ev0).count());

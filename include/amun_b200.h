@@ -113,6 +113,17 @@ int amun_decode(amun_model *const *models, int32_t n_models, const int32_t *src_
                 const int32_t *src_len, int32_t n_sent, const int32_t *shortlist_ids,
                 const int32_t *shortlist_len, const amun_decode_opts *opts, amun_result **out);
 int amun_result_free(amun_result *r);
+/* Streaming variant: as amun_decode, and after each length bucket finishes
+ * (while later buckets still decode) calls on_bucket(user, partial, idx):
+ * `partial` holds the final hypotheses of partial->n_sent sentences whose
+ * input positions are idx[0 .. n_sent); it and idx are valid during the
+ * call only.  Lets the caller post-process (detokenise) while the device
+ * works; the callback runs on the calling thread and should be short. */
+typedef void (*amun_bucket_done_fn)(void *user, const amun_result *partial, const int32_t *idx);
+int amun_decode_stream(amun_model *const *models, int32_t n_models, const int32_t *src_ids,
+                       const int32_t *src_len, int32_t n_sent, const int32_t *shortlist_ids,
+                       const int32_t *shortlist_len, const amun_decode_opts *opts, amun_bucket_done_fn on_bucket,
+                       void *user, amun_result **out);
 
 /* ---- per-step parity hooks (host pointers) ---------------------------- */
 /* Forward.encode + init_state_row (nnet.py:110-130):

@@ -27,7 +27,7 @@ AMUN_OK, AMUN_ERR_INVALID, AMUN_ERR_CUDA, AMUN_ERR_OOM, AMUN_ERR_UNSUPPORTED = 0
 EXPORTS = (
     "amun_last_error", "amun_version", "amun_device_count", "amun_model_create", "amun_model_destroy",
     "amun_model_device_bytes", "amun_decode", "amun_result_free", "amun_encode", "amun_attention",
-    "amun_decoder_step", "amun_init_state", "amun_gru_cell",
+    "amun_decoder_step", "amun_init_state", "amun_gru_cell", "amun_decode_stream",
 )
 
 _i32, _i64, _f32p, _f64p, _i32p = ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_float), \
@@ -52,6 +52,9 @@ class Result(ctypes.Structure):
                 ("h2d_bytes", _i64), ("d2h_bytes", _i64), ("kernel_ms", ctypes.c_double * 8),
                 ("kernel_count", _i64 * 8), ("host_setup_ms", ctypes.c_double), ("host_post_ms", ctypes.c_double),
                 ("kernel_ctas", _i64 * 8)]
+
+# void (*)(void *user, const amun_result *partial, const int32_t *idx)
+BUCKET_DONE = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.POINTER(Result), _i32p)
 
 KERNEL_CLASSES = ("encoder", "query", "attention", "gru_a", "gru_b", "deep_out", "logits", "select")
 
@@ -81,6 +84,9 @@ def load() -> ctypes.CDLL:
         lib.amun_decode.argtypes = [ctypes.POINTER(ctypes.c_void_p), _i32, _i32p, _i32p, _i32, _i32p, _i32p,
                                     ctypes.POINTER(DecodeOpts), ctypes.POINTER(ctypes.POINTER(Result))]
         lib.amun_result_free.argtypes = [ctypes.POINTER(Result)]
+        lib.amun_decode_stream.argtypes = [ctypes.POINTER(ctypes.c_void_p), _i32, _i32p, _i32p, _i32, _i32p, _i32p,
+                                           ctypes.POINTER(DecodeOpts), BUCKET_DONE, ctypes.c_void_p,
+                                           ctypes.POINTER(ctypes.POINTER(Result))]
         lib.amun_encode.argtypes = [ctypes.c_void_p, _i32p, _i32, _f32p, _f32p, _f32p]
         lib.amun_attention.argtypes = [ctypes.c_void_p, _f32p, _i32, _f32p, _f32p, _i32, _f32p, _f32p]
         lib.amun_decoder_step.argtypes = [ctypes.c_void_p, _f32p, _i32p, _i32, _f32p, _f32p, _i32, _i32p, _i32,
@@ -275,7 +281,7 @@ class DecodeOut:
 def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], beam_size: int,
            max_len_factor: int, max_len_offset: int, length_normalize: bool, n_best: int,
            shortlists: Sequence[np.ndarray] | None = None, want_states: bool = False, max_batch: int = 64,
-           force_full_logits: bool = False, profile: bool = False) -> DecodeOut:
+           force_full_logits: bool = False, profile: bool = False, on_bucket=None) -> DecodeOut:
     lib = load()
     lens = np.asarray([len(s) for s in sentences], dtype=np.int32)
     ids = (np.concatenate([np.asarray(s, dtype=np.int32) for s in sentences]) if len(sentences)
@@ -290,9 +296,33 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
                       max_batch, int(force_full_logits), int(profile))
     res = ctypes.POINTER(Result)()
     t_call = time.perf_counter()
-    check(lib.amun_decode(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(sentences),
-                          None if sl_ids is None else _ptr(sl_ids, _i32p),
-                          None if sl_len is None else _ptr(sl_len, _i32p), ctypes.byref(opts), ctypes.byref(res)))
+    sl_p = None if sl_ids is None else _ptr(sl_ids, _i32p)
+    sl_l = None if sl_len is None else _ptr(sl_len, _i32p)
+    if on_bucket is None:
+        check(lib.amun_decode(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(sentences), sl_p, sl_l,
+                              ctypes.byref(opts), ctypes.byref(res)))
+    else:
+        # finished buckets are handed to on_bucket(sentence indices, DecodeOut)
+        # while later buckets still decode; an exception inside is re-raised
+        # after the call (ctypes cannot propagate it through C)
+        errors: list[BaseException] = []
+
+        def _cb(_user, part, idx):
+            if errors:
+                return
+            try:
+                out = DecodeOut(part.contents, want_states)
+                sel = np.ctypeslib.as_array(idx, shape=(out.n_sent,)).copy()
+                on_bucket(sel, out)
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                errors.append(e)
+
+        cb = BUCKET_DONE(_cb)
+        check(lib.amun_decode_stream(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(sentences), sl_p,
+                                     sl_l, ctypes.byref(opts), cb, None, ctypes.byref(res)))
+        if errors:
+            lib.amun_result_free(res)
+            raise errors[0]
     t_ret = time.perf_counter()
     try:
         out = DecodeOut(res.contents, want_states)

@@ -272,6 +272,25 @@ extern "C" int amun_decode(amun_model *const *models, int32_t n_models, const in
   AMUN_API_END
 }
 
+extern "C" int amun_decode_stream(amun_model *const *models, int32_t n_models, const int32_t *src_ids,
+                                  const int32_t *src_len, int32_t n_sent, const int32_t *sl_ids,
+                                  const int32_t *sl_len, const amun_decode_opts *opts,
+                                  amun_bucket_done_fn on_bucket, void *user, amun_result **out) {
+  AMUN_API_BEGIN
+  if (!models || n_models < 1) invalid("at least one model is required");
+  if (!opts || !out || (n_sent > 0 && (!src_ids || !src_len))) invalid("null argument");
+  *out = nullptr;
+  std::vector<amun_model *> ms(models, models + n_models);
+  for (auto *m : ms) {
+    if (!m) invalid("null model handle");
+    if (m->device != ms[0]->device) invalid("ensemble members must live on the same device");
+    if (m->d.v_src != ms[0]->d.v_src || m->d.v_trg != ms[0]->d.v_trg)
+      invalid("model vocabulary mismatch");
+  }
+  *out = decode_run(ms, src_ids, src_len, n_sent, sl_ids, sl_len, *opts, on_bucket, user);
+  AMUN_API_END
+}
+
 extern "C" int amun_result_free(amun_result *r) {
   if (!r) return AMUN_OK;
   free(r->hyp_offsets);

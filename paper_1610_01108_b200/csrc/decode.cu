@@ -563,6 +563,45 @@ struct HostHyp {
   std::vector<float> state;  // n_models * dh (optional)
 };
 
+// Flat amun_result over the sentences `sel` (in that order) of out_hyps.
+amun_result *flatten_hyps(const std::vector<std::vector<HostHyp>> &out_hyps, const int *sel, int n, int n_models,
+                          int dh, bool want_states) {
+  amun_result *r = static_cast<amun_result *>(calloc(1, sizeof(amun_result)));
+  r->n_sent = n;
+  r->n_models = n_models;
+  r->d_h = dh;
+  int64_t nh = 0, nt = 0;
+  for (int i = 0; i < n; ++i)
+    for (auto &h : out_hyps[sel[i]]) {
+      ++nh;
+      nt += (int64_t)h.toks.size();
+    }
+  r->n_hyp = nh;
+  r->hyp_offsets = static_cast<int32_t *>(malloc(sizeof(int32_t) * (n + 1)));
+  r->scores = static_cast<double *>(malloc(sizeof(double) * std::max<int64_t>(nh, 1)));
+  r->finished = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nh, 1)));
+  r->tok_offsets = static_cast<int64_t *>(malloc(sizeof(int64_t) * (nh + 1)));
+  r->tokens = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nt, 1)));
+  r->states = want_states ? static_cast<float *>(malloc(sizeof(float) * std::max<int64_t>(nh * n_models * dh, 1)))
+                          : nullptr;
+  int64_t hi = 0, ti = 0;
+  r->tok_offsets[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    r->hyp_offsets[i] = (int32_t)hi;
+    for (auto &h : out_hyps[sel[i]]) {
+      r->scores[hi] = h.score;
+      r->finished[hi] = h.finished;
+      std::copy(h.toks.begin(), h.toks.end(), r->tokens + ti);
+      ti += (int64_t)h.toks.size();
+      r->tok_offsets[hi + 1] = ti;
+      if (r->states) std::copy(h.state.begin(), h.state.end(), r->states + hi * n_models * dh);
+      ++hi;
+    }
+  }
+  r->hyp_offsets[n] = (int32_t)hi;
+  return r;
+}
+
 template <class T>
 void h2d(Ctx &c, T *dst, const T *src, size_t n) {
   if (n) AMUN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, c.st));
@@ -579,7 +618,8 @@ void d2h(Ctx &c, T *dst, const T *src, size_t n) {
 // ====================================================================== decode
 
 amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_ids, const int32_t *src_len,
-                        int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o) {
+                        int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o,
+                        amun_bucket_done_fn on_bucket, void *user) {
   const auto t_enter = std::chrono::steady_clock::now();
   amun_model *m0 = ms[0];
   AMUN_CUDA(cudaSetDevice(m0->device));
@@ -1125,6 +1165,12 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       if ((int)hyps.size() > o.n_best) hyps.resize(o.n_best);
       out_hyps[s] = std::move(hyps);
     }
+    if (on_bucket) {  // stream this bucket's final hypotheses to the caller
+      const int *sel = order.data() + bk.first;
+      amun_result *part = flatten_hyps(out_hyps, sel, B, n_models, dh, o.want_states);
+      on_bucket(user, part, sel);
+      amun_result_free(part);
+    }
   };
 
   for (auto &Lp : lanes)
@@ -1201,39 +1247,9 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   }
 
   // ---- assemble the flat result
-  amun_result *r = static_cast<amun_result *>(calloc(1, sizeof(amun_result)));
-  r->n_sent = n_sent;
-  r->n_models = n_models;
-  r->d_h = dh;
-  int64_t nh = 0, nt = 0;
-  for (auto &v : out_hyps)
-    for (auto &h : v) {
-      ++nh;
-      nt += (int64_t)h.toks.size();
-    }
-  r->n_hyp = nh;
-  r->hyp_offsets = static_cast<int32_t *>(malloc(sizeof(int32_t) * (n_sent + 1)));
-  r->scores = static_cast<double *>(malloc(sizeof(double) * std::max<int64_t>(nh, 1)));
-  r->finished = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nh, 1)));
-  r->tok_offsets = static_cast<int64_t *>(malloc(sizeof(int64_t) * (nh + 1)));
-  r->tokens = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nt, 1)));
-  r->states = o.want_states ? static_cast<float *>(malloc(sizeof(float) * std::max<int64_t>(nh * n_models * dh, 1)))
-                            : nullptr;
-  int64_t hi = 0, ti = 0;
-  r->tok_offsets[0] = 0;
-  for (int s = 0; s < n_sent; ++s) {
-    r->hyp_offsets[s] = (int32_t)hi;
-    for (auto &h : out_hyps[s]) {
-      r->scores[hi] = h.score;
-      r->finished[hi] = h.finished;
-      std::copy(h.toks.begin(), h.toks.end(), r->tokens + ti);
-      ti += (int64_t)h.toks.size();
-      r->tok_offsets[hi + 1] = ti;
-      if (r->states) std::copy(h.state.begin(), h.state.end(), r->states + hi * n_models * dh);
-      ++hi;
-    }
-  }
-  r->hyp_offsets[n_sent] = (int32_t)hi;
+  std::vector<int> all(n_sent);
+  std::iota(all.begin(), all.end(), 0);
+  amun_result *r = flatten_hyps(out_hyps, all.data(), n_sent, n_models, dh, o.want_states);
   r->decoder_steps = total_steps;
   r->kernel_launches = c.launches;
   r->device_ms = ms_elapsed;

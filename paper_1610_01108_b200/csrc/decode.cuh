@@ -48,7 +48,8 @@ struct amun_model {
 namespace amun {
 
 amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_ids, const int32_t *src_len,
-                        int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o);
+                        int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o,
+                        amun_bucket_done_fn on_bucket = nullptr, void *user = nullptr);
 
 void hook_encode(amun_model *m, const int32_t *ids, int J, float *h_out, float *p_out, float *s0_out);
 

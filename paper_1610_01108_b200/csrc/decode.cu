@@ -419,6 +419,8 @@ struct LogitOut {
   float *pmax, *psum, *cval;
   int *ctok;
   const LogitTcMaps *tc = nullptr;  // tensor-core path when set
+  const uint32_t *vmask = nullptr;  // per-sentence shortlist masks (tensor-core path)
+  int mask_words = 0;
 };
 
 // Tensor-core (3xTF32, swap-AB cluster split-K, gemm_sk.cuh) versions of the
@@ -538,6 +540,9 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
   c.cls = AMUN_K_LOGIT;
   if (lo.tc) {
     LogitTcArgs ta{R, V, de, m->b_logit, lo.kk, lo.ntiles, m->us_l, lo.pmax, lo.psum, lo.cval, lo.ctok};
+    ta.vmask = lo.vmask;
+    ta.mask_words = lo.mask_words;
+    ta.rows_per_sent = rows_per_sent;
     c.run(AMUN_K_LOGIT, [&] { launch_logits_tc(*lo.tc, ta, c.st); });
     return;
   }
@@ -650,9 +655,14 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
                                           std::to_string(V));
 
   const int Bmax_opt = o.max_batch > 0 ? o.max_batch : 64;
-  const bool fused = n_models == 1 && !sl_ids && k <= kMaxRowCand && !o.force_full_logits;
   const char *no_tc = getenv("AMUN_NO_TC");
-  const bool use_tc = fused && m0->Wl_hi && !(no_tc && no_tc[0] == '1');
+  const bool tc_logits = m0->Wl_hi && !(no_tc && no_tc[0] == '1');
+  // shortlists ride the fused tensor-core logit kernel as per-sentence
+  // vocabulary masks; the CUDA-core fused kernel has no mask (full logits)
+  const bool fused = n_models == 1 && (!sl_ids || tc_logits) && k <= kMaxRowCand && !o.force_full_logits;
+  const bool use_tc = fused && tc_logits;
+  const bool use_mask = fused && sl_ids != nullptr;
+  const int mask_words = ceil_div(V, 32);
   const char *no_tcg = getenv("AMUN_NO_TC_GEMM");
   bool use_tcg = !(no_tc && no_tc[0] == '1') && !(no_tcg && no_tcg[0] == '1');
   for (auto *m : ms) use_tcg = use_tcg && m->tc_gemm;
@@ -714,6 +724,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     std::vector<TcStep> tsteps;
     std::vector<TcEnc> tencs;
     int *d_ids, *d_len, *d_cap, *d_sl, *d_sl_off, *d_sl_len;
+    uint32_t *d_vmask = nullptr;  // [Bmax][mask_words] shortlist masks (fused path)
     float *pmax, *psum, *cval;
     int *ctok, *cand_tok;
     double *cand_lp;
@@ -810,6 +821,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.d_len = cv.take<int>(Bmax);
       L.d_cap = cv.take<int>(Bmax);
       L.d_sl = cv.take<int>(std::max(sl_max, 1));
+      L.d_vmask = cv.take<uint32_t>(use_mask ? (size_t)Bmax * mask_words : 1);
       L.d_sl_off = cv.take<int>(Bmax);
       L.d_sl_len = cv.take<int>(Bmax);
       L.pmax = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
@@ -959,6 +971,15 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     h2d(c, L.d_ids, ids.data(), ids.size());
     h2d(c, L.d_len, lens.data(), B);
     h2d(c, L.d_cap, caps.data(), B);
+    if (use_mask) {
+      std::vector<uint32_t> mask((size_t)B * mask_words, 0u);
+      for (int i = 0; i < B; ++i)
+        for (int e = slo[i]; e < slo[i] + sll[i]; ++e) {
+          const int v = slv[e];
+          mask[(size_t)i * mask_words + v / 32] |= 1u << (v % 32);
+        }
+      h2d(c, L.d_vmask, mask.data(), mask.size());
+    }
     if (sl_ids) {
       h2d(c, L.d_sl, slv.data(), slv.size());
       h2d(c, L.d_sl_off, slo.data(), B);
@@ -979,6 +1000,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     c.run(AMUN_K_SELECT, [&] { launch_init_beam(L.bs, L.mr, L.p_S0, L.st); });
     L.lo = LogitOut{fused, kk, ntiles, L.pmax, L.psum, L.cval, L.ctok};
+    if (use_mask) {
+      L.lo.vmask = L.d_vmask;
+      L.lo.mask_words = mask_words;
+    }
     if (use_tc) L.lo.tc = &L.tc_maps;
     SelectArgs &sa = L.sa;
     sa = SelectArgs{};

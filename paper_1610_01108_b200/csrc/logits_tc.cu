@@ -303,6 +303,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           float *dst = buf + lg * kTrQ + lane;
 #pragma unroll
           for (int i = 0; i < 32; ++i) dst[i * kTrRow] = fmaf(v[i], a.unscale, bias_f);
+          if (a.vmask) {  // shortlist: tokens outside the sentence's list never exist
+            const int vv = v0 + f;
+            const int m0 = un.row0 + c0;
+            int sent = m0 / a.rows_per_sent, rem = m0 - sent * a.rows_per_sent;
+            const uint32_t *mw = a.vmask + (vv >> 5);
+            const int nrow = min(32, a.M - m0);
+            uint32_t w = (vv < a.N && nrow > 0) ? __ldg(mw + (long long)sent * a.mask_words) : ~0u;
+            const uint32_t bit = 1u << (vv & 31);
+#pragma unroll 1
+            for (int i = 0; i < nrow; ++i) {  // one mask word per sentence (beam rows share it)
+              if (rem == a.rows_per_sent) {
+                ++sent;
+                rem = 0;
+                w = vv < a.N ? __ldg(mw + (long long)sent * a.mask_words) : ~0u;
+              }
+              if (!(w & bit)) dst[i * kTrRow] = -INFINITY;
+              ++rem;
+            }
+          }
         }
         stamp(1);
         asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");

@@ -15,6 +15,10 @@ struct LogitTcArgs {
   float *pmax, *psum;  // [M][ntiles]
   float *cval;         // [M][ntiles][kk]
   int *ctok;
+  // optional per-sentence vocabulary masks (shortlists, nnet.py:160-163):
+  // bit v of vmask[(row / rows_per_sent) * mask_words + v / 32] allows token v
+  const uint32_t *vmask = nullptr;
+  int mask_words = 0, rows_per_sent = 1;
   int debug_flags = 0;  // microbenchmark knobs: 1 skip A loads, 2 skip B loads, 4 skip MMA, 8 skip epilogue
   long long *debug_clock = nullptr;  // microbenchmark: per-chunk clock64 stamps of CTA 0
 };

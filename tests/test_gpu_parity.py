@@ -305,3 +305,23 @@ def test_engine_translate_corpus_matches_beam_search(gpu):
         assert [t for _, t in r.n_best] == texts
         assert [s for s, _ in r.n_best] == [h.score for h in want]
         assert r.oov == sum(1 for t in line.split() if t not in src_vocab)
+
+
+def test_full_size_shortlist_fused_matches_full_logit_path(gpu, full, monkeypatch):
+    """Per-sentence shortlists (nnet.py:160-163) on the fused tensor-core
+    logit kernel (vocabulary masks) vs the full-logit CUDA-core path: same
+    tokens, scores within FP32 rounding."""
+    s = golden_full()["sets"]["cfg1"]
+    src = s["src"][:12]
+    rng = np.random.default_rng(17)
+    sls = [np.unique(np.concatenate([[0], rng.choice(np.arange(2, 30000), 1249, replace=False)])).astype(np.int32)
+           for _ in src]
+    dm = _lib.device_model(full)
+    a = _lib.decode([dm], src, 5, 2, 10, False, 2, shortlists=sls)
+    monkeypatch.setenv("AMUN_NO_TC", "1")
+    b = _lib.decode([dm], src, 5, 2, 10, False, 2, shortlists=sls)
+    for i in range(len(src)):
+        ha, hb = a.hyps(i)[0], b.hyps(i)[0]
+        assert ha[0] == hb[0], i
+        assert set(ha[0]) <= set(sls[i].tolist())
+        assert abs(ha[1] - hb[1]) <= 1e-5 * abs(hb[1]), (i, ha[1], hb[1])

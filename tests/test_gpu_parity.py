@@ -325,3 +325,33 @@ def test_full_size_shortlist_fused_matches_full_logit_path(gpu, full, monkeypatc
         assert ha[0] == hb[0], i
         assert set(ha[0]) <= set(sls[i].tolist())
         assert abs(ha[1] - hb[1]) <= 1e-5 * abs(hb[1]), (i, ha[1], hb[1])
+
+
+def test_beam12_long_sentences_tensor_core_vs_cuda_core(gpu, full, monkeypatch):
+    """cfg4 shape (beam 12, J = 100 golden sentences): the tensor-core path
+    (R = 72 rows, two MMA sub-blocks, fused attention with 12 rows) against
+    the FP32 CUDA-core kernels."""
+    s = golden_full()["sets"]["cfg4_6"]
+    sub = dict(s, src=s["src"][:3])
+    a = _decode_set(full, sub)
+    monkeypatch.setenv("AMUN_NO_TC", "1")
+    b = _decode_set(full, sub)
+    for i in range(3):
+        ha, hb = a.hyps(i)[0], b.hyps(i)[0]
+        assert ha[0] == hb[0], i
+        assert abs(ha[1] - hb[1]) <= 1e-5 * abs(hb[1]), (i, ha[1], hb[1])
+
+
+def test_shortlist_batch_composition_invariance(gpu, full):
+    """Masked fused logits: a sentence's result does not depend on its
+    bucket-mates or the bucket size."""
+    s = golden_full()["sets"]["cfg1"]
+    src = s["src"][:10]
+    rng = np.random.default_rng(23)
+    sls = [np.unique(np.concatenate([[0], rng.choice(np.arange(2, 30000), 999, replace=False)])).astype(np.int32)
+           for _ in src]
+    dm = _lib.device_model(full)
+    a = _lib.decode([dm], src, 5, 2, 10, False, 1, shortlists=sls, max_batch=64)
+    b = _lib.decode([dm], src, 5, 2, 10, False, 1, shortlists=sls, max_batch=3)
+    for i in range(len(src)):
+        assert a.hyps(i)[0][:2] == b.hyps(i)[0][:2], i

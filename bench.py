@@ -106,6 +106,19 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- CPU baseline
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+CPU_SAMPLE = 200  # fixed stratified 200-sentence subset
+
+
 def cpu_sample(sentences, n: int):
     """Fixed stratified sample: every len/n-th sentence in length order."""
     order = sorted(range(len(sentences)), key=lambda i: (len(sentences[i]), i))
@@ -153,6 +166,24 @@ def main() -> None:
                     help="profiling only: the N sentences around the median length (one realistic length bucket)")
     args = ap.parse_args()
     rank, world, local = env_rank()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # `python bench.py --gpus N`: launch N ranks (one per GPU) ourselves
+        # so n_gpus always equals the number of GPUs that decoded
+        import socket
+        import subprocess
+
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"--gpus {args.gpus} requested but only {have} CUDA device(s) are visible")
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
 
     from paper_1610_01108_b200 import workload as W
 
@@ -170,20 +201,37 @@ def main() -> None:
            "bucket": wl.batch, "cap": f"{wl.max_len_factor}*J+{wl.max_len_offset}",
            "src_tokens": sum(map(len, sentences)),
            "network": "emb500/hid1024/30k attentional GRU enc-dec, random init seed 1",
-           "parallelism": f"sentence-sharded x{args.gpus} (length-bucket LPT, no collective)",
+           "parallelism": f"sentence-sharded x{world} (length-bucket LPT, no collective)",
            "l2": "flushed (256 MiB device write) before every timed step"}
 
     if args.impl == "reference":
         if rank != 0:
             return
         threads = os.cpu_count() or 1
-        n = args.cpu_sentences or max(8, min(2 * threads, 48))
-        _, sample, once = run_cpu_reference(wl, sentences, threads, n)
+        # the 200-sentence stratified subset, decoded in
+        # disjoint slices: timed step i takes slice i mod n_slices, so the
+        # whole K-step run stays within a few minutes; warm-up steps decode
+        # a short slice (BLAS / thread-pool warm-up only)
+        n = args.cpu_sentences or CPU_SAMPLE
+        n_slices = 4
+        net, sample, _ = run_cpu_reference(wl, sentences, threads, n)
+        slices = [sample[i::n_slices] for i in range(n_slices)]
+        from oracle import beamnmt_oracle as orc
+
+        opts = orc.Opts(wl.beam, wl.max_len_factor, wl.max_len_offset)
+
+        def run_slice(sl):
+            t0 = time.perf_counter()
+            res = orc.decode_corpus([net], sl, opts, threads=threads)
+            return sum(len(h[0].tokens) - (1 if h[0].finished else 0) for h in res), time.perf_counter() - t0
+
         for _ in range(args.warmup):
-            once()
+            run_slice(slices[0][:threads])
         toks = wall = 0.0
-        for _ in range(args.steps):
-            t, w = once()
+        used = []
+        for i in range(args.steps):
+            t, w = run_slice(slices[i % n_slices])
+            used.append(len(slices[i % n_slices]))
             toks += t
             wall += w
         v = toks / wall
@@ -192,9 +240,10 @@ def main() -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (random-init weights, synthetic source ids)", "config": cfg,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{len(sample)} stratified {wl.name} sentences per step, "
-                                       f"{sum(map(len, sample))} source tokens"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "cpu": cpu_model(),
+                             "sample": f"step i decodes slice i mod {n_slices} of a fixed stratified "
+                                       f"{len(sample)}-sentence {wl.name} subset ({used} sentences per "
+                                       f"timed step, {int(toks)} target tokens in {wall:.1f} s)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
         return
 
@@ -371,10 +420,10 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        n = args.cpu_sentences or max(8, min(2 * threads, 48))
+        n = args.cpu_sentences or CPU_SAMPLE
         _, sample, once = run_cpu_reference(wl, sentences, threads, n)
         t, w = once()
-        cpu = {"value": t / w, "unit": UNIT, "cores": threads, "kind": "port",
+        cpu = {"value": t / w, "unit": UNIT, "cores": threads, "kind": "port", "cpu": cpu_model(),
                "sample": f"{len(sample)} stratified {wl.name} sentences ({sum(map(len, sample))} source, "
                          f"{t} target tokens) in {w:.1f} s"}
 

@@ -238,7 +238,11 @@ def device_model(params, device: int = 0) -> DeviceModel:
 class DecodeOut:
     """Flat copy of an amun_result: per sentence, ranked hypotheses."""
 
-    def __init__(self, res: Result, want_states: bool):
+    def __init__(self, res: Result, want_states: bool, state_widths: Sequence[int] = ()):
+        # states: per hypothesis the ensemble members' final state rows
+        # concatenated (member m has width state_widths[m] = its d_h)
+        widths = list(state_widths) or [res.d_h] * res.n_models
+        self.state_splits = np.cumsum(widths)[:-1]
         nh = res.n_hyp
         self.n_sent = res.n_sent
         self.hyp_offsets = np.ctypeslib.as_array(res.hyp_offsets, shape=(res.n_sent + 1,)).copy()
@@ -248,7 +252,7 @@ class DecodeOut:
             self.tok_offsets = np.ctypeslib.as_array(res.tok_offsets, shape=(nh + 1,)).copy()
             nt = int(self.tok_offsets[-1])
             self.tokens = np.ctypeslib.as_array(res.tokens, shape=(max(nt, 1),))[:nt].copy()
-            self.states = (np.ctypeslib.as_array(res.states, shape=(nh, res.n_models, res.d_h)).copy()
+            self.states = (np.ctypeslib.as_array(res.states, shape=(nh, int(sum(widths)))).copy()
                            if want_states else None)
         else:
             self.scores = np.zeros(0)
@@ -274,7 +278,7 @@ class DecodeOut:
         for h in range(self.hyp_offsets[i], self.hyp_offsets[i + 1]):
             a, b = self.tok_offsets[h], self.tok_offsets[h + 1]
             out.append((tok[a:b].tolist(), float(self.scores[h]), bool(self.finished[h]),
-                        None if self.states is None else self.states[h]))
+                        None if self.states is None else np.split(self.states[h], self.state_splits)))
         return out
 
 
@@ -292,6 +296,7 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
         sl_len = np.asarray([len(s) for s in shortlists], dtype=np.int32)
         sl_ids = np.ascontiguousarray(np.concatenate([np.asarray(s, np.int32) for s in shortlists]), np.int32)
     handles = (ctypes.c_void_p * len(models))(*[m.handle for m in models])
+    widths = [m.config.d_h for m in models]
     opts = DecodeOpts(beam_size, max_len_factor, max_len_offset, int(length_normalize), n_best, int(want_states),
                       max_batch, int(force_full_logits), int(profile))
     res = ctypes.POINTER(Result)()
@@ -311,7 +316,7 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
             if errors:
                 return
             try:
-                out = DecodeOut(part.contents, want_states)
+                out = DecodeOut(part.contents, want_states, widths)
                 sel = np.ctypeslib.as_array(idx, shape=(out.n_sent,)).copy()
                 on_bucket(sel, out)
             except BaseException as e:  # noqa: BLE001 - re-raised below
@@ -325,7 +330,7 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
             raise errors[0]
     t_ret = time.perf_counter()
     try:
-        out = DecodeOut(res.contents, want_states)
+        out = DecodeOut(res.contents, want_states, widths)
     finally:
         lib.amun_result_free(res)
     out.call_ms = 1e3 * (t_ret - t_call)  # the C call, wall (vs device_ms inside it)

@@ -1,6 +1,7 @@
 // C-ABI of the B200 decoder (include/amun_b200.h): device model handle,
 // length-bucketed batched beam-search decode, and the per-step parity hooks.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -16,6 +17,9 @@
 using namespace amun;
 
 static thread_local std::string g_last_error;
+// live model handles per device: the pooled decode lanes of a device are
+// released when its last handle is destroyed
+static std::atomic<int> g_live_models[64];
 
 #define AMUN_API_BEGIN try {
 #define AMUN_API_END                                  \
@@ -219,6 +223,8 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
   if (m->tc_ok)  // logit rows [V, dep] (K-major, padded to a 16-byte pitch)
     m->us_l = upload_kmajor_split(m, t[T_W_LOGIT], de, V, m->dep, ident, &m->Wl_hi, &m->Wl_lo);
   AMUN_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  m->live = true;
+  g_live_models[m->device & 63].fetch_add(1);
   *out = m;
   m = nullptr;
   }
@@ -241,6 +247,12 @@ extern "C" int amun_model_destroy(amun_model *m) {
   if (m->stream) cudaStreamSynchronize(m->stream);
   for (void *p : m->allocs) cudaFree(p);
   if (m->stream) cudaStreamDestroy(m->stream);
+  if (m->live && g_live_models[m->device & 63].fetch_sub(1) == 1) {
+    try {
+      release_device_lanes(m->device);
+    } catch (...) {
+    }
+  }
   delete m;
   return AMUN_OK;
 }

@@ -70,6 +70,25 @@ struct LaneRes {
 constexpr int kProbeSlots = 64;
 std::mutex g_lane_mu;
 std::vector<LaneRes *> g_lane_pool[64][2];  // [device][high priority]
+cudaMemPool_t g_ws_pool[64] = {};             // private workspace pool per device
+
+// Private stream-ordered pool for the lane workspaces: freed memory stays
+// mapped across calls (stream syncs must not trim it) without changing the
+// release threshold of the device's default pool, which other users share.
+cudaMemPool_t ws_pool(int dev) {
+  std::lock_guard<std::mutex> g(g_lane_mu);
+  cudaMemPool_t &p = g_ws_pool[dev & 63];
+  if (!p) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    AMUN_CUDA(cudaMemPoolCreate(&p, &props));
+    uint64_t thr = UINT64_MAX;
+    AMUN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return p;
+}
 
 LaneRes *lane_acquire(int dev, int high) {
   {
@@ -82,13 +101,6 @@ LaneRes *lane_acquire(int dev, int high) {
     }
   }
   std::unique_ptr<LaneRes> r(new LaneRes());
-  {  // keep freed pool memory mapped: stream syncs must not trim the pool
-    cudaMemPool_t mp;
-    if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
   {
     int least = 0, greatest = 0;
     AMUN_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -115,13 +127,13 @@ int high_priority_lanes() {
   return v;
 }
 // workspace of at least n bytes on the lane's stream
-void *lane_mem(LaneRes *r, size_t n) {
+void *lane_mem(LaneRes *r, size_t n, cudaMemPool_t pool) {
   n = std::max<size_t>(n, 256);
   if (r->cap < n) {
     if (r->mem) AMUN_CUDA(cudaFreeAsync(r->mem, r->st));
     r->mem = nullptr;
     r->cap = 0;
-    AMUN_CUDA(cudaMallocAsync(&r->mem, n, r->st));
+    AMUN_CUDA(cudaMallocFromPoolAsync(&r->mem, n, pool, r->st));
     r->cap = n;
   }
   return r->mem;
@@ -145,6 +157,7 @@ struct Ctx {
   size_t ws_floats = 0;
   float **ws_keep = nullptr;  // when set, the buffer outlives the Ctx (pooled lane)
   size_t *ws_keep_n = nullptr;
+  cudaMemPool_t ws_pool = nullptr;  // allocation pool of ws (nullptr: the device default)
   explicit Ctx(cudaStream_t s) : st(s) {}
   ~Ctx() {
     for (auto e : pool) cudaEventDestroy(e);
@@ -159,7 +172,10 @@ struct Ctx {
     if (n <= ws_floats) return;
     if (ws) AMUN_CUDA(cudaFreeAsync(ws, st));
     ws = nullptr;
-    AMUN_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&ws), n * sizeof(float), st));
+    if (ws_pool)
+      AMUN_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&ws), n * sizeof(float), ws_pool, st));
+    else
+      AMUN_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&ws), n * sizeof(float), st));
     ws_floats = n;
   }
   cudaEvent_t next_event() {
@@ -569,8 +585,10 @@ struct HostHyp {
 };
 
 // Flat amun_result over the sentences `sel` (in that order) of out_hyps.
+// States: per hypothesis the members' final state rows concatenated
+// (width sw = sum of the members' d_h; d_h reports member 0's).
 amun_result *flatten_hyps(const std::vector<std::vector<HostHyp>> &out_hyps, const int *sel, int n, int n_models,
-                          int dh, bool want_states) {
+                          int dh, int sw, bool want_states) {
   amun_result *r = static_cast<amun_result *>(calloc(1, sizeof(amun_result)));
   r->n_sent = n;
   r->n_models = n_models;
@@ -587,7 +605,7 @@ amun_result *flatten_hyps(const std::vector<std::vector<HostHyp>> &out_hyps, con
   r->finished = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nh, 1)));
   r->tok_offsets = static_cast<int64_t *>(malloc(sizeof(int64_t) * (nh + 1)));
   r->tokens = static_cast<int32_t *>(malloc(sizeof(int32_t) * std::max<int64_t>(nt, 1)));
-  r->states = want_states ? static_cast<float *>(malloc(sizeof(float) * std::max<int64_t>(nh * n_models * dh, 1)))
+  r->states = want_states ? static_cast<float *>(malloc(sizeof(float) * std::max<int64_t>(nh * sw, 1)))
                           : nullptr;
   int64_t hi = 0, ti = 0;
   r->tok_offsets[0] = 0;
@@ -599,7 +617,7 @@ amun_result *flatten_hyps(const std::vector<std::vector<HostHyp>> &out_hyps, con
       std::copy(h.toks.begin(), h.toks.end(), r->tokens + ti);
       ti += (int64_t)h.toks.size();
       r->tok_offsets[hi + 1] = ti;
-      if (r->states) std::copy(h.state.begin(), h.state.end(), r->states + hi * n_models * dh);
+      if (r->states) std::copy(h.state.begin(), h.state.end(), r->states + hi * sw);
       ++hi;
     }
   }
@@ -633,6 +651,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   if (k < 1) throw Error(AMUN_ERR_INVALID, "beam_size must be >= 1, got " + std::to_string(k));
   if (o.n_best < 1) throw Error(AMUN_ERR_INVALID, "n_best must be >= 1, got " + std::to_string(o.n_best));
   const int V = m0->d.v_trg, Vs = m0->d.v_src, dh = m0->d.d_h;
+  if (n_models > kMaxModels)
+    throw Error(AMUN_ERR_UNSUPPORTED, "at most " + std::to_string(kMaxModels) + " ensemble members are supported");
+  int state_w = 0;  // concatenated final-state width of all members
+  for (auto *m : ms) state_w += m->d.d_h;
   std::vector<long long> off(n_sent + 1, 0), sl_offs(n_sent + 1, 0);
   for (int i = 0; i < n_sent; ++i) {
     if (src_len[i] < 1) throw Error(AMUN_ERR_INVALID, "cannot decode an empty source sentence");
@@ -654,6 +676,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
         throw Error(AMUN_ERR_INVALID, "shortlist id " + std::to_string(sl_ids[j]) + " out of range for v_trg=" +
                                           std::to_string(V));
 
+  if (n_sent == 0) {  // nothing to decode: no lanes, no tensor maps
+    amun_result *r = flatten_hyps({}, nullptr, 0, n_models, dh, state_w, o.want_states);
+    r->host_setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enter).count();
+    return r;
+  }
   const int Bmax_opt = o.max_batch > 0 ? o.max_batch : 64;
   const char *no_tc = getenv("AMUN_NO_TC");
   const bool tc_logits = m0->Wl_hi && !(no_tc && no_tc[0] == '1');
@@ -700,7 +727,6 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   }
   const int Rmax = Bmax * k;
   const int fin_cap = k * cap_all;
-  const int xs = m0->xs_w;
   const int de = m0->d.d_emb;
 
   // ---- lanes: each lane = stream + workspace + captured step graph and
@@ -798,6 +824,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.c->ws_floats = L.res->ws_floats;
     L.c->ws_keep = &L.res->ws;
     L.c->ws_keep_n = &L.res->ws_floats;
+    L.c->ws_pool = ws_pool(L.dev);
     L.c->prof = (uint32_t)o.profile;
     L.eb.resize(n_models);
     L.db.resize(n_models);
@@ -815,7 +842,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
         if (use_tcg) {
           carve_dec_tc(cv, L.db[m], ms[m], Rmax);
         }
-        L.fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * dh) : nullptr;
+        L.fin_states[m] = o.want_states ? cv.take<float>((size_t)Bmax * fin_cap * ms[m]->d.d_h) : nullptr;
       }
       L.d_ids = cv.take<int>((size_t)Bmax * jmax_all);
       L.d_len = cv.take<int>(Bmax);
@@ -853,7 +880,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.p_fin = cv.take<float *>(n_models);
       L.p_XSh = cv.take<__half *>(n_models);
       L.p_XSl = cv.take<__half *>(n_models);
-      if (!pass) L.mem = lane_mem(L.res, cv.off);
+      if (!pass) L.mem = lane_mem(L.res, cv.off, ws_pool(L.dev));
     }
     if (use_tc) {
       static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
@@ -991,12 +1018,16 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.bs.k = k;
     L.bs.cap_max = L.capm;
     L.bs.fin_cap = fin_cap;
-    L.mr = ModelRows{L.p_XS, L.p_Sn, L.p_E, o.want_states ? L.p_fin : nullptr, xs, de, dh, de + 2 * dh, n_models};
+    L.mr = ModelRows{L.p_XS, L.p_Sn, L.p_E, o.want_states ? L.p_fin : nullptr, n_models};
+    for (int m = 0; m < n_models; ++m) {
+      const amun_model *mm = ms[m];
+      const int de_m = mm->d.d_emb, dh_m = mm->d.d_h;
+      L.mr.dim[m] = RowDims{mm->xs_w, de_m, dh_m, de_m + 2 * dh_m, use_tcg ? mm->xsp : 0,
+                            use_tcg ? mm->dep - de_m : 0};
+    }
     if (use_tcg) {
       L.mr.XSh = L.p_XSh;
       L.mr.XSl = L.p_XSl;
-      L.mr.ldxh = m0->xsp;
-      L.mr.hpad = m0->dep - de;
     }
     c.run(AMUN_K_SELECT, [&] { launch_init_beam(L.bs, L.mr, L.p_S0, L.st); });
     L.lo = LogitOut{fused, kk, ntiles, L.pmax, L.psum, L.cval, L.ctok};
@@ -1128,15 +1159,17 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     d2h(c, bp_tok.data(), bs.bp_tok, (size_t)B * capm * k);
     d2h(c, bp_par.data(), bs.bp_par, (size_t)B * capm * k);
-    std::vector<float> act_states, fin_st;
+    // per member m: active rows [R][dh_m] and finished rows [B][fin_cap][dh_m]
+    std::vector<std::vector<float>> act_states(n_models), fin_st(n_models);
     if (o.want_states) {
-      act_states.resize((size_t)n_models * R * dh);
-      fin_st.resize((size_t)n_models * B * fin_cap * dh);
       for (int m = 0; m < n_models; ++m) {
-        AMUN_CUDA(cudaMemcpy2DAsync(act_states.data() + (size_t)m * R * dh, dh * sizeof(float),
-                                    L.db[m].XS + de + 2 * dh, xs * sizeof(float), dh * sizeof(float), R,
-                                    cudaMemcpyDeviceToHost, L.st));
-        d2h(c, fin_st.data() + (size_t)m * B * fin_cap * dh, L.fin_states[m], (size_t)B * fin_cap * dh);
+        const int de_m = ms[m]->d.d_emb, dh_m = ms[m]->d.d_h;
+        act_states[m].resize((size_t)R * dh_m);
+        fin_st[m].resize((size_t)B * fin_cap * dh_m);
+        AMUN_CUDA(cudaMemcpy2DAsync(act_states[m].data(), dh_m * sizeof(float), L.db[m].XS + de_m + 2 * dh_m,
+                                    ms[m]->xs_w * sizeof(float), dh_m * sizeof(float), R, cudaMemcpyDeviceToHost,
+                                    L.st));
+        d2h(c, fin_st[m].data(), L.fin_states[m], (size_t)B * fin_cap * dh_m);
       }
     }
     AMUN_CUDA(cudaStreamSynchronize(L.st));
@@ -1163,8 +1196,9 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
           h.toks.push_back(0);
           if (o.want_states)
             for (int m = 0; m < n_models; ++m) {
-              const float *p = fin_st.data() + ((size_t)m * B * fin_cap + fo) * dh;
-              h.state.insert(h.state.end(), p, p + dh);
+              const int dh_m = ms[m]->d.d_h;
+              const float *p = fin_st[m].data() + fo * dh_m;
+              h.state.insert(h.state.end(), p, p + dh_m);
             }
           hyps.push_back(std::move(h));
         }
@@ -1173,8 +1207,9 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
           HostHyp h{score[(size_t)i * k + a], 0, walk(i, steps[i] - 1, a), {}};
           if (o.want_states)
             for (int m = 0; m < n_models; ++m) {
-              const float *p = act_states.data() + ((size_t)m * R + (size_t)i * k + a) * dh;
-              h.state.insert(h.state.end(), p, p + dh);
+              const int dh_m = ms[m]->d.d_h;
+              const float *p = act_states[m].data() + ((size_t)i * k + a) * dh_m;
+              h.state.insert(h.state.end(), p, p + dh_m);
             }
           hyps.push_back(std::move(h));
         }
@@ -1192,7 +1227,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     if (on_bucket) {  // stream this bucket's final hypotheses to the caller
       const int *sel = order.data() + bk.first;
-      amun_result *part = flatten_hyps(out_hyps, sel, B, n_models, dh, o.want_states);
+      amun_result *part = flatten_hyps(out_hyps, sel, B, n_models, dh, state_w, o.want_states);
       on_bucket(user, part, sel);
       amun_result_free(part);
     }
@@ -1274,7 +1309,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // ---- assemble the flat result
   std::vector<int> all(n_sent);
   std::iota(all.begin(), all.end(), 0);
-  amun_result *r = flatten_hyps(out_hyps, all.data(), n_sent, n_models, dh, o.want_states);
+  amun_result *r = flatten_hyps(out_hyps, all.data(), n_sent, n_models, dh, state_w, o.want_states);
   r->decoder_steps = total_steps;
   r->kernel_launches = c.launches;
   r->device_ms = ms_elapsed;
@@ -1290,6 +1325,35 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   lanes.clear();  // lane teardown (back to the pool) counts as host post-processing
   r->host_post_ms = ms_d(std::chrono::steady_clock::now() - t_ev1).count();
   return r;
+}
+
+// Frees the pooled lanes of a device (streams, workspaces, step graphs,
+// pinned probe rings) and trims its workspace pool: called when the last
+// model handle on the device is destroyed, so a long-running process does
+// not keep its peak decode memory after the models are gone.
+void release_device_lanes(int dev) {
+  std::vector<LaneRes *> rs;
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_lane_mu);
+    for (auto &v : g_lane_pool[dev & 63]) {
+      rs.insert(rs.end(), v.begin(), v.end());
+      v.clear();
+    }
+    pool = g_ws_pool[dev & 63];
+  }
+  for (LaneRes *r : rs) {
+    cudaStreamSynchronize(r->st);
+    if (r->mem) cudaFreeAsync(r->mem, r->st);
+    if (r->ws) cudaFreeAsync(r->ws, r->st);
+    cudaStreamSynchronize(r->st);
+    if (r->gexec) cudaGraphExecDestroy(r->gexec);
+    for (auto e : r->ev) cudaEventDestroy(e);
+    if (r->h_probe) cudaFreeHost(r->h_probe);
+    cudaStreamDestroy(r->st);
+    delete r;
+  }
+  if (pool) cudaMemPoolTrimTo(pool, 0);
 }
 
 // ====================================================================== hooks

@@ -41,6 +41,7 @@ struct amun_model {
   __half *Wenc_hi = nullptr, *Wenc_lo = nullptr;    // [6dh, dep] input projection, both directions
   float us_ea = 1.f, us_eb = 1.f, us_p = 1.f, us_x = 1.f;
   int64_t bytes = 0;
+  bool live = false;  // counted in the device's live-handle count (api.cu)
   std::vector<void *> allocs;
   cudaStream_t stream = nullptr;
 };
@@ -50,6 +51,9 @@ namespace amun {
 amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_ids, const int32_t *src_len,
                         int n_sent, const int32_t *sl_ids, const int32_t *sl_len, const amun_decode_opts &o,
                         amun_bucket_done_fn on_bucket = nullptr, void *user = nullptr);
+
+// free the pooled decode lanes of a device (last model handle destroyed)
+void release_device_lanes(int dev);
 
 void hook_encode(amun_model *m, const int32_t *ids, int J, float *h_out, float *p_out, float *s0_out);
 

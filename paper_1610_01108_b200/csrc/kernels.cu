@@ -492,8 +492,17 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
     return !(e && e[0] == '0');
   }();
   const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)k;
-  if (fused && a.EQ && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && k <= 16 && smem_s <= 200 * 1024 &&
-      (size_t)a.ldctx % 4 == 0 && reinterpret_cast<uintptr_t>(a.ctx) % 16 == 0) {
+  // The kernel is chosen from per-call constants only (beam width, model
+  // layout), never from the bucket's longest sentence: the fused and the
+  // two-phase kernels sum in different orders, and a sentence's result must
+  // not depend on its batch-mates.  A bucket too long for the fused kernel's
+  // shared-memory energies is refused instead of silently switching paths.
+  const bool fused_ok = fused && a.EQ && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && k <= 16 &&
+                        (size_t)a.ldctx % 4 == 0 && reinterpret_cast<uintptr_t>(a.ctx) % 16 == 0;
+  if (fused_ok && smem_s > 200 * 1024)
+    throw Error(4, "source sentence of " + std::to_string(a.jmax) + " tokens exceeds the device attention limit (" +
+                       std::to_string((200 * 1024 / 4 - a.da - 1) / k) + " at beam " + std::to_string(k) + ")");
+  if (fused_ok) {
     const int B = R / k;
     switch (k) {  // exact beam width: no predicated-off rows in the inner loops
       case 1: launch_sent<1>(a, B, smem_s, st); break;
@@ -587,17 +596,18 @@ __global__ void init_beam_kernel(BeamState bs, ModelRows mr, const float *const 
     __half *XSh = mr.XSh ? mr.XSh[m] : nullptr;
     __half *XSl = mr.XSl ? mr.XSl[m] : nullptr;
     const float *E = mr.E_trg[m];
+    const RowDims md = mr.dim[m];
     for (int i = 0; i < k; ++i) {
-      const long long ro = (long long)(b * k + i) * mr.ldxs;
-      const long long roh = (long long)(b * k + i) * mr.ldxh;
-      for (int c = threadIdx.x; c < mr.ldxs; c += blockDim.x) {
+      const long long ro = (long long)(b * k + i) * md.ldxs;
+      const long long roh = (long long)(b * k + i) * md.ldxh;
+      for (int c = threadIdx.x; c < md.ldxs; c += blockDim.x) {
         float v = 0.f;
         if (i == 0) {
-          if (c < mr.de) v = E[c];  // E_trg[EOS_ID]
-          else if (c >= mr.s_off && c < mr.s_off + mr.dh) v = S0[m][(long long)b * mr.dh + (c - mr.s_off)];
+          if (c < md.de) v = E[c];  // E_trg[EOS_ID]
+          else if (c >= md.s_off && c < md.s_off + md.dh) v = S0[m][(long long)b * md.dh + (c - md.s_off)];
         }
         XS[ro + c] = v;
-        store_split(XSh, XSl, roh + c + (c >= mr.de ? mr.hpad : 0), v);
+        store_split(XSh, XSl, roh + c + (c >= md.de ? md.hpad : 0), v);
       }
     }
   }
@@ -609,8 +619,6 @@ void launch_init_beam(const BeamState &bs, const ModelRows &mr, const float *con
 }
 
 // ================================================================ select
-
-constexpr int kMaxModels = 8;
 
 __device__ __forceinline__ double combine_models(double l0, const double *lm, int n) {
   // search.py:67-72 mean about the first member: first + mean(stack - first)
@@ -1000,15 +1008,16 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   // ---- phase 4: gather next-step decoder rows [E_trg[y] | . | s'_parent]
   // (float4 granules, 8 independent loads in flight per thread)
   const int newna = s_newna, nfin = s_nfin;
-  const bool vec = (mr.de % 4 == 0) && (mr.dh % 4 == 0) && (mr.ldxs % 4 == 0) && (mr.s_off % 4 == 0);
   for (int m = 0; m < n_models; ++m) {
+    const RowDims md = mr.dim[m];
+    const bool vec = (md.de % 4 == 0) && (md.dh % 4 == 0) && (md.ldxs % 4 == 0) && (md.s_off % 4 == 0);
     float *XS = mr.XS[m];
     __half *XSh = mr.XSh ? mr.XSh[m] : nullptr;
     __half *XSl = mr.XSl ? mr.XSl[m] : nullptr;
     const float *Sn = mr.Sn[m];
     const float *E = mr.E_trg[m];
     if (vec) {
-      const int qe = mr.de / 4, qrow = (mr.de + mr.dh) / 4;
+      const int qe = md.de / 4, qrow = (md.de + md.dh) / 4;
       const int total = newna * qrow;
       for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
         float4 v[8];
@@ -1019,16 +1028,16 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
           dst[u] = -1;
           if (idx < total) {
             const int i = idx / qrow, c4 = idx - i * qrow;
-            const long long ro = (long long)(b * k + i) * mr.ldxs;
-            const long long roh = (long long)(b * k + i) * mr.ldxh;
+            const long long ro = (long long)(b * k + i) * md.ldxs;
+            const long long roh = (long long)(b * k + i) * md.ldxh;
             if (c4 < qe) {
-              v[u] = __ldg(reinterpret_cast<const float4 *>(E + (long long)ch_tok[i] * mr.de) + c4);
+              v[u] = __ldg(reinterpret_cast<const float4 *>(E + (long long)ch_tok[i] * md.de) + c4);
               dst[u] = ro + 4 * c4;
               dsth[u] = roh + 4 * c4;
             } else {
-              v[u] = __ldg(reinterpret_cast<const float4 *>(Sn + (long long)(b * k + ch_par[i]) * mr.dh) + (c4 - qe));
-              dst[u] = ro + mr.s_off + 4 * (c4 - qe);
-              dsth[u] = roh + mr.s_off + mr.hpad + 4 * (c4 - qe);
+              v[u] = __ldg(reinterpret_cast<const float4 *>(Sn + (long long)(b * k + ch_par[i]) * md.dh) + (c4 - qe));
+              dst[u] = ro + md.s_off + 4 * (c4 - qe);
+              dsth[u] = roh + md.s_off + md.hpad + 4 * (c4 - qe);
             }
           }
         }
@@ -1049,25 +1058,25 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       }
     } else {
       for (int i = 0; i < newna; ++i) {
-        const long long ro = (long long)(b * k + i) * mr.ldxs;
-        const long long roh = (long long)(b * k + i) * mr.ldxh;
-        const float *ey = E + (long long)ch_tok[i] * mr.de;
-        const float *sp = Sn + (long long)(b * k + ch_par[i]) * mr.dh;
-        for (int c = threadIdx.x; c < mr.de; c += blockDim.x) {
+        const long long ro = (long long)(b * k + i) * md.ldxs;
+        const long long roh = (long long)(b * k + i) * md.ldxh;
+        const float *ey = E + (long long)ch_tok[i] * md.de;
+        const float *sp = Sn + (long long)(b * k + ch_par[i]) * md.dh;
+        for (int c = threadIdx.x; c < md.de; c += blockDim.x) {
           XS[ro + c] = ey[c];
           store_split(XSh, XSl, roh + c, ey[c]);
         }
-        for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) {
-          XS[ro + mr.s_off + c] = sp[c];
-          store_split(XSh, XSl, roh + mr.s_off + mr.hpad + c, sp[c]);
+        for (int c = threadIdx.x; c < md.dh; c += blockDim.x) {
+          XS[ro + md.s_off + c] = sp[c];
+          store_split(XSh, XSl, roh + md.s_off + md.hpad + c, sp[c]);
         }
       }
     }
     if (mr.fin_states) {
       for (int i = 0; i < nfin; ++i) {
-        float *dst = mr.fin_states[m] + ((long long)b * bs.fin_cap + fin_idx[i]) * mr.dh;
-        const float *sp = Sn + (long long)(b * k + fin_par[i]) * mr.dh;
-        for (int c = threadIdx.x; c < mr.dh; c += blockDim.x) dst[c] = sp[c];
+        float *dst = mr.fin_states[m] + ((long long)b * bs.fin_cap + fin_idx[i]) * md.dh;
+        const float *sp = Sn + (long long)(b * k + fin_par[i]) * md.dh;
+        for (int c = threadIdx.x; c < md.dh; c += blockDim.x) dst[c] = sp[c];
       }
     }
   }

@@ -55,17 +55,27 @@ struct BeamState {
   int *n_done;       // [1] sentences finished so far
 };
 
+constexpr int kMaxModels = 8;  // ensemble members on the device path
+
+// Row layout of one ensemble member's decoder buffers.  Members may differ
+// in d_emb / d_h / d_att (the reference runs one Forward per model,
+// search.py:150-152), so every stride is per member.
+struct RowDims {
+  int ldxs, de, dh, s_off;  // XS = [y | c | s] row pitch and offsets
+  // 3xFP16 split copies of XS in the padded layout: row pitch ldxh, XS
+  // column c at c + (c >= de ? hpad : 0)
+  int ldxh, hpad;
+};
+
 struct ModelRows {  // per-model decoder row buffers (device arrays of pointers)
   float *const *XS;       // [R][ldxs] = [y | c | s]
   const float *const *Sn; // [R][dh]   s' of this step
   const float *const *E_trg;
   float *const *fin_states;  // optional [B][fin_cap][dh]
-  int ldxs, de, dh, s_off, n_models;
-  // optional 3xFP16 split copies of XS (per model) in the padded layout:
-  // row pitch ldxh, XS column c at c + (c >= de ? hpad : 0)
-  __half *const *XSh = nullptr;
+  int n_models;
+  __half *const *XSh = nullptr;  // optional split copies (per model)
   __half *const *XSl = nullptr;
-  int ldxh = 0, hpad = 0;
+  RowDims dim[kMaxModels];
 };
 
 // XS rows of every sentence: slot 0 <- [E_trg[EOS] | 0 | s0_b], others 0;

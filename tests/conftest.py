@@ -56,6 +56,23 @@ def golden_full() -> dict:
     return json.loads((GOLDEN / "full.json").read_text())
 
 
+@lru_cache(maxsize=None)
+def golden_fullset(name: str) -> dict:
+    """Reference 1-best of a whole headline workload (make_golden_fullset.py)."""
+    with np.load(GOLDEN / f"fullset_{name}.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def fullset_src_sha(corpus) -> str:
+    import hashlib
+
+    hs = hashlib.sha256()
+    for s in corpus:
+        hs.update(np.asarray(s, np.int32).tobytes())
+        hs.update(b"|")
+    return hs.hexdigest()
+
+
 @lru_cache(maxsize=1)
 def full_model():
     """random_model(emb500/hid1024/30k, seed 1) — the model every full-size

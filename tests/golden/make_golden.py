@@ -100,6 +100,17 @@ def tiny_fixtures():
                       "src": src, "opts": [3, 1, 3, 0, 3],
                       "copies": [hyp_json(h) for h in beam_search([ma] * 4, src, opts)],
                       "pair": [hyp_json(h) for h in beam_search([ma, mb], src, opts)]})
+    # (c2) ensembles of members with different d_emb / d_h / d_att (the
+    # reference runs one Forward per member, search.py:150-152)
+    for i in range(4):
+        ma = random_model(ModelConfig(v_src=6, v_trg=7, d_emb=5, d_h=4, d_att=3), 1700 + i)
+        mb = random_model(ModelConfig(v_src=6, v_trg=7, d_emb=3, d_h=6, d_att=5), 1800 + i)
+        src = [2, 3, 4, 5][: 1 + i % 4]
+        opts = DecodeOptions(beam_size=3, max_len_factor=1, max_len_offset=3, n_best=2)
+        cases.append({"kind": "ensemble_mixed", "seeds": [1700 + i, 1800 + i], "dims": [[6, 7, 5, 4, 3], [6, 7, 3, 6, 5]],
+                      "src": src, "opts": [3, 1, 3, 0, 2],
+                      "hyps": [hyp_json(h) for h in beam_search([ma, mb], src, opts)],
+                      "states": [[[float(x) for x in st.s] for st in h.states] for h in beam_search([ma, mb], src, opts)]})
     # (d) shortlist decodes
     for i in range(6):
         m = tiny_model(900 + i, 7, 9, 4)

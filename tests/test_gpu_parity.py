@@ -12,7 +12,8 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import full_model, golden_full, golden_tiny, golden_tiny_arrays, tiny_model
+from conftest import (full_model, fullset_src_sha, golden_full, golden_fullset, golden_tiny, golden_tiny_arrays,
+                      tiny_model)
 from paper_1610_01108_b200 import _lib
 from paper_1610_01108_b200.model import EOS_ID, ModelConfig, ModelParams, random_model, schema
 from paper_1610_01108_b200.nnet import decoder_step, encode, gru_step, init_decoder_state, attention
@@ -23,6 +24,7 @@ pytestmark = pytest.mark.gpu
 
 TAU = 1e-4          # near-tie threshold on the reference's candidate gap
 SCORE_RTOL = 1e-5   # tiny models: fp32 vs f64 beam scores
+SCORE_RTOL_FULL = 1e-5  # full size: relative error of the summed f64 beam score (|score| up to ~2000)
 
 
 def _cmp_hyps(got, gold, tol=SCORE_RTOL):
@@ -72,6 +74,23 @@ def test_tiny_ensembles(gpu):
         single = beam_search([a], c["src"], opts)
         quad = beam_search([a] * 4, c["src"], opts)
         assert [h.tokens for h in single] == [h.tokens for h in quad]  # c03
+
+
+def test_tiny_mixed_dim_ensembles(gpu):
+    """Members with different d_emb / d_h / d_att (the reference runs one
+    Forward per member, search.py:150-152): per-member row strides on the
+    device, hypothesis states returned per member with its own width."""
+    cases = [c for c in golden_tiny()["cases"] if c["kind"] == "ensemble_mixed"]
+    assert cases
+    for c in cases:
+        ms = [random_model(ModelConfig(*d), s) for d, s in zip(c["dims"], c["seeds"])]
+        beam, f, o, norm, nb = c["opts"]
+        got = beam_search(ms, c["src"], DecodeOptions(beam, f, o, bool(norm), nb))
+        _cmp_hyps(got, c["hyps"])
+        for h, gst in zip(got, c["states"]):
+            assert [st.s.shape[0] for st in h.states] == [len(x) for x in gst]
+            for st, want in zip(h.states, gst):
+                np.testing.assert_allclose(st.s, want, rtol=1e-4, atol=1e-5)
 
 
 def test_tiny_shortlists(gpu):
@@ -173,24 +192,44 @@ def _decode_set(model, s, max_batch=64, **kw):
     return _lib.decode([dm], s["src"], beam, f, o, bool(norm), 2, max_batch=max_batch, **kw)
 
 
-def _adjudicate(name, s, out):
-    exact, ties, fails = 0, [], []
-    for i, r in enumerate(s["results"]):
-        gold = r["hyps"][0]
+def _first_divergence(got, want) -> int:
+    """Index of the first differing token (the decode step that emitted it)."""
+    for d, (x, y) in enumerate(zip(got, want)):
+        if x != y:
+            return d
+    return min(len(got), len(want))
+
+
+def _adjudicate(name, gold_hyps, gaps, out, score_rtol=SCORE_RTOL_FULL):
+    """Token identity per sentence, except documented near ties: a sentence
+    whose 1-best first differs from the reference's at token d is excused
+    only if the reference's k-th vs (k+1)-th candidate gap was < TAU at some
+    step <= d (the beams must have diverged no later than step d, so the
+    window [0, d] bounds the first divergent step; a near tie later in the
+    sentence excuses nothing), or if the two best final hypotheses are
+    within TAU (final-ranking tie).  Exact sentences must match the score
+    to score_rtol."""
+    exact, ties, fails, worst = 0, [], [], 0.0
+    for i, (gtoks, gscore) in enumerate(gold_hyps):
         hyps = out.hyps(i)
         toks, score = hyps[0][0], hyps[0][1]
-        gaps = np.array(r["kth"]) - np.array(r["next"])
-        min_gap = float(gaps.min()) if gaps.size else np.inf
-        final_gap = abs(hyps[0][1] - hyps[1][1]) if len(hyps) > 1 else np.inf
-        if toks == gold["tokens"]:
+        if toks == gtoks:
             exact += 1
-            assert abs(score - gold["score"]) <= 1e-4 * abs(gold["score"]) + 1e-4, (i, score, gold["score"])
-        elif min(min_gap, final_gap) < TAU:
-            ties.append((i, min_gap, final_gap))
-        else:
-            fails.append((i, min_gap, final_gap))
-    print(f"\n{name}: {exact}/{len(s['results'])} token-identical, near-tie exceptions {ties}")
-    assert not fails, f"{name}: divergences without a near tie: {fails}"
+            rel = abs(score - gscore) / max(1.0, abs(gscore))
+            worst = max(worst, rel)
+            assert rel <= score_rtol, (name, i, score, gscore)
+            continue
+        d = _first_divergence(toks, gtoks)
+        g = np.asarray(gaps[i][: d + 1], np.float64)
+        gap_d = float(g.min()) if g.size else np.inf
+        final_gap = abs(hyps[0][1] - hyps[1][1]) if len(hyps) > 1 else np.inf
+        (ties if min(gap_d, final_gap) < TAU else fails).append((i, d, gap_d, final_gap))
+    n = len(gold_hyps)
+    summary = (f"{name}: {exact}/{n} token-identical, {len(ties)} near-tie exceptions {ties}, "
+               f"{len(fails)} unexplained {fails[:10]}; max score rel err {worst:.2e}")
+    print("\n" + summary)
+    assert not fails, summary
+    assert len(ties) <= max(1, n // 100), summary  # SURVEY §8(d): expect 0.1-0.3% near-tie exceptions
     return exact, ties
 
 
@@ -198,8 +237,37 @@ def _adjudicate(name, s, out):
 def test_full_size_decode_matches_reference(gpu, full, name):
     s = golden_full()["sets"][name]
     out = _decode_set(full, s)
-    exact, ties = _adjudicate(name, s, out)
-    assert exact >= len(s["results"]) - max(2, len(s["results"]) // 20)
+    gold = [(r["hyps"][0]["tokens"], r["hyps"][0]["score"]) for r in s["results"]]
+    gaps = [np.array(r["kth"]) - np.array(r["next"]) for r in s["results"]]
+    _adjudicate(name, gold, gaps, out)
+
+
+@pytest.mark.parametrize("name,max_batch", [("cfg2", 64), ("cfg4", 64), ("cfg5", 512)])
+def test_fullset_decode_matches_reference(gpu, full, name, max_batch):
+    """The headline workloads in full, decoded exactly as
+    bench.py decodes them (same bucket size), against the reference's own
+    1-best of every sentence (tests/golden/make_golden_fullset.py),
+    including the sentences that stop early on </s>."""
+    from paper_1610_01108_b200 import workload as W
+
+    g = golden_fullset(name)
+    wl = W.WORKLOADS[name]
+    corpus = wl.corpus()
+    assert fullset_src_sha(corpus) == str(g["src_sha256"]), "workload generator drifted from the goldens"
+    beam, f, o, _, _ = (int(x) for x in g["opts"])
+    dm = _lib.device_model(full)
+    out = _lib.decode([dm], corpus, beam, f, o, False, 2, max_batch=max_batch)
+    n = len(corpus)
+    toff, goff = g["tok_off"], g["gap_off"]
+    gold = [(g["tokens"][toff[i]:toff[i + 1]].astype(int).tolist(), float(g["score"][i])) for i in range(n)]
+    gaps = [g["gap"][goff[i]:goff[i + 1]] for i in range(n)]
+    exact, ties = _adjudicate(name, gold, gaps, out)
+    early = np.nonzero(g["finished"])[0].tolist()
+    tied = {t[0] for t in ties}
+    for i in early:  # EOS -> finished list -> stop rules at full size
+        h = out.hyps(i)[0]
+        assert h[2] and (h[0] == gold[i][0] or i in tied), (name, i, h[0][-5:], gold[i][0][-5:])
+    print(f"{name}: early-stopping sentences {early} all reproduced")
 
 
 def test_batch_composition_invariance(gpu, full):
@@ -355,3 +423,26 @@ def test_shortlist_batch_composition_invariance(gpu, full):
     b = _lib.decode([dm], src, 5, 2, 10, False, 1, shortlists=sls, max_batch=3)
     for i in range(len(src)):
         assert a.hyps(i)[0][:2] == b.hyps(i)[0][:2], i
+
+
+def test_engine_two_workers_on_one_device(gpu, full):
+    """The multi-device Engine path (engine.py:181-221 analogue: shard by
+    length-bucket LPT -> one host thread per device -> concurrent decode ->
+    gather by input index) exercised as two workers on GPU 0: byte-identical
+    to one worker."""
+    from paper_1610_01108_b200 import workload as W
+    from paper_1610_01108_b200.engine import Engine, EngineConfig
+    from paper_1610_01108_b200.model import Vocabulary
+
+    sents = W.WORKLOADS["cfg2"].corpus()[:96]
+    lines = W.lines_of(sents)
+    vocab = Vocabulary.from_tokens([f"w{i}" for i in range(2, W.V_SRC)])
+
+    def engine(devices):
+        cfg = EngineConfig(model_paths=("<memory>",), src_vocab_path="<memory>", trg_vocab_path="<memory>",
+                           devices=devices, max_batch=16, n_best=2)
+        return Engine(cfg, [full], vocab, vocab, None, None, None, 0, 0.0)
+
+    one = engine((0,)).translate_corpus(lines)
+    two = engine((0, 0)).translate_corpus(lines)
+    assert [(r.text, r.score, r.n_best) for r in one] == [(r.text, r.score, r.n_best) for r in two]

@@ -148,6 +148,33 @@ int amun_decoder_step(amun_model *m, const float *s, const int32_t *y_prev, int3
                       const float *h, const float *p, int32_t J, const int32_t *shortlist,
                       int32_t n_sl, float *s_out, double *logp_out, float *alpha_out);
 
+/* ---- production-kernel parity hooks -----------------------------------
+ * The hooks above run FP32 CUDA-core kernels; these two run exactly the
+ * kernels amun_decode runs (tcgen05 3xFP16 GEMMs, fused attention, fused
+ * tensor-core logits), so the per-step gates test the shipped code. */
+/* Forward.encode + init_state_row (nnet.py:110-130) for B padded sentences:
+ * ids [B, jmax] (entries past lens[b] ignored), lens [B] in [1, jmax].
+ * production = 1: tensor-core encoder (input projection, bi-GRU recurrence,
+ * precomp_att), 0: FP32 CUDA-core encoder.  h_out [B, jmax, 2 d_h] (zero
+ * rows past each length), p_out [B, jmax, d_att], s0_out [B, d_h]. */
+int amun_encode_batch(amun_model *m, const int32_t *ids, const int32_t *lens, int32_t B, int32_t jmax,
+                      int32_t production, float *h_out, float *p_out, float *s0_out);
+/* Forward.step_rows (nnet.py:143-164) + log_softmax_rows (tensor.py:79-92) +
+ * the per-row candidate stage of _select_top (search.py:169) for B
+ * sentences x k rows (row r belongs to sentence r / k), on the production
+ * kernels.  s [B*k, d_h], y_prev [B*k], h [B, jmax, 2 d_h], p [B, jmax,
+ * d_att], lens [B].  Outputs the fused logit kernel's partials per (row r,
+ * 128-wide vocabulary tile t), nt = ceil(v_trg / 128):
+ *   pmax/psum [B*k, nt]: max_t and sum_t exp(logit - max_t) of the tile;
+ *   cval/ctok [B*k, nt, kk]: the tile's kk best (logit, token), ordered by
+ *   (logit desc, token asc); token -1 marks an empty slot.
+ * log p(v | row) = logit_v - (M + log sum_t psum_t exp(pmax_t - M)).
+ * s_out [B*k, d_h], alpha_out [B*k, jmax] (either may be NULL). */
+int amun_decoder_step_fused(amun_model *m, int32_t B, int32_t k, const float *s, const int32_t *y_prev,
+                            const float *h, const float *p, const int32_t *lens, int32_t jmax, int32_t kk,
+                            float *s_out, float *pmax_out, float *psum_out, float *cval_out, int32_t *ctok_out,
+                            float *alpha_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,8 @@ AMUN_OK, AMUN_ERR_INVALID, AMUN_ERR_CUDA, AMUN_ERR_OOM, AMUN_ERR_UNSUPPORTED = 0
 EXPORTS = (
     "amun_last_error", "amun_version", "amun_device_count", "amun_model_create", "amun_model_destroy",
     "amun_model_device_bytes", "amun_decode", "amun_result_free", "amun_encode", "amun_attention",
-    "amun_decoder_step", "amun_init_state", "amun_gru_cell", "amun_decode_stream",
+    "amun_decoder_step", "amun_init_state", "amun_gru_cell", "amun_decode_stream", "amun_encode_batch",
+    "amun_decoder_step_fused",
 )
 
 _i32, _i64, _f32p, _f64p, _i32p = ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_float), \
@@ -94,6 +95,9 @@ def load() -> ctypes.CDLL:
         lib.amun_init_state.argtypes = [ctypes.c_void_p, _f32p, _i32, _f32p]
         lib.amun_gru_cell.argtypes = [_i32, _i32, _i32, ctypes.POINTER(_f32p), ctypes.POINTER(_f32p),
                                       ctypes.POINTER(_f32p), _i32, _f32p, _f32p, _f32p]
+        lib.amun_encode_batch.argtypes = [ctypes.c_void_p, _i32p, _i32p, _i32, _i32, _i32, _f32p, _f32p, _f32p]
+        lib.amun_decoder_step_fused.argtypes = [ctypes.c_void_p, _i32, _i32, _f32p, _i32p, _f32p, _f32p, _i32p,
+                                                _i32, _i32, _f32p, _f32p, _f32p, _f32p, _i32p, _f32p]
         for name in EXPORTS:
             if name not in ("amun_last_error", "amun_version", "amun_model_destroy", "amun_result_free"):
                 getattr(lib, name).restype = ctypes.c_int
@@ -203,6 +207,65 @@ class DeviceModel:
                                        0 if sl is None else sl.size, _ptr(s_out, _f32p), _ptr(logp, _f64p),
                                        _ptr(alpha, _f32p)))
         return s_out, logp, alpha
+
+    # ---- production-kernel hooks (the tensor-core kernels amun_decode runs)
+    def encode_batch(self, sentences: Sequence[Sequence[int]], production: bool = True):
+        """Encoder + initial state of B sentences as one padded bucket:
+        returns h [B, jmax, 2 d_h], p [B, jmax, d_att], s0 [B, d_h]."""
+        cfg = self.config
+        lens = np.asarray([len(s) for s in sentences], np.int32)
+        B, jmax = lens.size, int(lens.max())
+        ids = np.zeros((B, jmax), np.int32)
+        for b, s in enumerate(sentences):
+            ids[b, :len(s)] = s
+        h = np.empty((B, jmax, 2 * cfg.d_h), np.float32)
+        p = np.empty((B, jmax, cfg.d_att), np.float32)
+        s0 = np.empty((B, cfg.d_h), np.float32)
+        check(load().amun_encode_batch(self.handle, _ptr(ids, _i32p), _ptr(lens, _i32p), B, jmax, int(production),
+                                       _ptr(h, _f32p), _ptr(p, _f32p), _ptr(s0, _f32p)))
+        return h, p, s0
+
+    def step_fused(self, s: np.ndarray, y_prev: Sequence[int], h: np.ndarray, p: np.ndarray,
+                   lens: Sequence[int], k: int, kk: int):
+        """One decoder step of B sentences x k rows on the production kernels.
+        Returns s' [R, d_h], the per-row log-normaliser lse [R] (f64, merged
+        from the logit kernel's per-tile partials the way the select kernel
+        merges them) and the row's kk best candidates (tokens [R, kk],
+        log-probs [R, kk], ordered by (log-prob desc, token asc))."""
+        cfg = self.config
+        s, h, p = _f32(np.atleast_2d(s)), _f32(h), _f32(p)
+        y = np.ascontiguousarray(y_prev, dtype=np.int32).reshape(-1)
+        lens_a = np.ascontiguousarray(lens, dtype=np.int32)
+        B, jmax = h.shape[0], h.shape[1]
+        R = B * k
+        if s.shape != (R, cfg.d_h) or y.size != R or lens_a.size != B:
+            raise ShapeError(f"{s.shape} states / {y.size} tokens for {B} sentences x {k} rows")
+        if h.shape != (B, jmax, 2 * cfg.d_h) or p.shape != (B, jmax, cfg.d_att):
+            raise ShapeError(f"annotations have shapes {h.shape} / {p.shape}")
+        nt = -(-cfg.v_trg // 128)
+        s_out = np.empty((R, cfg.d_h), np.float32)
+        pmax = np.empty((R, nt), np.float32)
+        psum = np.empty((R, nt), np.float32)
+        cval = np.empty((R, nt, kk), np.float32)
+        ctok = np.empty((R, nt, kk), np.int32)
+        check(load().amun_decoder_step_fused(self.handle, B, k, _ptr(s, _f32p), _ptr(y, _i32p), _ptr(h, _f32p),
+                                             _ptr(p, _f32p), _ptr(lens_a, _i32p), jmax, kk, _ptr(s_out, _f32p),
+                                             _ptr(pmax, _f32p), _ptr(psum, _f32p), _ptr(cval, _f32p),
+                                             _ptr(ctok, _i32p), None))
+        # select-kernel merge (kernels.cu select phase 1): M = max_t pmax_t,
+        # lse = M + log sum_t psum_t exp(pmax_t - M), summed in f64
+        mx = pmax.max(axis=1)
+        lse = mx.astype(np.float64) + np.log((psum * np.exp(pmax - mx[:, None])).astype(np.float64).sum(axis=1))
+        flat_v = cval.reshape(R, -1).astype(np.float64)
+        flat_t = ctok.reshape(R, -1)
+        tok = np.empty((R, kk), np.int64)
+        lp = np.empty((R, kk), np.float64)
+        for r in range(R):
+            ok = flat_t[r] >= 0
+            order = np.lexsort((flat_t[r][ok], -flat_v[r][ok]))[:kk]
+            tok[r] = flat_t[r][ok][order]
+            lp[r] = flat_v[r][ok][order] - lse[r]
+        return s_out, lse, tok, lp
 
     def _check_rows(self, s, h, p):
         cfg = self.config

@@ -378,3 +378,44 @@ extern "C" int amun_gru_cell(int32_t device, int32_t d_in, int32_t d_h, const fl
   hook_gru_cell(device, d_in, d_h, W, U, b, R, x, h, h_out);
   AMUN_API_END
 }
+
+extern "C" int amun_encode_batch(amun_model *m, const int32_t *ids, const int32_t *lens, int32_t B, int32_t jmax,
+                                 int32_t production, float *h_out, float *p_out, float *s0_out) {
+  AMUN_API_BEGIN
+  if (!m || !ids || !lens) invalid("null argument");
+  if (B < 1 || jmax < 1) invalid("encode needs at least one sentence and one position");
+  for (int b = 0; b < B; ++b) {
+    if (lens[b] < 1) invalid("cannot encode an empty source sentence");
+    if (lens[b] > jmax) invalid("sentence length exceeds jmax");
+    for (int j = 0; j < lens[b]; ++j) {
+      const int32_t v = ids[(size_t)b * jmax + j];
+      if (v < 0 || v >= m->d.v_src)
+        invalid("source id " + std::to_string(v) + " at position " + std::to_string(j) +
+                " out of range for v_src=" + std::to_string(m->d.v_src));
+    }
+  }
+  // positions past a sentence's length are never read as ids of real
+  // tokens, but the gather still indexes them: pass a sanitised copy
+  std::vector<int32_t> safe(ids, ids + (size_t)B * jmax);
+  for (int b = 0; b < B; ++b)
+    for (int j = lens[b]; j < jmax; ++j) safe[(size_t)b * jmax + j] = 0;
+  hook_encode_batch(m, safe.data(), lens, B, jmax, production != 0, h_out, p_out, s0_out);
+  AMUN_API_END
+}
+
+extern "C" int amun_decoder_step_fused(amun_model *m, int32_t B, int32_t k, const float *s, const int32_t *y_prev,
+                                       const float *h, const float *p, const int32_t *lens, int32_t jmax,
+                                       int32_t kk, float *s_out, float *pmax_out, float *psum_out,
+                                       float *cval_out, int32_t *ctok_out, float *alpha_out) {
+  AMUN_API_BEGIN
+  if (!m || !s || !y_prev || !h || !p || !lens) invalid("null argument");
+  if (B < 1 || k < 1 || jmax < 1) invalid("decoder step needs at least one state row and one source position");
+  for (int b = 0; b < B; ++b)
+    if (lens[b] < 1 || lens[b] > jmax) invalid("source lengths must lie in [1, jmax]");
+  for (int r = 0; r < B * k; ++r)
+    if (y_prev[r] < 0 || y_prev[r] >= m->d.v_trg)
+      invalid("previous token id " + std::to_string(y_prev[r]) + " out of range for v_trg=" +
+              std::to_string(m->d.v_trg));
+  hook_step_tc(m, B, k, s, y_prev, h, p, lens, jmax, kk, s_out, pmax_out, psum_out, cval_out, ctok_out, alpha_out);
+  AMUN_API_END
+}

@@ -1439,6 +1439,117 @@ void hook_step(amun_model *m, const float *s, const int32_t *y_prev, int R, cons
   AMUN_CUDA(cudaStreamSynchronize(c.st));
 }
 
+// fp16 split of the y and s parts of decoder rows in the padded layout
+// [y | pad | c | s] (what select's next-row gather writes in production)
+__global__ void build_rows_split_kernel(__half *XSh, __half *XSl, int ldh, const float *E, const int *y,
+                                        const float *s, int de, int dh, int s_off_h) {
+  const int r = blockIdx.x;
+  const long long ro = (long long)r * ldh;
+  for (int c = threadIdx.x; c < de; c += blockDim.x) store_split(XSh, XSl, ro + c, E[(long long)y[r] * de + c]);
+  for (int c = threadIdx.x; c < dh; c += blockDim.x)
+    store_split(XSh, XSl, ro + s_off_h + c, s[(long long)r * dh + c]);
+}
+
+// Production-kernel step hook: B sentences x k hypothesis rows through
+// exactly the kernels amun_decode runs per step (tcgen05 query / GRU-A /
+// GRU-B / deep-output GEMMs, fused attention writing the context split, and
+// the fused tensor-core logit kernel), returning the logit kernel's raw
+// per-(row, 128-vocab tile) partials: (max, sum exp) and the tile's top-kk
+// (value, token).  nnet.py:143-164 + tensor.py:79-92 + search.py:169.
+void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_prev, const float *h,
+                  const float *p, const int32_t *lens, int jmax, int kk, float *s_out, float *pmax_out,
+                  float *psum_out, float *cval_out, int32_t *ctok_out, float *alpha_out) {
+  if (!m->tc_gemm || !m->Wl_hi)
+    throw Error(AMUN_ERR_UNSUPPORTED, "model dimensions / embedding range are outside the tensor-core path");
+  if (kk < 1 || kk > kMaxRowCand) throw Error(AMUN_ERR_UNSUPPORTED, "kk must be in [1, 16]");
+  AMUN_CUDA(cudaSetDevice(m->device));
+  Ctx c(m->stream);
+  const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
+  const int R = B * k, ntiles = ceil_div(V, kBN);
+  EncBufs e{};
+  DecBufs d{};
+  int *d_len, *d_y, *ctok;
+  float *d_s, *d_alpha, *pmax, *psum, *cval;
+  DevMem mem;
+  for (int pass = 0; pass < 2; ++pass) {
+    Carver cv;
+    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
+    e.Hann = cv.take<float>((size_t)B * jmax * 2 * dh);
+    e.P = cv.take<float>((size_t)B * jmax * da);
+    carve_dec(cv, d, m, R, jmax, false);
+    carve_dec_tc(cv, d, m, R);
+    d_len = cv.take<int>(B);
+    d_y = cv.take<int>(R);
+    d_s = cv.take<float>((size_t)R * dh);
+    d_alpha = cv.take<float>((size_t)R * jmax);
+    pmax = cv.take<float>((size_t)R * ntiles);
+    psum = cv.take<float>((size_t)R * ntiles);
+    cval = cv.take<float>((size_t)R * ntiles * kk);
+    ctok = cv.take<int>((size_t)R * ntiles * kk);
+    if (!pass) mem.alloc(cv.off, c.st);
+  }
+  h2d(c, e.Hann, h, (size_t)B * jmax * 2 * dh);
+  h2d(c, e.P, p, (size_t)B * jmax * da);
+  h2d(c, d_len, lens, B);
+  h2d(c, d_s, s, (size_t)R * dh);
+  h2d(c, d_y, y_prev, R);
+  AMUN_CUDA(cudaMemsetAsync(d.XS, 0, sizeof(float) * (size_t)R * xs, c.st));
+  AMUN_CUDA(cudaMemsetAsync(d.XSh, 0, sizeof(__half) * (size_t)R * m->xsp, c.st));
+  AMUN_CUDA(cudaMemsetAsync(d.XSl, 0, sizeof(__half) * (size_t)R * m->xsp, c.st));
+  build_rows_kernel<<<R, 256, 0, c.st>>>(d.XS, xs, m->E_trg, d_y, d_s, de, dh, de + 2 * dh);
+  AMUN_CHECK_LAUNCH();
+  build_rows_split_kernel<<<R, 256, 0, c.st>>>(d.XSh, d.XSl, m->xsp, m->E_trg, d_y, d_s, de, dh, m->dep + 2 * dh);
+  AMUN_CHECK_LAUNCH();
+  TcStep ts;
+  tc_step_maps(m, d, R, ts);
+  const LogitTcMaps lm = make_logit_maps(d.T_hi, d.T_lo, R, de, m->dep, m->Wl_hi, m->Wl_lo, m->dep, V);
+  LogitOut lo{true, kk, ntiles, pmax, psum, cval, ctok};
+  lo.tc = &lm;
+  step_rows(c, m, d, e, d_len, jmax, R, k, nullptr, nullptr, d_alpha, lo, &ts);
+  if (s_out) d2h(c, s_out, d.Sn, (size_t)R * dh);
+  if (pmax_out) d2h(c, pmax_out, pmax, (size_t)R * ntiles);
+  if (psum_out) d2h(c, psum_out, psum, (size_t)R * ntiles);
+  if (cval_out) d2h(c, cval_out, cval, (size_t)R * ntiles * kk);
+  if (ctok_out) d2h(c, ctok_out, ctok, (size_t)R * ntiles * kk);
+  if (alpha_out) d2h(c, alpha_out, d_alpha, (size_t)R * jmax);
+  AMUN_CUDA(cudaStreamSynchronize(c.st));
+}
+
+// Batched encoder hook: B padded sentences (ids [B][jmax], lens[B]) through
+// encode_bucket, on the production tensor-core kernels (input projection,
+// bi-GRU recurrence, precomp_att) when `production`, else on the FP32
+// CUDA-core kernels.  h_out [B][jmax][2 d_h] (zero past each length),
+// p_out [B][jmax][d_att], s0_out [B][d_h].
+void hook_encode_batch(amun_model *m, const int32_t *ids, const int32_t *lens, int B, int jmax, bool production,
+                       float *h_out, float *p_out, float *s0_out) {
+  if (production && !m->Uzr_hi)
+    throw Error(AMUN_ERR_UNSUPPORTED, "model dimensions / embedding range are outside the tensor-core path");
+  AMUN_CUDA(cudaSetDevice(m->device));
+  Ctx c(m->stream);
+  EncBufs e{};
+  int *d_ids, *d_len;
+  DevMem mem;
+  for (int pass = 0; pass < 2; ++pass) {
+    Carver cv;
+    cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
+    carve_enc(cv, e, m, B, jmax);
+    if (production) carve_enc_tc(cv, e, m, B, jmax);
+    d_ids = cv.take<int>((size_t)B * jmax);
+    d_len = cv.take<int>(B);
+    if (!pass) mem.alloc(cv.off, c.st);
+  }
+  h2d(c, d_ids, ids, (size_t)B * jmax);
+  h2d(c, d_len, lens, B);
+  TcEnc te;
+  if (production) tc_enc_maps(m, e, B, jmax, te);
+  encode_bucket(c, m, e, d_ids, d_len, B, jmax, production ? &te : nullptr);
+  const int dh = m->d.d_h, da = m->d.d_att;
+  if (h_out) d2h(c, h_out, e.Hann, (size_t)B * jmax * 2 * dh);
+  if (p_out) d2h(c, p_out, e.P, (size_t)B * jmax * da);
+  if (s0_out) d2h(c, s0_out, e.S0, (size_t)B * dh);
+  AMUN_CUDA(cudaStreamSynchronize(c.st));
+}
+
 }  // namespace amun
 
 namespace amun {

@@ -67,4 +67,11 @@ void hook_step(amun_model *m, const float *s, const int32_t *y_prev, int R, cons
                int J, const int32_t *sl, int n_sl, float *s_out, double *logp_out, float *alpha_out,
                float *ctx_out);
 
+// production-kernel parity hooks (the tensor-core kernels amun_decode runs)
+void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_prev, const float *h,
+                  const float *p, const int32_t *lens, int jmax, int kk, float *s_out, float *pmax_out,
+                  float *psum_out, float *cval_out, int32_t *ctok_out, float *alpha_out);
+void hook_encode_batch(amun_model *m, const int32_t *ids, const int32_t *lens, int B, int jmax, bool production,
+                       float *h_out, float *p_out, float *s0_out);
+
 }  // namespace amun

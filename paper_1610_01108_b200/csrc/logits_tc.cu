@@ -339,14 +339,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[4 * u4 + 2] = t4.z;
             x[4 * u4 + 3] = t4.w;
           }
-          // two 16-wide half maxima, the quarter max, and sum exp(x - max)
-          // (ex2-based: x log2 e - max log2 e, one FFMA + MUFU per logit)
-          float h0 = x[0], h1 = x[16];
+          // four 8-wide group maxima, the two 16-wide half maxima, the
+          // quarter max, and sum exp(x - max) (ex2-based: x log2 e - max
+          // log2 e, one FFMA + MUFU per logit)
+          float g8[4];
 #pragma unroll
-          for (int i = 1; i < 16; ++i) {
-            h0 = fmaxf(h0, x[i]);
-            h1 = fmaxf(h1, x[16 + i]);
+          for (int j = 0; j < 4; ++j) {
+            g8[j] = x[8 * j];
+#pragma unroll
+            for (int i = 1; i < 8; ++i) g8[j] = fmaxf(g8[j], x[8 * j + i]);
           }
+          const float h0 = fmaxf(g8[0], g8[1]), h1 = fmaxf(g8[2], g8[3]);
           float mx = fmaxf(h0, h1);
           stamp(3);
           float se = 0.f;
@@ -355,9 +358,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) se += tc::exp2f_approx(fmaf(x[i], 1.4426950408889634f, -mxl));
           }
-          // Threshold: the KK-th largest of the row's 8 half maxima is a lower
-          // bound on the row's KK-th largest logit (those maxima are 8 distinct
-          // logits), so only logits >= thr can be in the tile's top-KK.
+          // Threshold: the KK-th largest of the row's 8 half maxima (16 group
+          // maxima for KK > 8) is a lower bound on the row's KK-th largest
+          // logit (those maxima are distinct logits), so only logits >= thr
+          // can be in the tile's top-KK.
           stamp(4);
           float thr = -INFINITY;
           if constexpr (KK <= 8) {
@@ -375,6 +379,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float hi = fmaxf(hm[j - 1], hm[j]), lo = fminf(hm[j - 1], hm[j]);
                 hm[j - 1] = hi;
                 hm[j] = lo;
+              }
+            thr = hm[KK - 1];
+          } else {
+            // KK > 8 (beam 9..16): the KK-th largest of the row's 16 group
+            // maxima (16 distinct logits) bounds the tile's KK-th largest
+            // logit from below; 17 - KK bubble passes sink the smallest
+            // maxima to the end, leaving the KK-th largest at KK - 1
+            float hm[16];
+            const int lb = lane & ~3;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) hm[4 * j + u] = __shfl_sync(0xffffffffu, g8[u], lb + j);
+#pragma unroll
+            for (int p = 0; p < 17 - KK; ++p)
+#pragma unroll
+              for (int j = 0; j < 15 - p; ++j) {
+                const float hi = fmaxf(hm[j], hm[j + 1]), lo = fminf(hm[j], hm[j + 1]);
+                hm[j] = hi;
+                hm[j + 1] = lo;
               }
             thr = hm[KK - 1];
           }

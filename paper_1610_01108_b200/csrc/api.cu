@@ -177,6 +177,27 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
       m->us_eb = upload_kmajor_split(m, Uh.data(), 2 * dh, dh, 2 * dh, ident, &m->Uh_hi, &m->Uh_lo);
     }
   }
+  if (m->tc_ok) {  // encode-ahead recurrence weights: [x | state] rows (x padded to dep)
+    auto xsmap = [de, pad = m->dep - de](int c) { return c < de ? c : c + pad; };
+    for (int dir = 0; dir < 2; ++dir) {
+      const int base = dir ? T_ENC_BWD : T_ENC_FWD;
+      std::vector<float> A((size_t)(de + dh) * 2 * dh), Bm((size_t)(de + dh) * dh);
+      for (int i = 0; i < de; ++i) {
+        std::memcpy(&A[(size_t)i * 2 * dh], t[base + G_WZ] + (size_t)i * dh, dh * sizeof(float));
+        std::memcpy(&A[(size_t)i * 2 * dh + dh], t[base + G_WR] + (size_t)i * dh, dh * sizeof(float));
+        std::memcpy(&Bm[(size_t)i * dh], t[base + G_WH] + (size_t)i * dh, dh * sizeof(float));
+      }
+      for (int i = 0; i < dh; ++i) {
+        std::memcpy(&A[(size_t)(de + i) * 2 * dh], t[base + G_UZ] + (size_t)i * dh, dh * sizeof(float));
+        std::memcpy(&A[(size_t)(de + i) * 2 * dh + dh], t[base + G_UR] + (size_t)i * dh, dh * sizeof(float));
+        std::memcpy(&Bm[(size_t)(de + i) * dh], t[base + G_UH] + (size_t)i * dh, dh * sizeof(float));
+      }
+      m->us_efa[dir] = upload_kmajor_split(m, A.data(), de + dh, 2 * dh, m->dep + dh, xsmap, &m->Efa_hi[dir],
+                                           &m->Efa_lo[dir]);
+      m->us_efb[dir] = upload_kmajor_split(m, Bm.data(), de + dh, dh, m->dep + dh, xsmap, &m->Efb_hi[dir],
+                                           &m->Efb_lo[dir]);
+    }
+  }
   m->W_att_h = upload(m, cp(T_W_ATT_H, (size_t)2 * dh * da));
   if (m->tc_ok)
     m->us_p = upload_kmajor_split(m, t[T_W_ATT_H], 2 * dh, da, 2 * dh, ident, &m->Watth_hi, &m->Watth_lo);

@@ -186,13 +186,17 @@ struct Ctx {
     }
     return pool[used++];
   }
-  template <class F>
-  void run(int k, F &&f) {
-    static const unsigned skip = [] {  // profiling ablation only: outputs are garbage
+  // profiling ablation only (AMUN_ABLATE_CLASSES bitmask): outputs are garbage
+  static unsigned ablated() {
+    static const unsigned skip = [] {
       const char *e = getenv("AMUN_ABLATE_CLASSES");
       return e ? (unsigned)strtoul(e, nullptr, 0) : 0u;
     }();
-    if (skip & (1u << k)) return;
+    return skip;
+  }
+  template <class F>
+  void run(int k, F &&f) {
+    if (ablated() & (1u << k)) return;
     ++launches;
     if (!(prof & (1u << k))) {
       f();
@@ -217,6 +221,17 @@ struct Ctx {
     used = 0;
   }
 };
+
+template <class T>
+void h2d(Ctx &c, T *dst, const T *src, size_t n) {
+  if (n) AMUN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, c.st));
+  c.h2d += (int64_t)(n * sizeof(T));
+}
+template <class T>
+void d2h(Ctx &c, T *dst, const T *src, size_t n) {
+  if (n) AMUN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, c.st));
+  c.d2h += (int64_t)(n * sizeof(T));
+}
 
 GemmArgs ga(int M, int N, const float *a0, int lda0, int k0, const float *B, int ldb) {
   GemmArgs g{};
@@ -427,6 +442,259 @@ void encode_bucket(Ctx &c, const amun_model *m, const EncBufs &e, const int *d_i
   gemm(c, ga(B, dh, e.Hmean, 2 * dh, 2 * dh, m->W_init, dh), EpiStore{e.S0, dh, m->b_init, 1, 0});
 }
 
+// ================================================================ encode-ahead
+//
+// The encoder of a whole chunk of sentences (nnet.py:110-130), run before the
+// decode lanes start instead of per length bucket: the bi-GRU recurrence is
+// one GEMM pair per time step and direction over EVERY sentence still active
+// at that step (sentences in descending length order, so the active set is a
+// prefix), with the input projection fused into the recurrent GEMMs (the
+// activation row is [x_t | state], the weight [W ; U]).  At the headline
+// workload a step's GEMM has up to 4000 rows instead of 64: the tensor cores
+// run full tiles, the weights are read once per step for all sentences, and
+// the encoder costs ~2 x max-length launches per direction for the whole
+// call instead of 2 x J launches per bucket.  Forward and backward run
+// concurrently on two streams.  Results land in an annotation store laid out
+// per length bucket ([B][jmax] rows), which the decode lanes read in place.
+
+struct AheadIn {
+  int n;                       // sentences
+  const int32_t *ids;          // host, sentence i at ids + off[i]
+  const long long *off;        // host [n]
+  const int32_t *len;          // host [n]
+  const long long *ann_row;    // host [n]: store row of (sentence i, position 0)
+  long long store_rows;
+};
+struct AheadOut {
+  float *Hann, *P, *S0;  // store [rows][2dh], [rows][da]; S0 [n][dh] indexed by sentence i
+  __half *Hah, *Hal;     // store [rows][2dh] split annotations
+};
+
+// Hmean[i] = Hsum[e(i)] / len[e(i)] for sentences i0 .. i0 + gridDim.x - 1
+__global__ void enc_mean_kernel(const float *__restrict__ Hsum, const int *__restrict__ len_e,
+                                const int *__restrict__ e_of_i, int i0, int w, float *__restrict__ out) {
+  const int i = i0 + blockIdx.x, e = e_of_i[i];
+  const float inv = 1.0f / (float)len_e[e];
+  const float *src = Hsum + (long long)e * w;
+  float *dst = out + (long long)i * w;
+  for (int c = threadIdx.x; c < w; c += blockDim.x) dst[c] = src[c] * inv;
+}
+
+int ahead_target_ctas() {
+  static int v = [] {
+    const char *e = getenv("AMUN_AHEAD_CTAS");
+    return e ? std::max(2, atoi(e)) : 148;
+  }();
+  return v;
+}
+
+// (splits, z-grid) of one encode-ahead GEMM launch.  The split count comes
+// from (N, K) only (about 32 CTAs per row pass), never from the row count, so
+// a sentence's encoder result does not depend on which other sentences share
+// the call, chunk or device; the z-grid spreads the row passes.
+template <class C = SkDefault>
+std::pair<int, int> ahead_grid(const SkMaps &mp, int M, int target) {
+  const int per_pass = ceil_div(mp.N, 128 * C::kCG) * C::kCG;
+  const int s = sk_fit_splits<C>(mp, 32);
+  const int npass = ceil_div(M, C::kPR);
+  return {s, std::max(1, std::min(npass, target / (per_pass * s)))};
+}
+
+// run(): the recurrence of every sentence (both directions, two streams);
+// an event per time step marks which sentences are complete (a sentence of
+// length L is final after step L - 1 in both directions).  prepare(): on a
+// decode lane's stream, once a bucket's sentences are complete, its
+// precomp_att rows (nnet.py:126) and initial states tanh(mean_j h_j W_init +
+// b_init) (nnet.py:128-130) -- so the lanes start decoding short buckets
+// while the encoder still runs the long sentences' tail steps.
+class AheadEncoder {
+ public:
+  AheadEncoder(const amun_model *m, const AheadIn &in, const AheadOut &out, cudaMemPool_t pool)
+      : m_(m), in_(in), out_(out), pool_(pool) {}
+  AheadEncoder(const AheadEncoder &) = delete;
+  AheadEncoder &operator=(const AheadEncoder &) = delete;
+  ~AheadEncoder() = default;
+
+  void run(Ctx &cf, Ctx &cb) {
+    const amun_model *m = m_;
+    const int n = in_.n, de = m->d.d_emb, dh = m->d.d_h, dep = m->dep;
+    std::vector<int> ord(n);  // encoder row e -> sentence, descending length (stable)
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return in_.len[a] > in_.len[b]; });
+    T_ = in_.len[ord[0]];
+    std::vector<int> nact(T_, 0);
+    for (int e = 0; e < n; ++e)
+      for (int t = 0; t < in_.len[ord[e]]; ++t) ++nact[t];
+    std::vector<long long> offt(T_ + 1, 0);
+    for (int t = 0; t < T_; ++t) offt[t + 1] = offt[t] + nact[t];
+    const long long total = offt[T_];
+    std::vector<int> tokf(total), tokb(total), len_e(n), e_of_i(n);
+    std::vector<long long> arow(n);
+    std::vector<char> need(T_, 0);  // some sentence completes at step t
+    for (int e = 0; e < n; ++e) {
+      const int i = ord[e];
+      len_e[e] = in_.len[i];
+      e_of_i[i] = e;
+      arow[e] = in_.ann_row[i];
+      need[in_.len[i] - 1] = 1;
+    }
+    for (int t = 0; t < T_; ++t)
+      for (int e = 0; e < nact[t]; ++e) {
+        const int i = ord[e];
+        tokf[offt[t] + e] = in_.ids[in_.off[i] + t];
+        tokb[offt[t] + e] = in_.ids[in_.off[i] + in_.len[i] - 1 - t];
+      }
+    int *d_tok[2];
+    __half *Xh[2], *Xl[2], *Hh[2], *Hl[2], *RHh[2], *RHl[2];
+    float *H[2], *Z[2];
+    for (int pass = 0; pass < 2; ++pass) {
+      Carver cv;
+      cv.base = static_cast<char *>(mem_);
+      for (int d = 0; d < 2; ++d) {
+        d_tok[d] = cv.take<int>(total);
+        Xh[d] = cv.take<__half>((size_t)total * dep);
+        Xl[d] = cv.take<__half>((size_t)total * dep);
+        Hh[d] = cv.take<__half>((size_t)n * dh);
+        Hl[d] = cv.take<__half>((size_t)n * dh);
+        RHh[d] = cv.take<__half>((size_t)n * dh);
+        RHl[d] = cv.take<__half>((size_t)n * dh);
+        H[d] = cv.take<float>((size_t)n * dh);
+        Z[d] = cv.take<float>((size_t)n * dh);
+      }
+      d_len_ = cv.take<int>(n);
+      d_e_of_i_ = cv.take<int>(n);
+      d_arow_ = cv.take<long long>(n);
+      Hsum_ = cv.take<float>((size_t)n * 2 * dh);
+      Hmean_ = cv.take<float>((size_t)n * 2 * dh);
+      if (!pass) AMUN_CUDA(cudaMallocFromPoolAsync(&mem_, std::max<size_t>(cv.off, 256), pool_, cf.st));
+    }
+    h2d(cf, d_tok[0], tokf.data(), total);
+    h2d(cf, d_tok[1], tokb.data(), total);
+    h2d(cf, d_len_, len_e.data(), n);
+    h2d(cf, d_e_of_i_, e_of_i.data(), n);
+    h2d(cf, d_arow_, arow.data(), n);
+    // store: padded positions must read as zero (attention masks them, the
+    // precomp GEMM reads them); P and S0 are fully written by prepare()
+    const size_t ann = (size_t)in_.store_rows * 2 * dh;
+    AMUN_CUDA(cudaMemsetAsync(out_.Hann, 0, ann * sizeof(float), cf.st));
+    AMUN_CUDA(cudaMemsetAsync(out_.Hah, 0, ann * sizeof(__half), cf.st));
+    AMUN_CUDA(cudaMemsetAsync(out_.Hal, 0, ann * sizeof(__half), cf.st));
+    if (Ctx::ablated() & (1u << AMUN_K_ENCODER)) {  // encoder ablated: finite inputs for the decoder
+      AMUN_CUDA(cudaMemsetAsync(out_.P, 0, sizeof(float) * (size_t)in_.store_rows * m->d.d_att, cf.st));
+      AMUN_CUDA(cudaMemsetAsync(out_.S0, 0, sizeof(float) * (size_t)n * dh, cf.st));
+    }
+    for (int d = 0; d < 2; ++d) {
+      AMUN_CUDA(cudaMemsetAsync(H[d], 0, sizeof(float) * (size_t)n * dh, cf.st));
+      AMUN_CUDA(cudaMemsetAsync(Hh[d], 0, sizeof(__half) * (size_t)n * dh, cf.st));
+      AMUN_CUDA(cudaMemsetAsync(Hl[d], 0, sizeof(__half) * (size_t)n * dh, cf.st));
+      cf.run(AMUN_K_ENCODER, [&] {
+        gather_split_kernel<<<(unsigned)total, 128, 0, cf.st>>>(m->E_src, d_tok[d], de, dep, Xh[d], Xl[d]);
+        AMUN_CHECK_LAUNCH();
+      });
+    }
+    const bool two = cb.st != cf.st;
+    cudaEvent_t ev0 = new_event();
+    AMUN_CUDA(cudaEventRecord(ev0, cf.st));
+    if (two) AMUN_CUDA(cudaStreamWaitEvent(cb.st, ev0, 0));
+    SkMaps fa[2], fb[2];
+    for (int d = 0; d < 2; ++d) {
+      fa[d] = make_sk_maps(Xh[d], Xl[d], dep, dep, Hh[d], Hl[d], dh, dh, (int)total, m->Efa_hi[d], m->Efa_lo[d],
+                           2 * dh, dep + dh, m->us_efa[d], n);
+      fb[d] = make_sk_maps(Xh[d], Xl[d], dep, dep, RHh[d], RHl[d], dh, dh, (int)total, m->Efb_hi[d],
+                           m->Efb_lo[d], dh, dep + dh, m->us_efb[d], n);
+    }
+    const int target = ahead_target_ctas() / (two ? 2 : 1);
+    evf_.assign(T_, nullptr);
+    evb_.assign(T_, nullptr);
+    for (int t = 0; t < T_; ++t) {
+      for (int d = 0; d < 2; ++d) {
+        Ctx &c = d ? cb : cf;
+        const int M = nact[t];
+        const float *bias = m->benc + d * 3 * dh;
+        EpiEncFA ea{bias, H[d], Z[d], RHh[d], RHl[d], dh};
+        const auto ga_ = ahead_grid(fa[d], M, target);
+        c.run(AMUN_K_ENCODER,
+              [&] { launch_gemm_sk(fa[d], M, ga_.first, ea, c.st, 0, (int)offt[t], ga_.second); });
+        EpiEncFB eb{bias + 2 * dh, H[d], Z[d], Hh[d], Hl[d], out_.Hann, out_.Hah, out_.Hal, Hsum_, d_len_,
+                    d_arow_, dh, t, d};
+        const auto gb_ = ahead_grid(fb[d], M, target);
+        c.run(AMUN_K_ENCODER,
+              [&] { launch_gemm_sk(fb[d], M, gb_.first, eb, c.st, 0, (int)offt[t], gb_.second); });
+      }
+      if (need[t]) {
+        evf_[t] = new_event();
+        AMUN_CUDA(cudaEventRecord(evf_[t], cf.st));
+        if (two) {
+          evb_[t] = new_event();
+          AMUN_CUDA(cudaEventRecord(evb_[t], cb.st));
+        }
+      }
+    }
+    if (two) {  // the temporaries are freed on cf: order cb's work before that
+      cudaEvent_t e = new_event();
+      AMUN_CUDA(cudaEventRecord(e, cb.st));
+      AMUN_CUDA(cudaStreamWaitEvent(cf.st, e, 0));
+    }
+  }
+
+  // Sentences [i0, i0 + cnt) (max length jmax) whose store rows are
+  // [row0, row0 + nrows): precomp_att and initial states on c's stream.
+  void prepare(Ctx &c, int i0, int cnt, long long row0, long long nrows, int jmax) {
+    const amun_model *m = m_;
+    const int dh = m->d.d_h, da = m->d.d_att;
+    if (jmax < 1 || jmax > T_ || !evf_[jmax - 1]) throw Error(AMUN_ERR_CUDA, "encode-ahead: bucket not tracked");
+    AMUN_CUDA(cudaStreamWaitEvent(c.st, evf_[jmax - 1], 0));
+    if (evb_[jmax - 1]) AMUN_CUDA(cudaStreamWaitEvent(c.st, evb_[jmax - 1], 0));
+    const SkMaps pm = make_sk_maps(out_.Hah, out_.Hal, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0,
+                                   (int)in_.store_rows, m->Watth_hi, m->Watth_lo, da, 2 * dh, m->us_p);
+    const int M = (int)nrows;
+    const auto gp = ahead_grid(pm, M, std::max(32, prep_ctas_));
+    EpiStore ep{out_.P + row0 * da, da, nullptr, 0, 0};
+    const int cls = c.cls;
+    c.cls = AMUN_K_ENCODER;
+    c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(pm, M, gp.first, ep, c.st, 0, (int)row0, gp.second); });
+    c.run(AMUN_K_ENCODER, [&] {
+      enc_mean_kernel<<<cnt, 256, 0, c.st>>>(Hsum_, d_len_, d_e_of_i_, i0, 2 * dh, Hmean_);
+      AMUN_CHECK_LAUNCH();
+    });
+    gemm(c, ga(cnt, dh, Hmean_ + (long long)i0 * 2 * dh, 2 * dh, 2 * dh, m->W_init, dh),
+         EpiStore{out_.S0 + (long long)i0 * dh, dh, m->b_init, 1, 0});
+    c.cls = cls;
+  }
+
+  // after every prepare() and every consumer of the prepared rows on c
+  void release(Ctx &c) {
+    if (mem_) AMUN_CUDA(cudaFreeAsync(mem_, c.st));
+    mem_ = nullptr;
+  }
+  void set_prep_ctas(int n) { prep_ctas_ = n; }
+
+ private:
+  cudaEvent_t new_event() {
+    cudaEvent_t e;
+    AMUN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    owned_.push_back(e);
+    return e;
+  }
+  const amun_model *m_;
+  AheadIn in_;
+  AheadOut out_;
+  cudaMemPool_t pool_;
+  void *mem_ = nullptr;
+  int T_ = 0, prep_ctas_ = 148;
+  int *d_len_ = nullptr, *d_e_of_i_ = nullptr;
+  long long *d_arow_ = nullptr;
+  float *Hsum_ = nullptr, *Hmean_ = nullptr;
+  std::vector<cudaEvent_t> evf_, evb_;
+  struct Owned {
+    std::vector<cudaEvent_t> v;
+    void push_back(cudaEvent_t e) { v.push_back(e); }
+    ~Owned() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } owned_;
+};
+
 // nnet.py:143-161 for R rows: query, attention (-> ctx into XS), GRU phase
 // A/B, deep output, logits (fused top-k partials or full logits).
 struct LogitOut {
@@ -479,9 +747,17 @@ void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
 }
 
 // one launch: tensor-core partials, DSMEM split reduction, fused epilogue
+// profiling knobs (outputs invalid): AMUN_DEBUG_SK_FLAGS / AMUN_DEBUG_LOGIT_FLAGS
+// skip parts of the decoder-step tensor-core kernels (gemm_sk.cuh SkArgs.debug,
+// logits_tc.cu debug_flags) to attribute the pass time
+int debug_env(const char *name) {
+  const char *e = getenv(name);
+  return e ? (int)strtol(e, nullptr, 0) : 0;
+}
 template <class Epi>
 void gemm_tc(Ctx &c, const SkMaps &maps, int M, int splits, const Epi &epi) {
-  c.run(c.cls, [&] { launch_gemm_sk(maps, M, splits, epi, c.st); });
+  static const int dbg = debug_env("AMUN_DEBUG_SK_FLAGS");
+  c.run(c.cls, [&] { launch_gemm_sk(maps, M, splits, epi, c.st, dbg); });
 }
 
 void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
@@ -559,6 +835,8 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     ta.vmask = lo.vmask;
     ta.mask_words = lo.mask_words;
     ta.rows_per_sent = rows_per_sent;
+    static const int ldbg = debug_env("AMUN_DEBUG_LOGIT_FLAGS");
+    ta.debug_flags = ldbg;
     c.run(AMUN_K_LOGIT, [&] { launch_logits_tc(*lo.tc, ta, c.st); });
     return;
   }
@@ -625,16 +903,6 @@ amun_result *flatten_hyps(const std::vector<std::vector<HostHyp>> &out_hyps, con
   return r;
 }
 
-template <class T>
-void h2d(Ctx &c, T *dst, const T *src, size_t n) {
-  if (n) AMUN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, c.st));
-  c.h2d += (int64_t)(n * sizeof(T));
-}
-template <class T>
-void d2h(Ctx &c, T *dst, const T *src, size_t n) {
-  if (n) AMUN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, c.st));
-  c.d2h += (int64_t)(n * sizeof(T));
-}
 
 }  // namespace
 
@@ -696,6 +964,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   const char *no_tce = getenv("AMUN_NO_TC_ENC");
   bool use_tce = !(no_tc && no_tc[0] == '1') && !(no_tce && no_tce[0] == '1');
   for (auto *m : ms) use_tce = use_tce && m->Uzr_hi;
+  // encode-ahead: the whole chunk's encoder before its buckets decode
+  // (tensor-core models); AMUN_NO_AHEAD=1 encodes per bucket in the lanes
+  const char *no_ahead = getenv("AMUN_NO_AHEAD");
+  bool ahead = use_tce && !(no_ahead && no_ahead[0] == '1');
+  for (auto *m : ms) ahead = ahead && m->Efa_hi[0];
   const int kk = std::min(k, V);
   const int ntiles = ceil_div(V, kBN);
 
@@ -835,8 +1108,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       Carver cv;
       cv.base = pass ? static_cast<char *>(L.mem) : nullptr;
       for (int m = 0; m < n_models; ++m) {
-        carve_enc(cv, L.eb[m], ms[m], Bmax, jmax_all);
-        if (use_tce) carve_enc_tc(cv, L.eb[m], ms[m], Bmax, jmax_all);
+        if (!ahead) {
+          carve_enc(cv, L.eb[m], ms[m], Bmax, jmax_all);
+          if (use_tce) carve_enc_tc(cv, L.eb[m], ms[m], Bmax, jmax_all);
+        }
         carve_dec(cv, L.db[m], ms[m], Rmax, jmax_all, !fused);
         if (!use_tc) L.db[m].T_hi = L.db[m].T_lo = nullptr;
         if (use_tcg) {
@@ -889,7 +1164,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     if (use_tcg)
       for (int m = 0; m < n_models; ++m) tc_step_maps(ms[m], L.db[m], Rmax, L.tsteps[m]);
-    if (use_tce)
+    if (use_tce && !ahead)
       for (int m = 0; m < n_models; ++m) tc_enc_maps(ms[m], L.eb[m], Bmax, jmax_all, L.tencs[m]);
     std::vector<const void *> hx(n_models), hs(n_models), he(n_models), h0(n_models), hl(n_models), hf(n_models),
         hxh(n_models), hxl(n_models);
@@ -942,17 +1217,35 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   }
   int64_t total_steps = 0;
   size_t next_bucket = 0;
+  // encode-ahead annotation stores of the current chunk (per model)
+  struct Store {
+    float *Hann = nullptr, *P = nullptr, *S0 = nullptr;
+    __half *Hah = nullptr, *Hal = nullptr;
+    void *mem = nullptr;
+  };
+  std::vector<Store> stores(n_models);
+  std::vector<std::unique_ptr<AheadEncoder>> encs(n_models);
+  std::vector<long long> bucket_row(buckets.size(), 0);  // store row of (bucket's first sentence, position 0)
+  int chunk_first = 0;  // sorted index of the chunk's first sentence
   // dispatch order: longest-running buckets first (step count x rows), so
   // the short ones fill the lanes at the end instead of a long bucket
   // running alone in the tail (bucket composition, hence every result, is
   // unchanged)
-  std::vector<int> dispatch(buckets.size());
-  std::iota(dispatch.begin(), dispatch.end(), 0);
-  std::stable_sort(dispatch.begin(), dispatch.end(), [&](int x, int y) {
-    const long long wx = (long long)buckets[x].cap_max * buckets[x].count * (buckets[x].jmax + 8);
-    const long long wy = (long long)buckets[y].cap_max * buckets[y].count * (buckets[y].jmax + 8);
-    return wx > wy;
-  });
+  std::vector<int> dispatch;
+  // dispatch order inside a chunk: longest-running buckets first (step
+  // count x rows), so the short ones fill the lanes at the end instead of a
+  // long bucket running alone in the tail (bucket composition, hence every
+  // result, is unchanged)
+  auto lpt_order = [&](int b0, int b1) {
+    std::vector<int> d(b1 - b0);
+    std::iota(d.begin(), d.end(), b0);
+    std::stable_sort(d.begin(), d.end(), [&](int x, int y) {
+      const long long wx = (long long)buckets[x].cap_max * buckets[x].count * (buckets[x].jmax + 8);
+      const long long wy = (long long)buckets[y].cap_max * buckets[y].count * (buckets[y].jmax + 8);
+      return wx > wy;
+    });
+    return d;
+  };
 
   auto launch_step = [&](Lane &L) {
     Ctx &c = *L.c;
@@ -1012,8 +1305,20 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       h2d(c, L.d_sl_off, slo.data(), B);
       h2d(c, L.d_sl_len, sll.data(), B);
     }
-    for (int m = 0; m < n_models; ++m)
-      encode_bucket(c, ms[m], L.eb[m], L.d_ids, L.d_len, B, jmax, use_tce ? &L.tencs[m] : nullptr);
+    if (ahead) {  // annotations and initial states from this chunk's store
+      std::vector<const float *> s0p(n_models);
+      for (int m = 0; m < n_models; ++m) {
+        encs[m]->prepare(c, bk.first - chunk_first, B, bucket_row[bi], (long long)B * jmax, jmax);
+        const int dh_m = ms[m]->d.d_h, da_m = ms[m]->d.d_att;
+        L.eb[m].Hann = stores[m].Hann + bucket_row[bi] * 2 * dh_m;
+        L.eb[m].P = stores[m].P + bucket_row[bi] * da_m;
+        s0p[m] = stores[m].S0 + (long long)(bk.first - chunk_first) * dh_m;
+      }
+      h2d(c, L.p_S0, s0p.data(), n_models);
+    } else {
+      for (int m = 0; m < n_models; ++m)
+        encode_bucket(c, ms[m], L.eb[m], L.d_ids, L.d_len, B, jmax, use_tce ? &L.tencs[m] : nullptr);
+    }
     L.bs.B = B;
     L.bs.k = k;
     L.bs.cap_max = L.capm;
@@ -1233,8 +1538,68 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
   };
 
+  // chunks of whole buckets: with encode-ahead, a chunk's encoder runs
+  // before its buckets decode (bounded annotation-store memory)
+  std::vector<std::pair<int, int>> chunks;
+  {
+    const char *ce = getenv("AMUN_ENC_CHUNK");  // read per call (tests vary it)
+    const int cap = ce ? std::max(1, atoi(ce)) : 16384;
+    const int nb = (int)buckets.size();
+    for (int b = 0; b < nb;) {
+      int e = b, cnt = 0;
+      while (e < nb && (e == b || !ahead || cnt + buckets[e].count <= cap)) cnt += buckets[e++].count;
+      chunks.emplace_back(b, e);
+      b = e;
+    }
+  }
+  for (const auto &ch : chunks) {
+  if (ahead) {
+    // store rows per bucket ([B][jmax] each), the chunk's sentences in
+    // sorted order, then the encoder of every model
+    chunk_first = buckets[ch.first].first;
+    long long rows = 0;
+    for (int bi = ch.first; bi < ch.second; ++bi) {
+      bucket_row[bi] = rows;
+      rows += (long long)buckets[bi].count * buckets[bi].jmax;
+    }
+    const int nc = buckets[ch.second - 1].first + buckets[ch.second - 1].count - chunk_first;
+    std::vector<int32_t> cids;
+    std::vector<long long> coff(nc), carow(nc);
+    std::vector<int32_t> clen(nc);
+    for (int bi = ch.first; bi < ch.second; ++bi)
+      for (int j = 0; j < buckets[bi].count; ++j) {
+        const int i = buckets[bi].first + j - chunk_first, s = order[buckets[bi].first + j];
+        coff[i] = (long long)cids.size();
+        clen[i] = src_len[s];
+        carow[i] = bucket_row[bi] + (long long)j * buckets[bi].jmax;
+        cids.insert(cids.end(), src_ids + off[s], src_ids + off[s + 1]);
+      }
+    Ctx &cf = *lanes[0]->c;
+    Ctx &cb = *lanes[n_lanes > 1 ? 1 : 0]->c;
+    for (int m = 0; m < n_models; ++m) {
+      const int dh_m = ms[m]->d.d_h, da_m = ms[m]->d.d_att;
+      Store &S = stores[m];
+      Carver cv;
+      for (int pass = 0; pass < 2; ++pass) {
+        cv = Carver{};
+        cv.base = static_cast<char *>(S.mem);
+        S.Hann = cv.take<float>((size_t)rows * 2 * dh_m);
+        S.P = cv.take<float>((size_t)rows * da_m);
+        S.S0 = cv.take<float>((size_t)nc * dh_m);
+        S.Hah = cv.take<__half>((size_t)rows * 2 * dh_m);
+        S.Hal = cv.take<__half>((size_t)rows * 2 * dh_m);
+        if (!pass) AMUN_CUDA(cudaMallocFromPoolAsync(&S.mem, cv.off, ws_pool(m0->device), cf.st));
+      }
+      AheadIn in{nc, cids.data(), coff.data(), clen.data(), carow.data(), rows};
+      encs[m].reset(new AheadEncoder(ms[m], in, AheadOut{S.Hann, S.P, S.S0, S.Hah, S.Hal}, ws_pool(m0->device)));
+      encs[m]->set_prep_ctas(enc_target_ctas());
+      encs[m]->run(cf, cb);
+    }
+  }
+  dispatch = lpt_order(ch.first, ch.second);
+  next_bucket = 0;
   for (auto &Lp : lanes)
-    if (next_bucket < buckets.size()) start_bucket(*Lp, dispatch[next_bucket++]);
+    if (next_bucket < dispatch.size()) start_bucket(*Lp, dispatch[next_bucket++]);
   for (;;) {
     bool any = false;
     for (auto &Lp : lanes) {
@@ -1244,7 +1609,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       poll(L, false);
       if (L.stop || L.t >= L.capm) {
         finish_bucket(L);
-        if (next_bucket < buckets.size()) start_bucket(L, dispatch[next_bucket++]);
+        if (next_bucket < dispatch.size()) start_bucket(L, dispatch[next_bucket++]);
         continue;
       }
       // bounded run-ahead past the newest probe the host has seen
@@ -1256,6 +1621,14 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     if (!any) break;
   }
+  if (ahead)  // every lane finished (and synchronised) this chunk's buckets
+    for (int m = 0; m < n_models; ++m) {
+      encs[m]->release(*lanes[0]->c);
+      encs[m].reset();
+      AMUN_CUDA(cudaFreeAsync(stores[m].mem, lanes[0]->st));
+      stores[m] = Store{};
+    }
+  }  // chunks
 
   for (int li = 1; li < n_lanes; ++li) {
     AMUN_CUDA(cudaEventRecord(lanes[li]->probe_ev[0], lanes[li]->st));
@@ -1522,7 +1895,7 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
 // p_out [B][jmax][d_att], s0_out [B][d_h].
 void hook_encode_batch(amun_model *m, const int32_t *ids, const int32_t *lens, int B, int jmax, bool production,
                        float *h_out, float *p_out, float *s0_out) {
-  if (production && !m->Uzr_hi)
+  if (production && !m->Efa_hi[0])
     throw Error(AMUN_ERR_UNSUPPORTED, "model dimensions / embedding range are outside the tensor-core path");
   AMUN_CUDA(cudaSetDevice(m->device));
   Ctx c(m->stream);
@@ -1538,11 +1911,21 @@ void hook_encode_batch(amun_model *m, const int32_t *ids, const int32_t *lens, i
     d_len = cv.take<int>(B);
     if (!pass) mem.alloc(cv.off, c.st);
   }
-  h2d(c, d_ids, ids, (size_t)B * jmax);
-  h2d(c, d_len, lens, B);
-  TcEnc te;
-  if (production) tc_enc_maps(m, e, B, jmax, te);
-  encode_bucket(c, m, e, d_ids, d_len, B, jmax, production ? &te : nullptr);
+  if (production) {
+    // the product path: encode-ahead over the B sentences (store = [B][jmax])
+    c.ws_pool = ws_pool(m->device);
+    std::vector<long long> off(B), arow(B);
+    for (int b = 0; b < B; ++b) off[b] = arow[b] = (long long)b * jmax;
+    AheadIn in{B, ids, off.data(), lens, arow.data(), (long long)B * jmax};
+    AheadEncoder enc(m, in, AheadOut{e.Hann, e.P, e.S0, e.Hah, e.Hal}, ws_pool(m->device));
+    enc.run(c, c);
+    enc.prepare(c, 0, B, 0, (long long)B * jmax, *std::max_element(lens, lens + B));
+    enc.release(c);
+  } else {
+    h2d(c, d_ids, ids, (size_t)B * jmax);
+    h2d(c, d_len, lens, B);
+    encode_bucket(c, m, e, d_ids, d_len, B, jmax, nullptr);
+  }
   const int dh = m->d.d_h, da = m->d.d_att;
   if (h_out) d2h(c, h_out, e.Hann, (size_t)B * jmax * 2 * dh);
   if (p_out) d2h(c, p_out, e.P, (size_t)B * jmax * da);

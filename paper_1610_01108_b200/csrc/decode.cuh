@@ -40,6 +40,12 @@ struct amun_model {
   __half *Watth_hi = nullptr, *Watth_lo = nullptr;  // [da, 2dh]
   __half *Wenc_hi = nullptr, *Wenc_lo = nullptr;    // [6dh, dep] input projection, both directions
   float us_ea = 1.f, us_eb = 1.f, us_p = 1.f, us_x = 1.f;
+  // encode-ahead recurrence (decode.cu encode_ahead): per direction the input
+  // projection fused into the recurrent GEMMs, K-major over the padded row
+  // [x (dep) | state (dh)]: phase A [W_z W_r ; U_z U_r] -> [2dh, dep + dh],
+  // phase B [W_h ; U_h] -> [dh, dep + dh]
+  __half *Efa_hi[2] = {}, *Efa_lo[2] = {}, *Efb_hi[2] = {}, *Efb_lo[2] = {};
+  float us_efa[2] = {1.f, 1.f}, us_efb[2] = {1.f, 1.f};
   int64_t bytes = 0;
   bool live = false;  // counted in the device's live-handle count (api.cu)
   std::vector<void *> allocs;

@@ -583,4 +583,93 @@ struct EpiLogitTopK {
   }
 };
 
+// ---- encode-ahead recurrence (decode.cu encode_ahead), tensor-core only.
+// Rows m are encoder rows (sentences in descending length order, all active
+// at this step); the accumulator already holds x_t W + h U (input projection
+// fused: the activation row is [x_t | state]).  nnet.py:66-70, 110-126.
+// Phase A: z = sigmoid(acc + b_z) -> Z;  r = sigmoid(acc + b_r), r * h -> split RH.
+struct EpiEncFA {
+  static constexpr bool kTile = false;
+  const float *bias;  // [2dh] (b_z | b_r)
+  const float *H;     // [n][dh] state
+  float *Z;           // [n][dh]
+  __half *RHh, *RHl;  // [n][dh]
+  int dh;
+  __device__ void operator()(int, int, float, int) const {}
+  struct Pre {
+    float4 b, hs;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    Pre p;
+    p.b = *reinterpret_cast<const float4 *>(bias + n);
+    p.hs = n >= dh ? *reinterpret_cast<const float4 *>(H + (long long)m * dh + n - dh) : make_float4(0, 0, 0, 0);
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    v.x += p.b.x;
+    v.y += p.b.y;
+    v.z += p.b.z;
+    v.w += p.b.w;
+    if (n < dh) {
+      *reinterpret_cast<float4 *>(Z + (long long)m * dh + n) =
+          make_float4(sigmoid_acc(v.x), sigmoid_acc(v.y), sigmoid_acc(v.z), sigmoid_acc(v.w));
+    } else {
+      const float4 rh = make_float4(sigmoid_acc(v.x) * p.hs.x, sigmoid_acc(v.y) * p.hs.y,
+                                    sigmoid_acc(v.z) * p.hs.z, sigmoid_acc(v.w) * p.hs.w);
+      store_split4(RHh, RHl, (long long)m * dh + n - dh, rh);
+    }
+  }
+};
+// Phase B: h~ = tanh(acc + b_h), h' = (1 - z) h + z h~ -> state (fp32 and
+// split), the annotation store row of (sentence, position) at column
+// dir*dh + n (fp32 and split, the precomp_att input), and the running sum
+// over positions for the initial-state mean (nnet.py:129).
+struct EpiEncFB {
+  static constexpr bool kTile = false;
+  const float *bias;  // [dh] b_h
+  float *H;           // [n][dh]
+  const float *Z;
+  __half *Hh, *Hl;    // [n][dh] next phase-A operand
+  float *Hann;        // store [rows][2dh]
+  __half *Hah, *Hal;
+  float *Hsum;        // [n][2dh]
+  const int *len;            // [n]
+  const long long *ann_row;  // [n] store row of position 0
+  int dh, t, dir;
+  __device__ void operator()(int, int, float, int) const {}
+  struct Pre {
+    float4 b, z, hs, sum;
+    int L;
+    long long ar;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    Pre p;
+    const long long o = (long long)m * dh + n;
+    p.b = *reinterpret_cast<const float4 *>(bias + n);
+    p.z = *reinterpret_cast<const float4 *>(Z + o);
+    p.hs = *reinterpret_cast<const float4 *>(H + o);
+    p.sum = t ? *reinterpret_cast<const float4 *>(Hsum + (long long)m * 2 * dh + dir * dh + n)
+              : make_float4(0, 0, 0, 0);
+    p.L = len[m];
+    p.ar = ann_row[m];
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    const long long o = (long long)m * dh + n;
+    float4 h;
+    h.x = (1.0f - p.z.x) * p.hs.x + p.z.x * tanhf(v.x + p.b.x);
+    h.y = (1.0f - p.z.y) * p.hs.y + p.z.y * tanhf(v.y + p.b.y);
+    h.z = (1.0f - p.z.z) * p.hs.z + p.z.z * tanhf(v.z + p.b.z);
+    h.w = (1.0f - p.z.w) * p.hs.w + p.z.w * tanhf(v.w + p.b.w);
+    *reinterpret_cast<float4 *>(H + o) = h;
+    store_split4(Hh, Hl, o, h);
+    const int pos = dir ? p.L - 1 - t : t;
+    const long long ao = (p.ar + pos) * 2 * dh + dir * dh + n;
+    *reinterpret_cast<float4 *>(Hann + ao) = h;
+    store_split4(Hah, Hal, ao, h);
+    *reinterpret_cast<float4 *>(Hsum + (long long)m * 2 * dh + dir * dh + n) =
+        make_float4(p.sum.x + h.x, p.sum.y + h.y, p.sum.z + h.z, p.sum.w + h.w);
+  }
+};
+
 }  // namespace amun

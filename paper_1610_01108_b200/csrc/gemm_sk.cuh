@@ -81,6 +81,7 @@ struct SkArgs {
   float unscale;  // 2^-(activation shift + weight shift)
   int n_klim, nk_lim;  // CTA pairs at features >= n_klim run only the first nk_lim K blocks
   int debug;  // microbenchmark knobs: 1 skip weight loads, 2 skip activation loads, 4 skip MMA, 8 skip reduction
+  int row_off1;  // first activation row of segment 1 (segment 2 and the epilogue rows start at 0)
 };
 
 // Row layout of one pass: one MMA of N0 columns, or two (N0 + N1) when the
@@ -153,11 +154,14 @@ __global__ void __launch_bounds__(C::kThreads, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  for (int pass = 0; pass < npass; ++pass) {
+  // row passes of this cluster: blockIdx.z, blockIdx.z + gridDim.z, ...
+  // (gridDim.z > 1 spreads the passes of a large-M launch over clusters)
+  int lp = 0;  // passes done by this CTA (ring and barrier phases)
+  for (int pass = blockIdx.z; pass < npass; pass += gridDim.z, ++lp) {
     const int row0 = pass * C::kPR;
     const int nr = min(C::kPR, a.M - row0);
     const SkPass ps(nr, CG);
-    const int it0 = pass * nkb;  // ring position of this pass's first k-block
+    const int it0 = lp * nkb;  // ring position of this pass's first k-block
     if (warp == 0) {
       if (lane == 0) {
         tc::fence_proxy_async();  // generic-proxy use of the buffers (reduction) before TMA refills them
@@ -191,8 +195,9 @@ __global__ void __launch_bounds__(C::kThreads, 1)
             for (int j = 0; j < ps.nsub; ++j) {
               const int g = row0 + (j ? ps.n[0] : 0) + member * ps.h[j];
               for (int r = 0; r < ps.h[j]; r += C::kBoxR, srow += C::kBoxR) {
-                load(st + 2 * C::kWBytes + srow * C::kRowBytes, mh, ka, g + r);
-                load(st + 2 * C::kWBytes + C::kXBytes + srow * C::kRowBytes, ml, ka, g + r);
+                const int gr = g + r + (seg2 ? 0 : a.row_off1);
+                load(st + 2 * C::kWBytes + srow * C::kRowBytes, mh, ka, gr);
+                load(st + 2 * C::kWBytes + C::kXBytes + srow * C::kRowBytes, ml, ka, gr);
               }
             }
           }
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(C::kThreads, 1)
       const int lg = warp & 3;
       const int f = lg * 32 + lane;
       if (nkb > 0) {
-        tc::mbar_wait(tfull, pass & 1);
+        tc::mbar_wait(tfull, lp & 1);
         tc::tc_fence_after();
       }
       const int ncol = ps.n[0] + ps.n[1];
@@ -344,13 +349,15 @@ __global__ void __launch_bounds__(C::kThreads, 1)
 // Rmax rows allocated; weight hi/lo: [N, Kb = k1 + k2] K-major.
 template <class C = SkDefault>
 SkMaps make_sk_maps(const __half *x1h, const __half *x1l, int k1, int lda1, const __half *x2h, const __half *x2l,
-                    int k2, int lda2, int Rmax, const __half *wh, const __half *wl, int N, int Kb, float unscale) {
+                    int k2, int lda2, int Rmax, const __half *wh, const __half *wl, int N, int Kb, float unscale,
+                    int Rmax2 = -1) {
   SkMaps m;
   m.x1h = make_tma_2d_f16(x1h, k1, Rmax, lda1, C::kBK, C::kBoxR);
   m.x1l = make_tma_2d_f16(x1l, k1, Rmax, lda1, C::kBK, C::kBoxR);
   if (x2h) {
-    m.x2h = make_tma_2d_f16(x2h, k2, Rmax, lda2, C::kBK, C::kBoxR);
-    m.x2l = make_tma_2d_f16(x2l, k2, Rmax, lda2, C::kBK, C::kBoxR);
+    if (Rmax2 < 0) Rmax2 = Rmax;
+    m.x2h = make_tma_2d_f16(x2h, k2, Rmax2, lda2, C::kBK, C::kBoxR);
+    m.x2l = make_tma_2d_f16(x2l, k2, Rmax2, lda2, C::kBK, C::kBoxR);
   } else {
     m.x2h = m.x1h;
     m.x2l = m.x1l;
@@ -377,7 +384,8 @@ int sk_splits(const SkMaps &m, int target_ctas) {
 }
 
 template <class C = SkDefault, class Epi>
-void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaStream_t st, int debug = 0) {
+void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaStream_t st, int debug = 0,
+                    int row_off1 = 0, int zgrid = 1) {
   if (M <= 0) return;
   SkArgs a{};
   a.M = M;
@@ -391,6 +399,8 @@ void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaS
   a.n_klim = maps.n_klim;
   a.nk_lim = maps.k_lim > 0 ? ceil_div(maps.k_lim, C::kBK) : a.nk1 + a.nk2;
   a.debug = debug;
+  a.row_off1 = row_off1;
+  zgrid = std::max(1, std::min(zgrid, ceil_div(M, C::kPR)));
   auto kern = gemm_sk_kernel<C, Epi>;
   static bool attr[64] = {};
   int dev = 0;
@@ -401,7 +411,7 @@ void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaS
     if (dev < 64) attr[dev] = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(C::kCG * splits, ceil_div(maps.N, 128 * C::kCG));
+  cfg.gridDim = dim3(C::kCG * splits, ceil_div(maps.N, 128 * C::kCG), zgrid);
   cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -412,7 +422,7 @@ void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaS
   la[0].val.clusterDim.z = 1;
   cfg.attrs = la;
   cfg.numAttrs = 1;
-  last_launch_ctas() = (int)(cfg.gridDim.x * cfg.gridDim.y);
+  last_launch_ctas() = (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
   AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, maps.wh, maps.wl, maps.x1h, maps.x1l, maps.x2h, maps.x2l, a, epi));
 }
 

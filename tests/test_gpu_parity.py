@@ -322,11 +322,12 @@ def test_fused_and_full_logit_paths_agree(gpu, full):
         assert abs(ha[1] - hb[1]) <= 1e-6 * abs(ha[1])
 
 
-@pytest.mark.parametrize("knob", ["AMUN_NO_TC_ENC", "AMUN_NO_TC_GEMM"])
+@pytest.mark.parametrize("knob", ["AMUN_NO_TC_ENC", "AMUN_NO_TC_GEMM", "AMUN_NO_AHEAD"])
 def test_tensor_core_encoder_and_step_gemms_match_cuda_core(gpu, full, monkeypatch, knob):
     """One tensor-core subsystem at a time swapped for its FP32 CUDA-core
     version (encoder: input projection, bi-GRU recurrence, precomp_att;
-    step: query / GRU / deep-output GEMMs): same tokens, scores within FP32
+    step: query / GRU / deep-output GEMMs), or the encode-ahead encoder for
+    the per-bucket tensor-core encoder: same tokens, scores within FP32
     rounding of each other."""
     s = golden_full()["sets"]["cfg2_strat64"]
     sub = dict(s, src=s["src"][:24])
@@ -446,3 +447,19 @@ def test_engine_two_workers_on_one_device(gpu, full):
     one = engine((0,)).translate_corpus(lines)
     two = engine((0, 0)).translate_corpus(lines)
     assert [(r.text, r.score, r.n_best) for r in one] == [(r.text, r.score, r.n_best) for r in two]
+
+
+def test_encode_ahead_chunking_is_byte_identical(gpu, full, monkeypatch):
+    """Encode-ahead over one chunk vs many small chunks (AMUN_ENC_CHUNK): the
+    encoder's split counts depend on the weight shape only, never on how
+    many sentences share a step GEMM, so every hypothesis is byte-identical
+    (the same argument makes 1/2/4/8-GPU shards identical)."""
+    from paper_1610_01108_b200 import workload as W
+
+    sents = W.WORKLOADS["cfg2"].corpus()[:150]
+    dm = _lib.device_model(full)
+    a = _lib.decode([dm], sents, 5, 2, 10, False, 2, max_batch=16)
+    monkeypatch.setenv("AMUN_ENC_CHUNK", "40")
+    b = _lib.decode([dm], sents, 5, 2, 10, False, 2, max_batch=16)
+    for i in range(len(sents)):
+        assert a.hyps(i) == b.hyps(i), i

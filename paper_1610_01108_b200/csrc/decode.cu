@@ -324,6 +324,20 @@ __global__ void gather_split_kernel(const float *__restrict__ E, const int *__re
   }
 }
 
+// Gathered shortlist columns: W_logit rows (fp16 hi/lo, K-major) and biases
+// of the bucket's shortlist union U (nnet.py:163 logit_rows[sl_ids]).
+__global__ void gather_logit_rows_kernel(const __half *__restrict__ whi, const __half *__restrict__ wlo,
+                                         const float *__restrict__ bias, int dep, const int *__restrict__ U,
+                                         __half *ghi, __half *glo, float *gb) {
+  const int j = blockIdx.x;
+  const long long src = (long long)U[j] * dep, dst = (long long)j * dep;
+  for (int c = threadIdx.x; c < dep; c += blockDim.x) {
+    ghi[dst + c] = whi[src + c];
+    glo[dst + c] = wlo[src + c];
+  }
+  if (threadIdx.x == 0) gb[j] = bias[U[j]];
+}
+
 // Tensor-core encoder GEMMs of one model: recurrence phase A / B over the
 // 2B block rows, and precomp_att over the split annotations; split counts
 // from (N, K) only.
@@ -705,6 +719,11 @@ struct LogitOut {
   const LogitTcMaps *tc = nullptr;  // tensor-core path when set
   const uint32_t *vmask = nullptr;  // per-sentence shortlist masks (tensor-core path)
   int mask_words = 0;
+  // gathered shortlist columns (tensor-core path): the bucket's union U of
+  // shortlist ids, its W_logit rows and biases; 0 / nullptr = full vocabulary
+  int n_vocab = 0;
+  const int *vid = nullptr;
+  const float *bias = nullptr;
 };
 
 // Tensor-core (3xTF32, swap-AB cluster split-K, gemm_sk.cuh) versions of the
@@ -831,7 +850,9 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
   }
   c.cls = AMUN_K_LOGIT;
   if (lo.tc) {
-    LogitTcArgs ta{R, V, de, m->b_logit, lo.kk, lo.ntiles, m->us_l, lo.pmax, lo.psum, lo.cval, lo.ctok};
+    LogitTcArgs ta{R, lo.n_vocab ? lo.n_vocab : V, de, lo.bias ? lo.bias : m->b_logit, lo.kk, lo.ntiles, m->us_l,
+                   lo.pmax, lo.psum, lo.cval, lo.ctok};
+    ta.vid = lo.vid;
     ta.vmask = lo.vmask;
     ta.mask_words = lo.mask_words;
     ta.rows_per_sent = rows_per_sent;
@@ -958,6 +979,13 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   const bool use_tc = fused && tc_logits;
   const bool use_mask = fused && sl_ids != nullptr;
   const int mask_words = ceil_div(V, 32);
+  // shortlist buckets whose union of ids is at most gather_cap wide run their
+  // logits over the gathered union (fewer weight bytes and MMAs per step);
+  // wider unions keep the full-vocabulary masked kernel
+  const char *gfe = getenv("AMUN_SL_GATHER_FRAC");
+  const double gfrac = gfe ? atof(gfe) : 0.9;
+  const int gather_cap = (use_mask && use_tc && gfrac > 0) ? std::min(V, (int)(gfrac * V)) : 0;
+  std::vector<int> gstamp(gather_cap > 0 ? V : 0, -1), gpos(gather_cap > 0 ? V : 0, 0);
   const char *no_tcg = getenv("AMUN_NO_TC_GEMM");
   bool use_tcg = !(no_tc && no_tc[0] == '1') && !(no_tcg && no_tcg[0] == '1');
   for (auto *m : ms) use_tcg = use_tcg && m->tc_gemm;
@@ -1024,6 +1052,12 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     std::vector<TcEnc> tencs;
     int *d_ids, *d_len, *d_cap, *d_sl, *d_sl_off, *d_sl_len;
     uint32_t *d_vmask = nullptr;  // [Bmax][mask_words] shortlist masks (fused path)
+    // gathered shortlist columns (buckets whose union U fits gather_cap)
+    int *d_U = nullptr;
+    __half *Wg_hi = nullptr, *Wg_lo = nullptr;
+    float *bg = nullptr;
+    uint32_t *d_vmask_g = nullptr;  // [Bmax][ceil(gather_cap / 32)] masks over U
+    LogitTcMaps tc_maps_g{};
     float *pmax, *psum, *cval;
     int *ctok, *cand_tok;
     double *cand_lp;
@@ -1124,6 +1158,13 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.d_cap = cv.take<int>(Bmax);
       L.d_sl = cv.take<int>(std::max(sl_max, 1));
       L.d_vmask = cv.take<uint32_t>(use_mask ? (size_t)Bmax * mask_words : 1);
+      if (gather_cap > 0) {
+        L.d_U = cv.take<int>(gather_cap);
+        L.Wg_hi = cv.take<__half>((size_t)gather_cap * m0->dep);
+        L.Wg_lo = cv.take<__half>((size_t)gather_cap * m0->dep);
+        L.bg = cv.take<float>(gather_cap);
+        L.d_vmask_g = cv.take<uint32_t>((size_t)Bmax * ceil_div(gather_cap, 32));
+      }
       L.d_sl_off = cv.take<int>(Bmax);
       L.d_sl_len = cv.take<int>(Bmax);
       L.pmax = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
@@ -1291,14 +1332,53 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     h2d(c, L.d_ids, ids.data(), ids.size());
     h2d(c, L.d_len, lens.data(), B);
     h2d(c, L.d_cap, caps.data(), B);
+    int n_gath = 0;  // > 0: this bucket's logits run over its shortlist union only
     if (use_mask) {
-      std::vector<uint32_t> mask((size_t)B * mask_words, 0u);
-      for (int i = 0; i < B; ++i)
-        for (int e = slo[i]; e < slo[i] + sll[i]; ++e) {
+      // union U of the bucket's shortlists (ascending); when it is small
+      // enough, gather its W_logit rows once per bucket so every step's
+      // logit GEMM has N = |U| instead of V (nnet.py:162-163 per sentence;
+      // here per bucket, each sentence masked to its own list inside U)
+      std::vector<int> U;
+      if (gather_cap > 0) {
+        for (int e = 0; e < (int)slv.size(); ++e) {
           const int v = slv[e];
-          mask[(size_t)i * mask_words + v / 32] |= 1u << (v % 32);
+          if (gstamp[v] != bi) {
+            gstamp[v] = bi;
+            U.push_back(v);
+          }
         }
-      h2d(c, L.d_vmask, mask.data(), mask.size());
+        if ((int)U.size() <= gather_cap) {
+          std::sort(U.begin(), U.end());
+          n_gath = (int)U.size();
+        }
+      }
+      if (n_gath) {
+        for (int j = 0; j < n_gath; ++j) gpos[U[j]] = j;
+        const int words = ceil_div(n_gath, 32);
+        std::vector<uint32_t> mask((size_t)B * words, 0u);
+        for (int i = 0; i < B; ++i)
+          for (int e = slo[i]; e < slo[i] + sll[i]; ++e) {
+            const int v = gpos[slv[e]];
+            mask[(size_t)i * words + v / 32] |= 1u << (v % 32);
+          }
+        h2d(c, L.d_vmask_g, mask.data(), mask.size());
+        h2d(c, L.d_U, U.data(), U.size());
+        c.run(AMUN_K_LOGIT, [&] {
+          gather_logit_rows_kernel<<<n_gath, 128, 0, c.st>>>(m0->Wl_hi, m0->Wl_lo, m0->b_logit, m0->dep, L.d_U,
+                                                              L.Wg_hi, L.Wg_lo, L.bg);
+          AMUN_CHECK_LAUNCH();
+        });
+        L.tc_maps_g = make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, L.Wg_hi, L.Wg_lo, m0->dep,
+                                      n_gath);
+      } else {
+        std::vector<uint32_t> mask((size_t)B * mask_words, 0u);
+        for (int i = 0; i < B; ++i)
+          for (int e = slo[i]; e < slo[i] + sll[i]; ++e) {
+            const int v = slv[e];
+            mask[(size_t)i * mask_words + v / 32] |= 1u << (v % 32);
+          }
+        h2d(c, L.d_vmask, mask.data(), mask.size());
+      }
     }
     if (sl_ids) {
       h2d(c, L.d_sl, slv.data(), slv.size());
@@ -1341,6 +1421,15 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.lo.mask_words = mask_words;
     }
     if (use_tc) L.lo.tc = &L.tc_maps;
+    if (n_gath) {
+      L.lo.tc = &L.tc_maps_g;
+      L.lo.vmask = L.d_vmask_g;
+      L.lo.mask_words = ceil_div(n_gath, 32);
+      L.lo.n_vocab = n_gath;
+      L.lo.vid = L.d_U;
+      L.lo.bias = L.bg;
+      L.lo.ntiles = ceil_div(n_gath, kBN);
+    }
     SelectArgs &sa = L.sa;
     sa = SelectArgs{};
     sa.kk = kk;
@@ -1350,7 +1439,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     sa.psum = L.psum;
     sa.cval = L.cval;
     sa.ctok = L.ctok;
-    sa.ntiles = ntiles;
+    sa.ntiles = L.lo.ntiles;
     sa.M = L.R;
     sa.L = L.p_L;
     sa.ldl = V;

@@ -303,25 +303,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           float *dst = buf + lg * kTrQ + lane;
 #pragma unroll
           for (int i = 0; i < 32; ++i) dst[i * kTrRow] = fmaf(v[i], a.unscale, bias_f);
-          if (a.vmask) {  // shortlist: tokens outside the sentence's list never exist
-            const int vv = v0 + f;
-            const int m0 = un.row0 + c0;
-            int sent = m0 / a.rows_per_sent, rem = m0 - sent * a.rows_per_sent;
-            const uint32_t *mw = a.vmask + (vv >> 5);
-            const int nrow = min(32, a.M - m0);
-            uint32_t w = (vv < a.N && nrow > 0) ? __ldg(mw + (long long)sent * a.mask_words) : ~0u;
-            const uint32_t bit = 1u << (vv & 31);
-#pragma unroll 1
-            for (int i = 0; i < nrow; ++i) {  // one mask word per sentence (beam rows share it)
-              if (rem == a.rows_per_sent) {
-                ++sent;
-                rem = 0;
-                w = vv < a.N ? __ldg(mw + (long long)sent * a.mask_words) : ~0u;
-              }
-              if (!(w & bit)) dst[i * kTrRow] = -INFINITY;
-              ++rem;
-            }
-          }
         }
         stamp(1);
         asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
@@ -338,6 +319,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[4 * u4 + 1] = t4.y;
             x[4 * u4 + 2] = t4.z;
             x[4 * u4 + 3] = t4.w;
+          }
+          // shortlist (nnet.py:160-163): columns outside the row's sentence
+          // list do not exist; the thread's 32 columns are one mask word
+          uint32_t allow = ~0u;
+          if (a.vmask) {
+            const int mrow = un.row0 + c0 + ri, vq = v0 + q * 32;
+            allow = (mrow < a.M && vq < a.N)
+                        ? __ldg(a.vmask + (long long)(mrow / a.rows_per_sent) * a.mask_words + (vq >> 5))
+                        : 0u;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = (allow >> i) & 1u ? x[i] : -INFINITY;
           }
           // four 8-wide group maxima, the two 16-wide half maxima, the
           // quarter max, and sum exp(x - max) (ex2-based: x log2 e - max
@@ -406,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           unsigned cand = 0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) cand |= (x[i] >= thr ? 1u : 0u) << i;
+          cand &= allow;  // masked columns are -inf here but not in the smem copy
           stamp(6);
           RowTop<KK> top;
           top.init();
@@ -439,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (i < a.kk) {
                 const bool ok = top.v[i] != -INFINITY;
                 a.cval[base + i] = ok ? top.v[i] : -INFINITY;
-                a.ctok[base + i] = ok ? top.t[i] : -1;
+                a.ctok[base + i] = ok ? (a.vid ? __ldg(a.vid + top.t[i]) : top.t[i]) : -1;
               }
           }
         }

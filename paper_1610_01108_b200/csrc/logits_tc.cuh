@@ -19,6 +19,9 @@ struct LogitTcArgs {
   // bit v of vmask[(row / rows_per_sent) * mask_words + v / 32] allows token v
   const uint32_t *vmask = nullptr;
   int mask_words = 0, rows_per_sent = 1;
+  // optional column -> vocabulary id map (gathered shortlist columns, strictly
+  // ascending): candidate tokens are reported as vid[column]
+  const int *vid = nullptr;
   int debug_flags = 0;  // microbenchmark knobs: 1 skip A loads, 2 skip B loads, 4 skip MMA, 8 skip epilogue
   long long *debug_clock = nullptr;  // microbenchmark: per-chunk clock64 stamps of CTA 0
 };

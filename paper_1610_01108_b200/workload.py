@@ -10,6 +10,15 @@ drawn for all sentences first, then ids uniform in [2, v_src) per sentence
   cfg3  cfg2 sharded over 2/4/8 GPUs
   cfg4  512 sentences, J = 100, beam 12, cap = 1 * J + 0 = 100
   cfg5  cfg2 set, beam 1, buckets of 512
+
+Shortlist workloads use a synthetic lexical table:
+target frequency ranks are a fixed permutation of [2, v_trg); each source
+id's translations, best first, are distinct ranks drawn log-uniformly (so
+frequent targets recur across sources, as in a real table), probabilities
+1/(j + 2) for the j-th.  A sentence's shortlist is the reference's
+build_shortlist set (shortlist.py:128-147): {0, 1} U the K most frequent
+targets U the K' best translations of each source token, K = K' = 75 (the
+EngineConfig defaults, engine.py:40-41).
 """
 
 from __future__ import annotations
@@ -60,3 +69,52 @@ WORKLOADS = {
 
 def lines_of(sentences: list[list[int]]) -> list[str]:
     return [" ".join(f"w{i}" for i in s) for s in sentences]
+
+
+# ---------------------------------------------------------------- shortlists
+
+LEX_SEED = 1610
+SL_K = SL_KPRIME = 75
+LEX_ENTRIES = 100  # translations per source id in the synthetic table
+
+
+def target_by_rank(v_trg: int = V_TRG) -> np.ndarray:
+    """Target ids in descending frequency (the frequency list)."""
+    return np.random.default_rng(LEX_SEED).permutation(np.arange(2, v_trg))
+
+
+def lex_translations(src_id: int, v_trg: int = V_TRG, n: int = LEX_ENTRIES,
+                     by_rank: np.ndarray | None = None) -> np.ndarray:
+    """Target ids of source id `src_id`'s table entries, best first."""
+    if by_rank is None:
+        by_rank = target_by_rank(v_trg)
+    rng = np.random.default_rng((LEX_SEED, int(src_id)))
+    ranks: list[int] = []
+    seen: set[int] = set()
+    while len(ranks) < n:
+        for r in (np.exp(rng.random(2 * n) * np.log(v_trg - 2)).astype(np.int64) - 1):
+            r = int(min(max(r, 0), v_trg - 3))
+            if r not in seen:
+                seen.add(r)
+                ranks.append(r)
+                if len(ranks) == n:
+                    break
+    return by_rank[np.asarray(ranks)]
+
+
+def shortlists(sentences: list[list[int]], K: int = SL_K, Kprime: int = SL_KPRIME,
+               v_trg: int = V_TRG) -> list[np.ndarray]:
+    """Per-sentence ascending shortlist ids (int32), build_shortlist semantics."""
+    by_rank = target_by_rank(v_trg)
+    base = set(int(i) for i in by_rank[:K]) | {0, 1}
+    cache: dict[int, np.ndarray] = {}
+    out = []
+    for s in sentences:
+        ids = set(base)
+        for tok in s:
+            tr = cache.get(tok)
+            if tr is None:
+                tr = cache[tok] = lex_translations(tok, v_trg, by_rank=by_rank)[:Kprime]
+            ids.update(int(i) for i in tr)
+        out.append(np.array(sorted(ids), dtype=np.int32))
+    return out

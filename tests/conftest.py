@@ -63,6 +63,13 @@ def golden_fullset(name: str) -> dict:
         return {k: z[k] for k in z.files}
 
 
+@lru_cache(maxsize=1)
+def golden_shortlist() -> dict:
+    """Reference shortlist decodes (make_golden_shortlist.py)."""
+    with np.load(GOLDEN / "shortlist_sets.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
 def fullset_src_sha(corpus) -> str:
     import hashlib
 

@@ -201,15 +201,20 @@ def _first_divergence(got, want) -> int:
 
 
 def _adjudicate(name, gold_hyps, gaps, out, score_rtol=SCORE_RTOL_FULL):
-    """Token identity per sentence, except documented near ties: a sentence
-    whose 1-best first differs from the reference's at token d is excused
-    only if the reference's k-th vs (k+1)-th candidate gap was < TAU at some
-    step <= d (the beams must have diverged no later than step d, so the
-    window [0, d] bounds the first divergent step; a near tie later in the
-    sentence excuses nothing), or if the two best final hypotheses are
-    within TAU (final-ranking tie).  Exact sentences must match the score
-    to score_rtol."""
-    exact, ties, fails, worst = 0, [], [], 0.0
+    """Token identity per sentence, except documented near ties.
+
+    A sentence whose 1-best first differs from the reference's at token d is
+    excused only if, at some search step <= d (the beams must have diverged
+    no later than step d; a near tie later in the sentence excuses nothing),
+    the reference's k-th vs (k+1)-th candidate gap was below the accumulated
+    score error of two hypotheses after that many steps: tau(d) =
+    max(TAU, 2 * eps * (d + 1)), where eps is the largest per-step score
+    error measured on this run's token-identical sentences (|score -
+    reference| / steps; fp32-equivalent arithmetic vs the reference's f64
+    drifts ~1e-5 per step, dominated by the fp32 GRU state).  A final-ranking
+    tie (two best hypotheses within tau) is excused likewise.  Exact
+    sentences must match the score to score_rtol."""
+    exact, ties, fails, worst, eps = 0, [], [], 0.0, 0.0
     for i, (gtoks, gscore) in enumerate(gold_hyps):
         hyps = out.hyps(i)
         toks, score = hyps[0][0], hyps[0][1]
@@ -217,16 +222,23 @@ def _adjudicate(name, gold_hyps, gaps, out, score_rtol=SCORE_RTOL_FULL):
             exact += 1
             rel = abs(score - gscore) / max(1.0, abs(gscore))
             worst = max(worst, rel)
+            eps = max(eps, abs(score - gscore) / max(1, len(gtoks)))
             assert rel <= score_rtol, (name, i, score, gscore)
+    for i, (gtoks, gscore) in enumerate(gold_hyps):
+        hyps = out.hyps(i)
+        toks = hyps[0][0]
+        if toks == gtoks:
             continue
         d = _first_divergence(toks, gtoks)
+        tau = max(TAU, 2.0 * eps * (d + 1))
         g = np.asarray(gaps[i][: d + 1], np.float64)
         gap_d = float(g.min()) if g.size else np.inf
         final_gap = abs(hyps[0][1] - hyps[1][1]) if len(hyps) > 1 else np.inf
-        (ties if min(gap_d, final_gap) < TAU else fails).append((i, d, gap_d, final_gap))
+        (ties if min(gap_d, final_gap) < tau else fails).append((i, d, gap_d, round(tau, 7), final_gap))
     n = len(gold_hyps)
     summary = (f"{name}: {exact}/{n} token-identical, {len(ties)} near-tie exceptions {ties}, "
-               f"{len(fails)} unexplained {fails[:10]}; max score rel err {worst:.2e}")
+               f"{len(fails)} unexplained {fails[:10]}; max score rel err {worst:.2e}, "
+               f"per-step score error eps {eps:.2e}")
     print("\n" + summary)
     assert not fails, summary
     assert len(ties) <= max(1, n // 100), summary  # expect 0.1-0.3% near-tie exceptions
@@ -411,7 +423,7 @@ def test_beam12_long_sentences_tensor_core_vs_cuda_core(gpu, full, monkeypatch):
         assert abs(ha[1] - hb[1]) <= 1e-5 * abs(hb[1]), (i, ha[1], hb[1])
 
 
-def test_shortlist_batch_composition_invariance(gpu, full):
+def test_shortlist_batch_composition_invariance(gpu, full, monkeypatch):
     """Masked fused logits: a sentence's result does not depend on its
     bucket-mates or the bucket size."""
     s = golden_full()["sets"]["cfg1"]
@@ -420,6 +432,16 @@ def test_shortlist_batch_composition_invariance(gpu, full):
     sls = [np.unique(np.concatenate([[0], rng.choice(np.arange(2, 30000), 999, replace=False)])).astype(np.int32)
            for _ in src]
     dm = _lib.device_model(full)
+    a = _lib.decode([dm], src, 5, 2, 10, False, 1, shortlists=sls, max_batch=64)
+    b = _lib.decode([dm], src, 5, 2, 10, False, 1, shortlists=sls, max_batch=3)
+    for i in range(len(src)):
+        # buckets gather their shortlist union, so the log-normaliser's
+        # per-tile grouping (fp32 partials) follows the bucket: tokens are
+        # identical, scores agree to fp32 rounding
+        ha, hb = a.hyps(i)[0], b.hyps(i)[0]
+        assert ha[0] == hb[0], i
+        assert abs(ha[1] - hb[1]) <= 1e-6 * abs(hb[1]), (i, ha[1], hb[1])
+    monkeypatch.setenv("AMUN_SL_GATHER_FRAC", "0")  # full-vocabulary masked kernel: byte-identical
     a = _lib.decode([dm], src, 5, 2, 10, False, 1, shortlists=sls, max_batch=64)
     b = _lib.decode([dm], src, 5, 2, 10, False, 1, shortlists=sls, max_batch=3)
     for i in range(len(src)):
@@ -463,3 +485,29 @@ def test_encode_ahead_chunking_is_byte_identical(gpu, full, monkeypatch):
     b = _lib.decode([dm], sents, 5, 2, 10, False, 2, max_batch=16)
     for i in range(len(sents)):
         assert a.hyps(i) == b.hyps(i), i
+
+
+@pytest.mark.parametrize("name,max_batch", [("cfg1", 1), ("cfg1", 64), ("cfg2", 64)])
+def test_shortlist_decode_matches_reference(gpu, full, name, max_batch):
+    """Shortlist decodes (nnet.py:160-163, search.py:146-148) against the
+    reference's own beam_search with its build_shortlist lists over the
+    synthetic lexical table (tests/golden/make_golden_shortlist.py): the
+    gathered-union logit path (batch 1: the sentence's own list; buckets:
+    the union with per-sentence masks) and, for wide unions, the masked
+    full-vocabulary kernel."""
+    from conftest import golden_shortlist
+    from paper_1610_01108_b200 import workload as W
+
+    g = golden_shortlist()
+    corpus = W.WORKLOADS[name].corpus()
+    sents = [corpus[i] for i in g[f"{name}_idx"]]
+    sls = W.shortlists(sents)
+    beam, f, o, _, _ = (int(x) for x in g[f"{name}_opts"])
+    out = _lib.decode([_lib.device_model(full)], sents, beam, f, o, False, 2, shortlists=sls, max_batch=max_batch)
+    toff, goff = g[f"{name}_tok_off"], g[f"{name}_gap_off"]
+    gold = [(g[f"{name}_tokens"][toff[i]:toff[i + 1]].astype(int).tolist(), float(g[f"{name}_score"][i]))
+            for i in range(len(sents))]
+    gaps = [g[f"{name}_gap"][goff[i]:goff[i + 1]] for i in range(len(sents))]
+    _adjudicate(f"shortlist {name} batch {max_batch}", gold, gaps, out)
+    for i in range(len(sents)):
+        assert set(out.hyps(i)[0][0]) <= set(sls[i].tolist())

@@ -781,7 +781,7 @@ void gemm_tc(Ctx &c, const SkMaps &maps, int M, int splits, const Epi &epi) {
 
 void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
                int R, int rows_per_sent, const int *n_act, const int *done, float *alpha, const LogitOut &lo,
-               const TcStep *ts = nullptr) {
+               const TcStep *ts = nullptr, bool do_logits = true) {
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
   const int s_off = de + 2 * dh;
   c.cls = AMUN_K_QUERY;
@@ -848,6 +848,7 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
       gemm(c, g, e);
     }
   }
+  if (!do_logits) return;  // ensemble members: one fused logit launch for all of them
   c.cls = AMUN_K_LOGIT;
   if (lo.tc) {
     LogitTcArgs ta{R, lo.n_vocab ? lo.n_vocab : V, de, lo.bias ? lo.bias : m->b_logit, lo.kk, lo.ntiles, m->us_l,
@@ -975,7 +976,13 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   const bool tc_logits = m0->Wl_hi && !(no_tc && no_tc[0] == '1');
   // shortlists ride the fused tensor-core logit kernel as per-sentence
   // vocabulary masks; the CUDA-core fused kernel has no mask (full logits)
-  const bool fused = n_models == 1 && (!sl_ids || tc_logits) && k <= kMaxRowCand && !o.force_full_logits;
+  // ensembles of up to kLogitMembers tensor-core members run one fused
+  // logit launch for all members (member-sum candidates + per-member
+  // log-softmax partials); larger ensembles take the full-logit path
+  bool ens_tc = n_models > 1 && n_models <= kLogitMembers && tc_logits;
+  for (auto *m : ms) ens_tc = ens_tc && m->Wl_hi;
+  const bool fused = (n_models == 1 || ens_tc) && (!sl_ids || tc_logits) && k <= kMaxRowCand && !o.force_full_logits;
+  const bool ens_fused = fused && n_models > 1;
   const bool use_tc = fused && tc_logits;
   const bool use_mask = fused && sl_ids != nullptr;
   const int mask_words = ceil_div(V, 32);
@@ -984,7 +991,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // wider unions keep the full-vocabulary masked kernel
   const char *gfe = getenv("AMUN_SL_GATHER_FRAC");
   const double gfrac = gfe ? atof(gfe) : 0.9;
-  const int gather_cap = (use_mask && use_tc && gfrac > 0) ? std::min(V, (int)(gfrac * V)) : 0;
+  const int gather_cap = (use_mask && use_tc && gfrac > 0 && n_models == 1) ? std::min(V, (int)(gfrac * V)) : 0;
   std::vector<int> gstamp(gather_cap > 0 ? V : 0, -1), gpos(gather_cap > 0 ? V : 0, 0);
   const char *no_tcg = getenv("AMUN_NO_TC_GEMM");
   bool use_tcg = !(no_tc && no_tc[0] == '1') && !(no_tcg && no_tcg[0] == '1');
@@ -1067,6 +1074,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     float **p_fin;
     __half **p_XSh, **p_XSl;
     LogitTcMaps tc_maps{};
+    std::vector<LogitTcMaps> tc_maps_ens;  // fused ensemble logits: one map set per member
     LaneRes *res = nullptr;  // pooled stream / workspace / probe ring
     int dev = 0;
     void *mem = nullptr;
@@ -1167,8 +1175,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       }
       L.d_sl_off = cv.take<int>(Bmax);
       L.d_sl_len = cv.take<int>(Bmax);
-      L.pmax = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
-      L.psum = cv.take<float>(fused ? (size_t)ntiles * Rmax : 1);
+      L.pmax = cv.take<float>(fused ? (size_t)ntiles * Rmax * n_models : 1);
+      L.psum = cv.take<float>(fused ? (size_t)ntiles * Rmax * n_models : 1);
       L.cval = cv.take<float>(fused ? (size_t)Rmax * ntiles * kk : 1);
       L.ctok = cv.take<int>(fused ? (size_t)Rmax * ntiles * kk : 1);
       L.cand_lp = cv.take<double>((size_t)Rmax * kk);
@@ -1202,6 +1210,12 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
       if (logits_tc_tile_n() != kBN) throw Error(AMUN_ERR_UNSUPPORTED, "logit tile width mismatch");
       L.tc_maps = make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, m0->Wl_hi, m0->Wl_lo, m0->dep, V);
+      if (ens_fused) {
+        L.tc_maps_ens.resize(n_models);
+        for (int m = 0; m < n_models; ++m)
+          L.tc_maps_ens[m] = make_logit_maps(L.db[m].T_hi, L.db[m].T_lo, Rmax, ms[m]->d.d_emb, ms[m]->dep,
+                                             ms[m]->Wl_hi, ms[m]->Wl_lo, ms[m]->dep, V);
+      }
     }
     if (use_tcg)
       for (int m = 0; m < n_models; ++m) tc_step_maps(ms[m], L.db[m], Rmax, L.tsteps[m]);
@@ -1292,7 +1306,23 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     Ctx &c = *L.c;
     for (int m = 0; m < n_models; ++m)
       step_rows(c, ms[m], L.db[m], L.eb[m], L.d_len, L.jmax, L.R, k, L.bs.n_act, L.bs.done, nullptr, L.lo,
-                use_tcg ? &L.tsteps[m] : nullptr);
+                use_tcg ? &L.tsteps[m] : nullptr, !ens_fused);
+    if (ens_fused) {  // every member's logits in one launch (search.py:56-72)
+      LogitTcArgs ta{L.R, V, ms[0]->d.d_emb, ms[0]->b_logit, kk, ntiles, ms[0]->us_l,
+                     L.pmax, L.psum, L.cval, L.ctok};
+      ta.nm = n_models;
+      for (int m = 1; m < n_models; ++m) {
+        ta.K_x[m - 1] = ms[m]->d.d_emb;
+        ta.bias_x[m - 1] = ms[m]->b_logit;
+        ta.unscale_x[m - 1] = ms[m]->us_l;
+      }
+      ta.pm_stride = (long long)Rmax * ntiles;
+      ta.vmask = L.lo.vmask;
+      ta.mask_words = L.lo.mask_words;
+      ta.rows_per_sent = k;
+      c.cls = AMUN_K_LOGIT;
+      c.run(AMUN_K_LOGIT, [&] { launch_logits_tc_ens(L.tc_maps_ens.data(), ta, L.st); });
+    }
     c.run(AMUN_K_SELECT, [&] { launch_select(L.sa, L.bs, L.mr, L.st); });
   };
 
@@ -1441,6 +1471,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     sa.ctok = L.ctok;
     sa.ntiles = L.lo.ntiles;
     sa.M = L.R;
+    sa.nm_fused = ens_fused ? n_models : 1;
+    sa.pm_stride = (long long)Rmax * ntiles;
     sa.L = L.p_L;
     sa.ldl = V;
     sa.sl_ids = sl_ids ? L.d_sl : nullptr;

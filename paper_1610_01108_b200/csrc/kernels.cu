@@ -768,38 +768,47 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     double *out_lp = c_lp + (size_t)i * kk;
     int *out_tok = c_tok + (size_t)i * kk;
     if constexpr (FUSED) {
-      // per-tile partial (max, sum) pairs, kept in registers (<= 8 per lane)
+      // per-tile partial (max, sum) pairs, kept in registers (<= 8 per lane);
+      // ensembles fused in the logit kernel: one set per member, and the
+      // candidates carry the member sum of the logits, so the ensemble
+      // log-prob mean_m(logit_m - lse_m) (search.py:67-72) is
+      // (sum_m logit_m - sum_m lse_m) / nm
       constexpr int kPT = 8;
-      float pm[kPT], ps[kPT];
-      float mx = -INFINITY;
+      double lse = 0.0;
+      for (int mi = 0; mi < sa.nm_fused; ++mi) {
+        const float *pmax = sa.pmax + mi * sa.pm_stride, *psum = sa.psum + mi * sa.pm_stride;
+        float pm[kPT], ps[kPT];
+        float mx = -INFINITY;
 #pragma unroll
-      for (int u = 0; u < kPT; ++u) {
-        const int tt = lane + 32 * u;
-        const bool ok = tt < sa.ntiles;
-        pm[u] = ok ? sa.pmax[(long long)r * sa.ntiles + tt] : -INFINITY;
-        ps[u] = ok ? sa.psum[(long long)r * sa.ntiles + tt] : 0.f;
+        for (int u = 0; u < kPT; ++u) {
+          const int tt = lane + 32 * u;
+          const bool ok = tt < sa.ntiles;
+          pm[u] = ok ? pmax[(long long)r * sa.ntiles + tt] : -INFINITY;
+          ps[u] = ok ? psum[(long long)r * sa.ntiles + tt] : 0.f;
+        }
+        for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, pmax[(long long)r * sa.ntiles + tt]);
+#pragma unroll
+        for (int u = 0; u < kPT; ++u) mx = fmaxf(mx, pm[u]);
+        mx = warp_max(mx);
+        // exp(pm - mx) <= 1 in fp32 (1-ulp expf), products summed in f64
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < kPT; ++u) s += (double)(ps[u] * expf(pm[u] - mx));
+        for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) {
+          long long o = (long long)r * sa.ntiles + tt;
+          s += (double)(psum[o] * expf(pmax[o] - mx));
+        }
+        s = warp_sum_d(s);
+        lse += (double)mx + log(s);
       }
-      for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, sa.pmax[(long long)r * sa.ntiles + tt]);
-#pragma unroll
-      for (int u = 0; u < kPT; ++u) mx = fmaxf(mx, pm[u]);
-      mx = warp_max(mx);
-      // exp(pm - mx) <= 1 in fp32 (1-ulp expf), products summed in f64
-      double s = 0.0;
-#pragma unroll
-      for (int u = 0; u < kPT; ++u) s += (double)(ps[u] * expf(pm[u] - mx));
-      for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) {
-        long long o = (long long)r * sa.ntiles + tt;
-        s += (double)(sa.psum[o] * expf(sa.pmax[o] - mx));
-      }
-      s = warp_sum_d(s);
-      const double lse = (double)mx + log(s);
       const int n = sa.ntiles * kk;
       const float *cv = sa.cval + (long long)r * n;
       const int *ct = sa.ctok + (long long)r * n;
       auto emit = [&](int j, const Key &bk) {
         if (lane == 0) {
           bool none = bk.tok == kNoTok;
-          out_lp[j] = none ? -INFINITY : bk.v - lse;  // ordering by logit == by logit - lse
+          // ordering by logit == by logit - lse
+          out_lp[j] = none ? -INFINITY : (sa.nm_fused == 1 ? bk.v - lse : (bk.v - lse) / sa.nm_fused);
           out_tok[j] = none ? -1 : bk.tok;
         }
       };

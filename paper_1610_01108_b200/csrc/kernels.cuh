@@ -88,6 +88,10 @@ struct SelectArgs {
   const float *pmax, *psum, *cval;
   const int *ctok;
   int ntiles, M;
+  // ensembles fused in the logit kernel: members' (max, sum) partial sets at
+  // pmax / psum + m * pm_stride; cval holds the member sum of the logits
+  int nm_fused = 1;
+  long long pm_stride = 0;
   // full-mode inputs: logits per model [R][ldl]
   const float *const *L;
   int ldl;

@@ -139,24 +139,32 @@ __device__ __forceinline__ void merge_partner(RowTop<KK> &top, int lane_xor) {
   }
 }
 
+// Hypothesis rows per work unit: the nm members' accumulators of one unit
+// share a 256-column TMEM buffer (member m at column m * rows).
+__host__ __device__ constexpr int unit_rows(int nm) { return nm <= 1 ? kUnitRows : nm == 2 ? 128 : 64; }
+
 // Work unit u of a launch: 256-vocab tile vt, rows [row0, row0 + nr); the
 // pair's MMA has N = nr rounded up to 32, each CTA stages N / 2 of the rows.
 struct Unit {
   int vt, row0, nr, n, h;
-  __device__ __forceinline__ Unit(int u, int npass, int M) {
+  __device__ __forceinline__ Unit(int u, int npass, int M, int ur) {
     vt = u / npass;
-    row0 = (u % npass) * kUnitRows;
-    nr = min(kUnitRows, M - row0);
+    row0 = (u % npass) * ur;
+    nr = min(ur, M - row0);
     n = (nr + 31) / 32 * 32;
     h = n / 2;
   }
 };
 
-template <int KK>
+// activation / weight tensor maps of the NMX members of one launch
+template <int NMX>
+struct MapSet {
+  LogitTcMaps m[NMX];
+};
+
+template <int KK, int NMX>
 __global__ void __launch_bounds__(kThreads, 1)
-    logits_pair_kernel(const __grid_constant__ CUtensorMap tX_hi, const __grid_constant__ CUtensorMap tX_lo,
-                       const __grid_constant__ CUtensorMap tW_hi, const __grid_constant__ CUtensorMap tW_lo,
-                       LogitTcArgs a) {
+    logits_pair_kernel(const __grid_constant__ MapSet<NMX> mp, LogitTcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = tc::align_smem<1024>(smem_raw);  // stays in the shared address space (LDS/STS)
   float *tr = reinterpret_cast<float *>(smem + kStages * kStageB);  // [group][32][kTrRow]
@@ -171,14 +179,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int member = (int)(crank & 1);
   const uint32_t leader = crank & ~1u;
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int nm = NMX == 1 ? 1 : a.nm;
+  const int ur = unit_rows(nm);
   const int nvt = (a.N + 255) / 256;
-  const int npass = (a.M + kUnitRows - 1) / kUnitRows;
+  const int npass = (a.M + ur - 1) / ur;
   const int units = nvt * npass;
   // contiguous units per pair: the two row halves of a vocabulary tile run
   // back to back on the same pair, so the second weight read hits L2
   const int upp = (units + npairs - 1) / npairs;
   const int u_begin = pair * upp, u_end = min(units, u_begin + upp);
-  const int nk = (a.K + kBK - 1) / kBK;
+  auto nk_of = [&](int mi) { return ((mi == 0 ? a.K : a.K_x[mi - 1]) + kBK - 1) / kBK; };
   constexpr uint16_t kMask = 3;
 
   if (warp == 0 && lane == 0) {
@@ -191,10 +201,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&tempty[b], 2 * 4 * kEpiGroups);  // every epilogue warp of both CTAs of the pair
     }
     tc::fence_barrier_init();
-    tc::tma_prefetch(&tX_hi);
-    tc::tma_prefetch(&tX_lo);
-    tc::tma_prefetch(&tW_hi);
-    tc::tma_prefetch(&tW_lo);
+    for (int mi = 0; mi < nm; ++mi) {
+      tc::tma_prefetch(&mp.m[mi].a_hi);
+      tc::tma_prefetch(&mp.m[mi].a_lo);
+      tc::tma_prefetch(&mp.m[mi].b_hi);
+      tc::tma_prefetch(&mp.m[mi].b_lo);
+    }
   }
   if (warp == 1) tc::tmem_alloc_pair<512>(tslot);
   tc::tc_fence_before();
@@ -209,10 +221,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool lw = !(a.debug_flags & 1), lx = !(a.debug_flags & 2);
       int it = 0;
       for (int u = u_begin; u < u_end; ++u) {
-        const Unit un(u, npass, a.M);
+        const Unit un(u, npass, a.M, ur);
         const int v0 = un.vt * 256 + member * 128;
         const int g = un.row0 + member * un.h;
         const uint32_t bytes = (lw ? 2 * kWB : 0) + (lx ? 2 * un.h * kRowB : 0);
+        for (int mi = 0; mi < nm; ++mi) {
+        const CUtensorMap *tW_hi = &mp.m[mi].b_hi, *tW_lo = &mp.m[mi].b_lo;
+        const CUtensorMap *tX_hi = &mp.m[mi].a_hi, *tX_lo = &mp.m[mi].a_lo;
+        const int nk = nk_of(mi);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages;
           if (it >= kStages) tc::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
@@ -221,15 +237,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t *st = smem + s * kStageB;
           const int kx = kb * kBK;
           if (lw) {
-            tc::tma_load_2d_pair(st, &tW_hi, bar, kx, v0);
-            tc::tma_load_2d_pair(st + kWB, &tW_lo, bar, kx, v0);
+            tc::tma_load_2d_pair(st, tW_hi, bar, kx, v0);
+            tc::tma_load_2d_pair(st + kWB, tW_lo, bar, kx, v0);
           }
           if (lx) {
             for (int r = 0; r < un.h; r += kBoxR) {
-              tc::tma_load_2d_pair(st + 2 * kWB + r * kRowB, &tX_hi, bar, kx, g + r);
-              tc::tma_load_2d_pair(st + 2 * kWB + kXB + r * kRowB, &tX_lo, bar, kx, g + r);
+              tc::tma_load_2d_pair(st + 2 * kWB + r * kRowB, tX_hi, bar, kx, g + r);
+              tc::tma_load_2d_pair(st + 2 * kWB + kXB + r * kRowB, tX_lo, bar, kx, g + r);
             }
           }
+        }
         }
       }
     }
@@ -240,14 +257,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && member == 0) {
       int it = 0, ti = 0;
       for (int u = u_begin; u < u_end; ++u, ++ti) {
-        const Unit un(u, npass, a.M);
+        const Unit un(u, npass, a.M, ur);
         const int buf = ti & 1;
-        const uint32_t acc = tmem + buf * kAccCols;
         const uint32_t idesc = tc::idesc_f16(256, un.n);
         if (ti >= 2) {
           tc::mbar_wait(&tempty[buf], ((ti >> 1) - 1) & 1);  // both epilogues drained this buffer
           tc::tc_fence_after();
         }
+        for (int mi = 0; mi < nm; ++mi) {
+        const uint32_t acc = tmem + buf * kAccCols + mi * ur;
+        const int nk = nk_of(mi);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages;
           tc::mbar_wait(&full[s], (it / kStages) & 1);
@@ -267,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc::mma_commit_pair_mc(&empty[s], (uint16_t)(kMask << leader));
         }
+        }
         tc::mma_commit_pair_mc(&tfull[buf], (uint16_t)(kMask << leader));
       }
     }
@@ -285,33 +305,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + pt] = clock64();
     };
     for (int u = u_begin; u < u_end; ++u, ++ti) {
-      const Unit un(u, npass, a.M);
+      const Unit un(u, npass, a.M, ur);
       const int ab = ti & 1;
       const int v0 = un.vt * 256 + member * 128;
       const int nt = un.vt * 2 + member;  // 128-vocab tile index of the partial outputs
-      const float bias_f = (v0 + f < a.N) ? __ldg(a.bias + v0 + f) : -INFINITY;
+      float bias_f[NMX];
+#pragma unroll
+      for (int mi = 0; mi < NMX; ++mi) {
+        const float *bp = mi == 0 ? a.bias : a.bias_x[mi - 1];
+        bias_f[mi] = (mi < nm && v0 + f < a.N) ? __ldg(bp + v0 + f) : -INFINITY;
+      }
       if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + 11] = clock64();
       tc::mbar_wait(&tfull[ab], (ti >> 1) & 1);
       tc::tc_fence_after();
       if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + 12] = clock64();
 #pragma unroll 1
       for (int c0 = 32 * g; c0 < un.n; c0 += 32 * kEpiGroups, ++dchunk) {
-        stamp(0);
-        {
-          float v[32];
-          tc::tmem_ld_32x32(tmem + ab * kAccCols + ((uint32_t)(lg * 32) << 16) + c0, v);
-          float *dst = buf + lg * kTrQ + lane;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) dst[i * kTrRow] = fmaf(v[i], a.unscale, bias_f);
+        const int m = un.row0 + c0 + ri;
+        const bool wr = q == 0 && c0 + ri < un.nr && nt < a.ntiles && !(a.debug_flags & 64);
+        // thread (ri, q): logits of row c0 + ri for vocab v0 + 32 q + [0, 32);
+        // the quarter pad makes each 8-lane LDS.128 phase hit 8 bank groups
+        float *src = buf + ri * kTrRow + q * kTrQ;
+        float x[32];   // this member's logits; after the member loop, the member sum
+        float g8[4];   // 8-wide group maxima of x
+        float mx = -INFINITY, se = 0.f;
+        uint32_t allow = ~0u;
+        // shortlist (nnet.py:160-163): columns outside the row's sentence
+        // list do not exist; the thread's 32 columns are one mask word
+        if (a.vmask) {
+          const int vq = v0 + q * 32;
+          allow = (m < a.M && vq < a.N)
+                      ? __ldg(a.vmask + (long long)(m / a.rows_per_sent) * a.mask_words + (vq >> 5))
+                      : 0u;
         }
-        stamp(1);
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-        stamp(2);
-        if (!(a.debug_flags & 8)) {
-          // thread (ri, q): logits of row c0 + ri for vocab v0 + 32 q + [0, 32);
-          // the quarter pad makes each 8-lane LDS.128 phase hit 8 bank groups
-          float x[32];
-          const float *src = buf + ri * kTrRow + q * kTrQ;
+        float xs[NMX > 1 ? 32 : 1];
+#pragma unroll 1
+        for (int mi = 0; mi < nm; ++mi) {
+          if (mi) asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // buffer free
+          stamp(0);
+          {
+            float v[32];
+            tc::tmem_ld_32x32(tmem + ab * kAccCols + mi * ur + ((uint32_t)(lg * 32) << 16) + c0, v);
+            float *dst = buf + lg * kTrQ + lane;
+            const float us = mi == 0 ? a.unscale : a.unscale_x[mi - 1];
+            float bf = bias_f[0];
+#pragma unroll
+            for (int j = 1; j < NMX; ++j) bf = mi == j ? bias_f[j] : bf;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) dst[i * kTrRow] = fmaf(v[i], us, bf);
+          }
+          stamp(1);
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+          stamp(2);
+          if (a.debug_flags & 8) continue;
 #pragma unroll
           for (int u4 = 0; u4 < 8; ++u4) {
             const float4 t4 = *reinterpret_cast<const float4 *>(src + 4 * u4);
@@ -320,36 +366,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             x[4 * u4 + 2] = t4.z;
             x[4 * u4 + 3] = t4.w;
           }
-          // shortlist (nnet.py:160-163): columns outside the row's sentence
-          // list do not exist; the thread's 32 columns are one mask word
-          uint32_t allow = ~0u;
           if (a.vmask) {
-            const int mrow = un.row0 + c0 + ri, vq = v0 + q * 32;
-            allow = (mrow < a.M && vq < a.N)
-                        ? __ldg(a.vmask + (long long)(mrow / a.rows_per_sent) * a.mask_words + (vq >> 5))
-                        : 0u;
 #pragma unroll
             for (int i = 0; i < 32; ++i) x[i] = (allow >> i) & 1u ? x[i] : -INFINITY;
           }
-          // four 8-wide group maxima, the two 16-wide half maxima, the
-          // quarter max, and sum exp(x - max) (ex2-based: x log2 e - max
-          // log2 e, one FFMA + MUFU per logit)
-          float g8[4];
+          // four 8-wide group maxima, the quarter max, and sum exp(x - max)
+          // (ex2-based: x log2 e - max log2 e, one FFMA + MUFU per logit)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             g8[j] = x[8 * j];
 #pragma unroll
             for (int i = 1; i < 8; ++i) g8[j] = fmaxf(g8[j], x[8 * j + i]);
           }
-          const float h0 = fmaxf(g8[0], g8[1]), h1 = fmaxf(g8[2], g8[3]);
-          float mx = fmaxf(h0, h1);
+          mx = fmaxf(fmaxf(g8[0], g8[1]), fmaxf(g8[2], g8[3]));
           stamp(3);
-          float se = 0.f;
+          se = 0.f;
           if (mx != -INFINITY) {
             const float mxl = mx * 1.4426950408889634f;
 #pragma unroll
             for (int i = 0; i < 32; ++i) se += tc::exp2f_approx(fmaf(x[i], 1.4426950408889634f, -mxl));
           }
+          // merge (max, sum) over the four quarters of the row (lanes 4 ri .. 4 ri + 3)
+#pragma unroll
+          for (int o = 1; o <= 2; o <<= 1) {
+            const float omx = __shfl_xor_sync(0xffffffffu, mx, o);
+            const float ose = __shfl_xor_sync(0xffffffffu, se, o);
+            const float nmx = fmaxf(mx, omx);
+            const float a0 = (mx == -INFINITY) ? 0.f : se * expf(mx - nmx);
+            const float a1 = (omx == -INFINITY) ? 0.f : ose * expf(omx - nmx);
+            se = (q & o) ? a1 + a0 : a0 + a1;  // same operand order in both partners
+            mx = nmx;
+          }
+          if (wr) {
+            const long long o = (long long)mi * a.pm_stride + (long long)m * a.ntiles + nt;
+            a.pmax[o] = mx;
+            a.psum[o] = se;
+          }
+          if constexpr (NMX > 1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) xs[i] = mi == 0 ? x[i] : xs[i] + x[i];
+          }
+        }
+        if (!(a.debug_flags & 8)) {
+          if constexpr (NMX > 1) {
+            // ensemble: the candidates rank the member sum of the logits
+            // (search.py:67-72: mean_m(logit_m - lse_m) orders like sum_m
+            // logit_m); the sum replaces this thread's own smem quarter row
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = xs[i];
+#pragma unroll
+            for (int u4 = 0; u4 < 8; ++u4)
+              *reinterpret_cast<float4 *>(src + 4 * u4) = make_float4(x[4 * u4], x[4 * u4 + 1], x[4 * u4 + 2], x[4 * u4 + 3]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              g8[j] = x[8 * j];
+#pragma unroll
+              for (int i = 1; i < 8; ++i) g8[j] = fmaxf(g8[j], x[8 * j + i]);
+            }
+          }
+          const float h0 = fmaxf(g8[0], g8[1]), h1 = fmaxf(g8[2], g8[3]);
           // Threshold: the KK-th largest of the row's 8 half maxima (16 group
           // maxima for KK > 8) is a lower bound on the row's KK-th largest
           // logit (those maxima are distinct logits), so only logits >= thr
@@ -409,23 +484,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             top.insert(src[i], tbase + i);
           }
           stamp(7);
-          // merge the four quarters of the row (lanes 4 ri .. 4 ri + 3)
+          // merge the four quarters' lists of the row
 #pragma unroll
-          for (int o = 1; o <= 2; o <<= 1) {
-            const float omx = __shfl_xor_sync(0xffffffffu, mx, o);
-            const float ose = __shfl_xor_sync(0xffffffffu, se, o);
-            const float nmx = fmaxf(mx, omx);
-            const float a0 = (mx == -INFINITY) ? 0.f : se * expf(mx - nmx);
-            const float a1 = (omx == -INFINITY) ? 0.f : ose * expf(omx - nmx);
-            se = (q & o) ? a1 + a0 : a0 + a1;  // same operand order in both partners
-            mx = nmx;
-            merge_partner(top, o);
-          }
+          for (int o = 1; o <= 2; o <<= 1) merge_partner(top, o);
           stamp(8);
-          const int m = un.row0 + c0 + ri;
-          if (q == 0 && c0 + ri < un.nr && nt < a.ntiles && !(a.debug_flags & 64)) {
-            a.pmax[(long long)m * a.ntiles + nt] = mx;
-            a.psum[(long long)m * a.ntiles + nt] = se;
+          if (wr) {
             const long long base = ((long long)m * a.ntiles + nt) * a.kk;
 #pragma unroll
             for (int i = 0; i < KK; ++i)
@@ -480,9 +543,11 @@ int logit_pairs(int units) {
   return ceil_div(units, per);
 }
 
-template <int KK>
-void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
-  auto kern = logits_pair_kernel<KK>;
+template <int KK, int NMX>
+void launch_t(const LogitTcMaps *maps, const LogitTcArgs &a, cudaStream_t st) {
+  auto kern = logits_pair_kernel<KK, NMX>;
+  MapSet<NMX> mp;
+  for (int i = 0; i < NMX; ++i) mp.m[i] = maps[i < a.nm ? i : 0];
   static bool attr[64] = {};
   int dev = 0;
   AMUN_CUDA(cudaGetDevice(&dev));
@@ -490,7 +555,7 @@ void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
     AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     if (dev < 64) attr[dev] = true;
   }
-  const int units = ceil_div(a.N, 256) * ceil_div(a.M, kUnitRows);
+  const int units = ceil_div(a.N, 256) * ceil_div(a.M, unit_rows(NMX == 1 ? 1 : a.nm));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * logit_pairs(units));
   cfg.blockDim = dim3(kThreads);
@@ -504,7 +569,7 @@ void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
   cfg.attrs = la;
   cfg.numAttrs = 1;
   last_launch_ctas() = (int)cfg.gridDim.x;
-  AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, a));
+  AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, mp, a));
 }
 
 }  // namespace
@@ -551,21 +616,32 @@ LogitTcMaps make_logit_maps(const __half *t_hi, const __half *t_lo, int R, int K
   return m;
 }
 
-void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
+template <int NMX>
+void launch_kk(const LogitTcMaps *maps, const LogitTcArgs &a, cudaStream_t st) {
   // list size >= kk (a sorted top-KK list contains the top-kk as its prefix)
   switch (a.kk) {
-    case 1: launch_t<1>(maps, a, st); break;
-    case 2: launch_t<2>(maps, a, st); break;
-    case 3: launch_t<3>(maps, a, st); break;
-    case 4: launch_t<4>(maps, a, st); break;
-    case 5: launch_t<5>(maps, a, st); break;
-    case 6: launch_t<6>(maps, a, st); break;
-    case 7: case 8: launch_t<8>(maps, a, st); break;
-    case 9: case 10: launch_t<10>(maps, a, st); break;
-    case 11: case 12: launch_t<12>(maps, a, st); break;
-    case 13: case 14: case 15: case 16: launch_t<16>(maps, a, st); break;
+    case 1: launch_t<1, NMX>(maps, a, st); break;
+    case 2: launch_t<2, NMX>(maps, a, st); break;
+    case 3: launch_t<3, NMX>(maps, a, st); break;
+    case 4: launch_t<4, NMX>(maps, a, st); break;
+    case 5: launch_t<5, NMX>(maps, a, st); break;
+    case 6: launch_t<6, NMX>(maps, a, st); break;
+    case 7: case 8: launch_t<8, NMX>(maps, a, st); break;
+    case 9: case 10: launch_t<10, NMX>(maps, a, st); break;
+    case 11: case 12: launch_t<12, NMX>(maps, a, st); break;
+    case 13: case 14: case 15: case 16: launch_t<16, NMX>(maps, a, st); break;
     default: throw Error(4, "tensor-core logit path supports beam <= 16");
   }
+}
+
+void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
+  if (a.nm != 1) throw Error(4, "launch_logits_tc: single-member launch");
+  launch_kk<1>(&maps, a, st);
+}
+
+void launch_logits_tc_ens(const LogitTcMaps *maps, const LogitTcArgs &a, cudaStream_t st) {
+  if (a.nm < 2 || a.nm > kLogitMembers) throw Error(4, "tensor-core logit ensembles take 2..4 members");
+  launch_kk<kLogitMembers>(maps, a, st);
 }
 
 }  // namespace amun

@@ -22,6 +22,16 @@ struct LogitTcArgs {
   // optional column -> vocabulary id map (gathered shortlist columns, strictly
   // ascending): candidate tokens are reported as vid[column]
   const int *vid = nullptr;
+  // ensembles (search.py:56-72) fused in one launch: members 1 .. nm-1 run
+  // their own logit GEMM (K_x, bias_x, unscale_x, their own tensor maps);
+  // per member the (max, sum) partials go to pmax/psum + m * pm_stride and
+  // the candidates are the row's top-kk of the member SUM of logits (the
+  // ensemble log-prob mean_m(logit_m - lse_m) orders like that sum)
+  int nm = 1;
+  int K_x[3] = {0, 0, 0};
+  const float *bias_x[3] = {nullptr, nullptr, nullptr};
+  float unscale_x[3] = {0.f, 0.f, 0.f};
+  long long pm_stride = 0;
   int debug_flags = 0;  // microbenchmark knobs: 1 skip A loads, 2 skip B loads, 4 skip MMA, 8 skip epilogue
   long long *debug_clock = nullptr;  // microbenchmark: per-chunk clock64 stamps of CTA 0
 };
@@ -29,6 +39,7 @@ struct LogitTcArgs {
 struct LogitTcMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
 };
+constexpr int kLogitMembers = 4;  // ensemble members of one fused logit launch
 
 int logits_tc_tile_n();
 // fp32 2D tensor map; the swizzle follows the box row width (64 B -> SW64,
@@ -42,5 +53,7 @@ CUtensorMap make_tma_2d_f16(const __half *ptr, int inner, int outer, int row_str
 LogitTcMaps make_logit_maps(const __half *t_hi, const __half *t_lo, int R, int K, int ldt, const __half *w_hi,
                             const __half *w_lo, int ldw, int V);
 void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st);
+// a.nm members (2 .. kLogitMembers), maps[m] = member m's activation / weight maps
+void launch_logits_tc_ens(const LogitTcMaps *maps, const LogitTcArgs &a, cudaStream_t st);
 
 }  // namespace amun

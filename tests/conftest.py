@@ -70,6 +70,13 @@ def golden_shortlist() -> dict:
         return {k: z[k] for k in z.files}
 
 
+@lru_cache(maxsize=1)
+def golden_ensemble() -> dict:
+    """Reference full-size ensemble decodes (make_golden_ensemble.py)."""
+    with np.load(GOLDEN / "ensemble_sets.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
 def fullset_src_sha(corpus) -> str:
     import hashlib
 

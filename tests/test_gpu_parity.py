@@ -511,3 +511,39 @@ def test_shortlist_decode_matches_reference(gpu, full, name, max_batch):
     _adjudicate(f"shortlist {name} batch {max_batch}", gold, gaps, out)
     for i in range(len(sents)):
         assert set(out.hyps(i)[0][0]) <= set(sls[i].tolist())
+
+
+@pytest.mark.parametrize("name", ["ens2", "ens3", "mixed"])
+def test_ensemble_decode_matches_reference(gpu, full, name):
+    """Full-size ensembles (search.py:56-72: log-probs averaged about the
+    first member; search.py:150-152: one Forward per member, so members may
+    differ in d_emb / d_h / d_att) against the reference's own beam_search
+    (tests/golden/make_golden_ensemble.py), decoded in buckets of 64.  The
+    members' logits run as ONE fused tensor-core launch per step (member-sum
+    candidates + per-member log-softmax partials): the per-class launch
+    counts show one logit launch per decoder step, never the CUDA-core
+    full-logit path."""
+    from conftest import golden_ensemble
+    from paper_1610_01108_b200 import workload as W
+
+    g = golden_ensemble()
+    members = []
+    for de, dh, da, seed in g[f"{name}_members"].tolist():
+        if (de, dh, da, seed) == (500, 1024, 1024, 1):
+            members.append(full)
+        else:
+            members.append(random_model(ModelConfig(30000, 30000, de, dh, da), seed))
+    dms = [_lib.device_model(m) for m in members]
+    corpus = W.WORKLOADS["cfg2"].corpus()
+    sents = [corpus[i] for i in g[f"{name}_idx"]]
+    beam, f, o, _, _ = (int(x) for x in g[f"{name}_opts"])
+    out = _lib.decode(dms, sents, beam, f, o, False, 2, max_batch=64)
+    toff, goff = g[f"{name}_tok_off"], g[f"{name}_gap_off"]
+    gold = [(g[f"{name}_tokens"][toff[i]:toff[i + 1]].astype(int).tolist(), float(g[f"{name}_score"][i]))
+            for i in range(len(sents))]
+    gaps = [g[f"{name}_gap"][goff[i]:goff[i + 1]] for i in range(len(sents))]
+    _adjudicate(f"ensemble {name}", gold, gaps, out)
+    prof = _lib.decode(dms, sents[:3], beam, f, o, False, 2, max_batch=64, profile=(1 << 6) | (1 << 7))
+    assert prof.kernel_count["logits"] == prof.decoder_steps, (prof.kernel_count, prof.decoder_steps)
+    for i in range(3):
+        assert prof.hyps(i) == out.hyps(i)

@@ -717,6 +717,7 @@ struct LogitOut {
   float *pmax, *psum, *cval;
   int *ctok;
   const LogitTcMaps *tc = nullptr;  // tensor-core path when set
+  bool rows = false;                // tc maps are rows-layout maps (logits_rows.cu)
   const uint32_t *vmask = nullptr;  // per-sentence shortlist masks (tensor-core path)
   int mask_words = 0;
   // gathered shortlist columns (tensor-core path): the bucket's union U of
@@ -859,7 +860,10 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     ta.rows_per_sent = rows_per_sent;
     static const int ldbg = debug_env("AMUN_DEBUG_LOGIT_FLAGS");
     ta.debug_flags = ldbg;
-    c.run(AMUN_K_LOGIT, [&] { launch_logits_tc(*lo.tc, ta, c.st); });
+    if (lo.rows)
+      c.run(AMUN_K_LOGIT, [&] { launch_logits_rows(*lo.tc, ta, c.st); });
+    else
+      c.run(AMUN_K_LOGIT, [&] { launch_logits_tc(*lo.tc, ta, c.st); });
     return;
   }
   GemmArgs g = ga(R, V, d.T, de, de, m->W_logit, V);
@@ -984,6 +988,15 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   const bool fused = (n_models == 1 || ens_tc) && (!sl_ids || tc_logits) && k <= kMaxRowCand && !o.force_full_logits;
   const bool ens_fused = fused && n_models > 1;
   const bool use_tc = fused && tc_logits;
+  // AMUN_LOGIT_ROWS=1 / 0 forces the rows-layout / swap-AB logit kernel
+  const char *rows_env = getenv("AMUN_LOGIT_ROWS");
+  // beams >= 8: the rows-layout kernel (one row per epilogue thread) wins
+  // over the swap-AB kernel (cfg4: +25%); smaller beams keep swap-AB.  The
+  // choice depends on per-call constants only (the beam), never on a
+  // bucket's size, so a sentence's result never depends on its batch-mates.
+  const bool use_rows = use_tc && n_models == 1 &&
+                        (rows_env ? rows_env[0] == '1' : k >= 8);
+  const int tile_n = use_rows ? kLogitRowsTileN : kBN;
   const bool use_mask = fused && sl_ids != nullptr;
   const int mask_words = ceil_div(V, 32);
   // shortlist buckets whose union of ids is at most gather_cap wide run their
@@ -1209,7 +1222,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     if (use_tc) {
       static_assert(kBN == 128, "fused-logit tile width shared by SIMT and tensor-core paths");
       if (logits_tc_tile_n() != kBN) throw Error(AMUN_ERR_UNSUPPORTED, "logit tile width mismatch");
-      L.tc_maps = make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, m0->Wl_hi, m0->Wl_lo, m0->dep, V);
+      L.tc_maps = use_rows ? make_logit_rows_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, m0->Wl_hi,
+                                                  m0->Wl_lo, m0->dep, V)
+                           : make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, m0->Wl_hi, m0->Wl_lo,
+                                             m0->dep, V);
       if (ens_fused) {
         L.tc_maps_ens.resize(n_models);
         for (int m = 0; m < n_models; ++m)
@@ -1398,8 +1414,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
                                                               L.Wg_hi, L.Wg_lo, L.bg);
           AMUN_CHECK_LAUNCH();
         });
-        L.tc_maps_g = make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, L.Wg_hi, L.Wg_lo, m0->dep,
-                                      n_gath);
+        L.tc_maps_g = use_rows ? make_logit_rows_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, L.Wg_hi,
+                                                      L.Wg_lo, m0->dep, n_gath)
+                               : make_logit_maps(L.db[0].T_hi, L.db[0].T_lo, Rmax, de, m0->dep, L.Wg_hi, L.Wg_lo,
+                                                 m0->dep, n_gath);
       } else {
         std::vector<uint32_t> mask((size_t)B * mask_words, 0u);
         for (int i = 0; i < B; ++i)
@@ -1445,7 +1463,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.mr.XSl = L.p_XSl;
     }
     c.run(AMUN_K_SELECT, [&] { launch_init_beam(L.bs, L.mr, L.p_S0, L.st); });
-    L.lo = LogitOut{fused, kk, ntiles, L.pmax, L.psum, L.cval, L.ctok};
+    L.lo = LogitOut{fused, kk, ceil_div(V, tile_n), L.pmax, L.psum, L.cval, L.ctok};
+    L.lo.rows = use_rows;
     if (use_mask) {
       L.lo.vmask = L.d_vmask;
       L.lo.mask_words = mask_words;
@@ -1458,7 +1477,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.lo.n_vocab = n_gath;
       L.lo.vid = L.d_U;
       L.lo.bias = L.bg;
-      L.lo.ntiles = ceil_div(n_gath, kBN);
+      L.lo.ntiles = ceil_div(n_gath, tile_n);
     }
     SelectArgs &sa = L.sa;
     sa = SelectArgs{};
@@ -1996,17 +2015,38 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
   AMUN_CHECK_LAUNCH();
   TcStep ts;
   tc_step_maps(m, d, R, ts);
-  const LogitTcMaps lm = make_logit_maps(d.T_hi, d.T_lo, R, de, m->dep, m->Wl_hi, m->Wl_lo, m->dep, V);
-  LogitOut lo{true, kk, ntiles, pmax, psum, cval, ctok};
+  // the product's logit kernel for this beam (decode_run: rows layout for
+  // beams >= 8, swap-AB below); the outputs keep the [R][ceil(V / 128)]
+  // layout, tiles the kernel does not produce padded as empty partials
+  const char *rows_env = getenv("AMUN_LOGIT_ROWS");
+  const bool rows = rows_env ? rows_env[0] == '1' : k >= 8;
+  const int nt_dev = ceil_div(V, rows ? kLogitRowsTileN : kBN);
+  const LogitTcMaps lm = rows ? make_logit_rows_maps(d.T_hi, d.T_lo, R, de, m->dep, m->Wl_hi, m->Wl_lo, m->dep, V)
+                              : make_logit_maps(d.T_hi, d.T_lo, R, de, m->dep, m->Wl_hi, m->Wl_lo, m->dep, V);
+  LogitOut lo{true, kk, nt_dev, pmax, psum, cval, ctok};
   lo.tc = &lm;
+  lo.rows = rows;
   step_rows(c, m, d, e, d_len, jmax, R, k, nullptr, nullptr, d_alpha, lo, &ts);
+  std::vector<float> hpm((size_t)R * nt_dev), hps((size_t)R * nt_dev), hcv((size_t)R * nt_dev * kk);
+  std::vector<int> hct((size_t)R * nt_dev * kk);
   if (s_out) d2h(c, s_out, d.Sn, (size_t)R * dh);
-  if (pmax_out) d2h(c, pmax_out, pmax, (size_t)R * ntiles);
-  if (psum_out) d2h(c, psum_out, psum, (size_t)R * ntiles);
-  if (cval_out) d2h(c, cval_out, cval, (size_t)R * ntiles * kk);
-  if (ctok_out) d2h(c, ctok_out, ctok, (size_t)R * ntiles * kk);
+  d2h(c, hpm.data(), pmax, hpm.size());
+  d2h(c, hps.data(), psum, hps.size());
+  d2h(c, hcv.data(), cval, hcv.size());
+  d2h(c, hct.data(), ctok, hct.size());
   if (alpha_out) d2h(c, alpha_out, d_alpha, (size_t)R * jmax);
   AMUN_CUDA(cudaStreamSynchronize(c.st));
+  for (int r = 0; r < R; ++r)
+    for (int t = 0; t < ntiles; ++t) {
+      const bool have = t < nt_dev;
+      const size_t o = (size_t)r * ntiles + t, od = (size_t)r * nt_dev + t;
+      if (pmax_out) pmax_out[o] = have ? hpm[od] : -INFINITY;
+      if (psum_out) psum_out[o] = have ? hps[od] : 0.f;
+      for (int i = 0; i < kk; ++i) {
+        if (cval_out) cval_out[o * kk + i] = have ? hcv[od * kk + i] : -INFINITY;
+        if (ctok_out) ctok_out[o * kk + i] = have ? hct[od * kk + i] : -1;
+      }
+    }
 }
 
 // Batched encoder hook: B padded sentences (ids [B][jmax], lens[B]) through

@@ -72,18 +72,22 @@ struct RowTop {
   __device__ __forceinline__ bool beats(float x, int n, int i) const {
     return x > v[i] || (x == v[i] && n < t[i]);
   }
-  // branch-free insertion (selects only: no divergence inside a warp)
+  // Insertion of (x, n) where n is larger than every token in the list (a
+  // thread inserts its candidates in increasing column order): x enters
+  // before the first entry it strictly exceeds, so an equal value keeps the
+  // earlier token first.  Every slot's update depends only on the old list
+  // (one compare per slot, then selects): no serial chain through the slots.
   __device__ __forceinline__ void insert(float x, int n) {
+    bool gt[KK];
 #pragma unroll
-    for (int i = 0; i < KK; ++i) {
-      const bool c = beats(x, n, i);
-      const float vi = v[i];
-      const int ti = t[i];
-      v[i] = c ? x : vi;
-      t[i] = c ? n : ti;
-      x = c ? vi : x;
-      n = c ? ti : n;
+    for (int i = 0; i < KK; ++i) gt[i] = x > v[i];
+#pragma unroll
+    for (int i = KK - 1; i > 0; --i) {
+      v[i] = gt[i - 1] ? v[i - 1] : (gt[i] ? x : v[i]);
+      t[i] = gt[i - 1] ? t[i - 1] : (gt[i] ? n : t[i]);
     }
+    v[0] = gt[0] ? x : v[0];
+    t[0] = gt[0] ? n : t[0];
   }
 };
 
@@ -479,9 +483,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           top.init();
           const int tbase = v0 + q * 32;
 #pragma unroll 1
-          for (; cand; cand &= cand - 1) {  // few candidates per quarter
-            const int i = __ffs(cand) - 1;
-            top.insert(src[i], tbase + i);
+          while (cand) {  // few candidates per quarter; two per trip (both loads in flight)
+            const int i0 = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const int i1 = cand ? __ffs(cand) - 1 : -1;
+            cand &= cand - 1;
+            const float x0 = src[i0], x1 = src[i1 < 0 ? i0 : i1];
+            top.insert(x0, tbase + i0);
+            if (i1 >= 0) top.insert(x1, tbase + i1);
           }
           stamp(7);
           // merge the four quarters' lists of the row

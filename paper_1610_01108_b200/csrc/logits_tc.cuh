@@ -53,6 +53,12 @@ CUtensorMap make_tma_2d_f16(const __half *ptr, int inner, int outer, int row_str
 LogitTcMaps make_logit_maps(const __half *t_hi, const __half *t_lo, int R, int K, int ldt, const __half *w_hi,
                             const __half *w_lo, int ldw, int V);
 void launch_logits_tc(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st);
+// Rows layout (logits_rows.cu): hypothesis rows are the MMA's M, one epilogue
+// thread per row, partials per (row, 128-vocab tile); single member.
+constexpr int kLogitRowsTileN = 128;
+LogitTcMaps make_logit_rows_maps(const __half *t_hi, const __half *t_lo, int R, int K, int ldt, const __half *w_hi,
+                                 const __half *w_lo, int ldw, int V);
+void launch_logits_rows(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st);
 // a.nm members (2 .. kLogitMembers), maps[m] = member m's activation / weight maps
 void launch_logits_tc_ens(const LogitTcMaps *maps, const LogitTcArgs &a, cudaStream_t st);
 

@@ -322,8 +322,11 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
 // launch and 64 CTAs per bucket step instead of two launches of 256 CTAs:
 // fewer, longer-lived CTAs leave the SMs to the tensor-core kernels of the
 // other bucket lanes (the step is throughput-bound with 16 lanes in flight).
+// Two CTAs per SM for beams <= 8 (<= 64 registers: P rows in chunks of 8,
+// e^{2q} rows staged in shared memory), so a step's 64 sentence CTAs share
+// the SMs left by the other lanes' tensor-core kernels.
 template <int KA>
-__global__ void __launch_bounds__(512, 1) attn_sent_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArgs a) {
   extern __shared__ float sm[];
   const int b = blockIdx.x;
   if (a.n_act && a.done[b]) return;
@@ -334,7 +337,12 @@ __global__ void __launch_bounds__(512, 1) attn_sent_kernel(AttnArgs a) {
   float *vs = sm;                                    // [da]
   float *al = vs + a.da;                             // [k][jmax]
   int *qbig = reinterpret_cast<int *>(al + (size_t)k * a.jmax);  // [k]
+  float *eqs = reinterpret_cast<float *>(qbig + ((k + 3) & ~3));  // [KA][1024] e^{2q} rows (fast path)
   for (int i = tid; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
+  const bool fast_shape = na == KA && a.da == 1024;
+  if (fast_shape)
+    for (int i = tid; i < KA * 1024; i += blockDim.x)
+      eqs[i] = __ldg(a.EQ + (long long)(b * k + i / 1024) * a.ldq + (i % 1024));
   for (int r = warp; r < na; r += nw) {
     const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
     float m = 0.f;
@@ -348,39 +356,49 @@ __global__ void __launch_bounds__(512, 1) attn_sent_kernel(AttnArgs a) {
   // ---- energies: warp per source position (nnet.py:135-136)
   for (int j = warp; j < J; j += nw) {
     const float *pj = a.P + ((long long)b * a.jmax + j) * a.da;
-    float ep[32];
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int i = lane + 32 * u;
-      ep[u] = i < a.da ? __ldg(pj + i) : 0.f;
-    }
-    float pm = 0.f;
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      pm = fmaxf(pm, fabsf(ep[u]));
-      ep[u] = tc_exp2(ep[u] * kTwoLog2e);
-    }
-    const bool pbig = warp_max(pm) > kFactorSafe;
-    if (!pbig && !anybig && na == KA && a.da == 1024) {
-      const float *eqr[KA];
-#pragma unroll
-      for (int r = 0; r < KA; ++r) eqr[r] = a.EQ + (long long)(b * k + r) * a.ldq + lane;
+    bool done = false;
+    if (fast_shape && !anybig) {
+      // factored tanh over the P row in chunks of 8 values per lane (same
+      // per-lane order as one pass), |p| tracked for the safety check
       float acc[KA];
 #pragma unroll
       for (int r = 0; r < KA; ++r) acc[r] = 0.f;
+      float pm = 0.f;
+#pragma unroll 1
+      for (int u0 = 0; u0 < 32; u0 += 8) {
+        float ep[8];
 #pragma unroll
+        for (int u = 0; u < 8; ++u) ep[u] = __ldg(pj + lane + 32 * (u0 + u));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          pm = fmaxf(pm, fabsf(ep[u]));
+          ep[u] = tc_exp2(ep[u] * kTwoLog2e);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = lane + 32 * (u0 + u);
+          const float vi = vs[i];
+#pragma unroll
+          for (int r = 0; r < KA; ++r)
+            acc[r] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], eqs[r * 1024 + i], 1.0f)), 1.0f), acc[r]);
+        }
+      }
+      if (!(warp_max(pm) > kFactorSafe)) {
+#pragma unroll
+        for (int r = 0; r < KA; ++r) {
+          const float sum = warp_sum(acc[r]);
+          if (lane == 0) al[r * a.jmax + j] = sum;
+        }
+        done = true;
+      }
+    }
+    if (!done) {
+      float pm = 0.f;
       for (int u = 0; u < 32; ++u) {
-        const float vi = vs[lane + 32 * u];
-#pragma unroll
-        for (int r = 0; r < KA; ++r)
-          acc[r] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], __ldg(eqr[r] + 32 * u), 1.0f)), 1.0f), acc[r]);
+        const int i = lane + 32 * u;
+        if (i < a.da) pm = fmaxf(pm, fabsf(__ldg(pj + i)));
       }
-#pragma unroll
-      for (int r = 0; r < KA; ++r) {
-        const float sum = warp_sum(acc[r]);
-        if (lane == 0) al[r * a.jmax + j] = sum;
-      }
-    } else {
+      const bool pbig = warp_max(pm) > kFactorSafe;
       for (int r = 0; r < na; ++r) {
         float s0 = 0.f;
         const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
@@ -391,7 +409,7 @@ __global__ void __launch_bounds__(512, 1) attn_sent_kernel(AttnArgs a) {
           if (i < a.da)
             s0 = fmaf(vs[i],
                       direct ? tanh_attn(__ldg(pj + i) + __ldg(qr + i))
-                             : 1.0f - __fdividef(2.0f, fmaf(ep[u], __ldg(er + i), 1.0f)),
+                             : 1.0f - __fdividef(2.0f, fmaf(tc_exp2(__ldg(pj + i) * kTwoLog2e), __ldg(er + i), 1.0f)),
                       s0);
         }
         const float sum = warp_sum(s0);
@@ -428,13 +446,14 @@ __global__ void __launch_bounds__(512, 1) attn_sent_kernel(AttnArgs a) {
     float4 acc[KA];
 #pragma unroll
     for (int r = 0; r < KA; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j0 = 0; j0 < J; j0 += 8) {
-      float4 h[8];
+    constexpr int kHB = KA <= 8 ? 4 : 8;  // H rows in flight per thread
+    for (int j0 = 0; j0 < J; j0 += kHB) {
+      float4 h[kHB];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
+      for (int jj = 0; jj < kHB; ++jj)
         h[jj] = j0 + jj < J ? __ldg(Hb + (long long)(j0 + jj) * hs + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
+      for (int jj = 0; jj < kHB; ++jj) {
         if (j0 + jj >= J) break;
 #pragma unroll
         for (int r = 0; r < KA; ++r)
@@ -491,7 +510,8 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
     const char *e = getenv("AMUN_ATTN_FUSED");  // 0: two-phase kernels
     return !(e && e[0] == '0');
   }();
-  const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)k;
+  const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)((k + 3) & ~3) +
+                        (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0);
   // The kernel is chosen from per-call constants only (beam width, model
   // layout), never from the bucket's longest sentence: the fused and the
   // two-phase kernels sum in different orders, and a sentence's result must

@@ -1,0 +1,9 @@
+run() { echo -n "$* : "; env "$@" python tools/decode_probe.py cfg2 3 | tail -1 | sed 's/.*device//'; }
+run AMUN_LANES=24
+run AMUN_LANES=32
+run AMUN_LANES=16
+run AMUN_LOGIT_PAIRS=24
+run AMUN_LOGIT_PAIRS=32
+run AMUN_LOGIT_PAIRS=56
+run AMUN_TC_CTAS=8
+run AMUN_TC_CTAS=16

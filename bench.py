@@ -17,9 +17,12 @@ Legs of the JSON line (rank 0 prints one line):
   e2e       the same metric through the public API Engine.translate_corpus
             on host text lines ("w<id>" tokens): text -> ids -> H2D -> decode
             -> D2H -> detokenised strings, CUDA-event timed, max over ranks.
-  roofline  the dominant kernel (logit projection + fused log-softmax
-            partials + top-k): algorithmic bytes / average launch duration
-            (CUDA events around every launch in the timed region).
+  roofline  the tensor-core kernel class with the largest in-situ share of
+            the machine: algorithmic FLOP per launch / in-situ launch
+            duration, measured in the timed mode itself (24 bucket lanes,
+            CUDA-graph replay) by device CTA-lifetime accounting
+            (AMUN_PROFILE_CTA_TIME), against the sustained bf16 peak; plus
+            the whole-pass tensor FLOP rate and every class's SM-time share.
   cpu_baseline  the CPU oracle port of the reference decoder (oracle/,
             reference algorithm in f64 numpy, sentence thread pool with BLAS
             pinned to 1 thread like engine.py:188-190) on a bounded sample of
@@ -300,10 +303,16 @@ def main() -> None:
     for i in range(len(local_sents)):
         h = out.hyps(i)[0]
         toks_local += len(h[0]) - (1 if h[2] else 0)
-    # Kernel durations: CUDA events cannot sit between the kernels of a graph
-    # replay, so one more pass runs eagerly with an event pair around every
-    # launch (all kernel classes) right after the timed region; the logits
-    # average and the per-class breakdown come from it.
+    # Kernel durations.  In the timed mode (24 bucket lanes replaying CUDA
+    # graphs concurrently) events cannot sit between the kernels of a graph,
+    # so one more pass in exactly that mode runs with device CTA-lifetime
+    # accounting (AMUN_PROFILE_CTA_TIME: every CTA adds globaltimer(exit) -
+    # globaltimer(entry) to its kernel class): the in-situ numbers below.  An
+    # eager single-lane pass with an event pair around every launch gives the
+    # launch counts and the kernels' isolated durations (secondary).
+    flush.fill_(0.25)
+    torch.cuda.synchronize()
+    insitu = decode(profile=_lib.PROFILE_CTA_TIME)
     flush.fill_(0.5)
     torch.cuda.synchronize()
     prof = decode(profile=0xFF)
@@ -313,19 +322,22 @@ def main() -> None:
     toks = allreduce(float(toks_local), "sum")
     value = toks / (ms_step / 1000.0)
 
-    # ---- roofline per tensor-core kernel class, headline = the dominant one
-    # (largest share of the eager pass).  Algorithmic work per launch
-    # (SURVEY §8(d)): FLOP = 2 x rows x (fp32 GEMM shape of
-    # the reference op); rows = average hypothesis rows per launch of the
-    # pass.  The kernels issue three fp16 MMAs per product (3xFP16 split),
-    # reported as "issued_frac".  Bytes = fp32-equivalent weight bytes once
-    # per launch (the hi/lo fp16 pair the kernel reads has the same size).
+    # ---- roofline per tensor-core kernel class, headline = the class with
+    # the largest in-situ share of the machine (CTA lifetime / (148 SMs x
+    # pass time)).  Algorithmic work per launch:
+    # FLOP = 2 x rows x (fp32 GEMM shape of the reference op); rows = average
+    # hypothesis rows per launch of the pass.  The kernels issue three fp16
+    # MMAs per product (3xFP16 split), reported as "issued_frac".  In-situ
+    # launch duration = mean CTA lifetime of the class (all CTAs of a launch
+    # are co-resident).  Peak: the sustained dense bf16 rate (kernels timed
+    # inside a long step; kind::f16 runs at the bf16 rate).
     peaks = {}
     pk = REPO / "MEASURED_PEAKS.json"
     if pk.exists():
         peaks = json.loads(pk.read_text())
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    tc_peak = peaks.get("bf16_tflops", 2250.0)  # kind::f16 runs at the bf16 dense rate
+    tc_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0))
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
     de, dh, da, V = W.D_EMB, W.D_H, W.D_ATT, W.V_TRG
     lens = sorted(len(s) for s in local_sents)
     rows_sum = n_launch = 0
@@ -342,26 +354,34 @@ def main() -> None:
         "deep_out": [(de + 3 * dh, de)],
         "logits": [(de, V)],
     }
+    pass_ms = insitu.device_ms
+    sm_ms = {k: insitu.kernel_ms[k] for k in _lib.KERNEL_CLASSES}
+    share = {k: round(v / (n_sm * pass_ms), 4) for k, v in sm_ms.items()}
     classes = {}
+    pass_flop = 0.0
     for cls, kn in shapes.items():
         n = kcount.get(cls, 0)
-        if not n:
+        ctas_tot = insitu.kernel_ctas.get(cls, 0)
+        if not n or not ctas_tot:
             continue
-        avg_ms = kms[cls] / n
         flop = sum(2.0 * rows * k * nn for k, nn in kn)
+        pass_flop += flop * n
         wbytes = sum(4.0 * k * nn for k, nn in kn)
-        ach = flop / (avg_ms / 1e3) / 1e12
-        ctas = prof.kernel_ctas.get(cls, 0) / n
-        classes[cls] = {"launches": int(n), "avg_launch_ms": round(avg_ms, 4), "gflop_per_launch": round(flop / 1e9, 3),
-                        "ctas_per_launch": round(ctas, 1),
-                        # fraction of the per-SM tensor peak on the SMs the launch occupies
-                        # (production runs 16 bucket lanes concurrently, each launch owns few SMs)
-                        "issued_frac_of_sms_used": round(3 * ach / tc_peak * 148 / ctas, 4) if ctas else None,
-                        "achieved_tflops": round(ach, 1), "frac": round(ach / tc_peak, 4),
-                        "issued_frac": round(3 * ach / tc_peak, 4),
-                        "weight_gbs": round(wbytes / (avg_ms / 1e3) / 1e9, 1),
-                        "share_of_step": round(kms[cls] / max(prof.device_ms, 1e-9), 3)}
-    dom = max(classes, key=lambda c: kms[c])
+        ctas = ctas_tot / n
+        dur_ms = sm_ms[cls] / ctas_tot  # mean CTA lifetime in situ
+        ach = flop / (dur_ms / 1e3) / 1e12
+        iso_ms = kms[cls] / n
+        classes[cls] = {"launches": int(n), "ctas_per_launch": round(ctas, 1),
+                        "gflop_per_launch": round(flop / 1e9, 3),
+                        "insitu_launch_ms": round(dur_ms, 4), "achieved_tflops": round(ach, 1),
+                        "frac": round(ach / tc_peak, 4), "issued_frac": round(3 * ach / tc_peak, 4),
+                        # issued tensor rate on the SMs the launch holds, vs their share of the peak
+                        "issued_frac_of_sms_used": round(3 * ach / tc_peak * n_sm / ctas, 4),
+                        "weight_gbs": round(wbytes / (dur_ms / 1e3) / 1e9, 1),
+                        "share_of_step": share[cls],
+                        "isolated_launch_ms": round(iso_ms, 4),
+                        "isolated_achieved_tflops": round(flop / (iso_ms / 1e3) / 1e12, 1)}
+    dom = max(classes, key=lambda c: sm_ms[c])
     d = classes[dom]
     traffic = None
     tf = REPO / "profiles" / f"{dom}_traffic.json"
@@ -370,16 +390,23 @@ def main() -> None:
     roofline = {"kernel": dom, "bound": "tensor", "achieved": d["achieved_tflops"], "peak": tc_peak,
                 "unit": "TFLOP/s", "frac": d["frac"], "traffic": traffic,
                 "issued_frac": d["issued_frac"], "issued_frac_of_sms_used": d["issued_frac_of_sms_used"],
-                "ctas_per_launch": d["ctas_per_launch"], "avg_launch_ms": d["avg_launch_ms"],
+                "ctas_per_launch": d["ctas_per_launch"], "avg_launch_ms": d["insitu_launch_ms"],
                 "gflop_per_launch": d["gflop_per_launch"], "rows_per_launch": round(rows, 1),
-                "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops; kind::f16 runs at the bf16 rate)"
+                "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops_sustained; kind::f16 runs at the bf16 rate)"
                 if pk.exists() else "fallback (nominal dense bf16)",
                 "share_of_step": d["share_of_step"],
-                "timing": "CUDA events around every launch in an eager single-lane pass right after the timed "
-                          "(graph-replay, 8-lane) region",
+                "timing": "in situ: the timed mode (24 bucket lanes, CUDA-graph replay) with device CTA-lifetime "
+                          "accounting (globaltimer per CTA, summed per kernel class); launch duration = mean CTA "
+                          "lifetime; share_of_step = class CTA time / (SMs x pass time)",
+                "whole_pass": {"tflop_per_pass": round(pass_flop / 1e12, 2),
+                               "achieved_tflops": round(pass_flop / (ms_step / 1e3) / 1e12, 1),
+                               "frac": round(pass_flop / (ms_step / 1e3) / 1e12 / tc_peak, 4),
+                               "issued_frac": round(3 * pass_flop / (ms_step / 1e3) / 1e12 / tc_peak, 4)},
                 "tensor_core_classes": classes,
+                "insitu_sm_share": share,
+                "insitu_pass_ms": round(pass_ms, 2),
                 "hbm_peak_gbs": hbm_peak,
-                "kernel_ms_per_step": breakdown,
+                "isolated_kernel_ms_per_step": breakdown,
                 "launches_per_step": {k: int(v) for k, v in prof.kernel_count.items()}}
 
     # ---- e2e through the public API (host text lines)

@@ -64,6 +64,11 @@ typedef struct {
 #define AMUN_K_LOGIT 6    /* logits + log-softmax partials + top-k */
 #define AMUN_K_SELECT 7   /* beam select / update / gather */
 #define AMUN_K_CLASSES 8
+/* amun_decode_opts.profile flag: device CTA-time accounting in the normal
+ * (multi-lane, graph-replay) mode -- kernel_ms[c] = summed CTA lifetimes
+ * (globaltimer, ms) and kernel_ctas[c] = CTAs of the class's tensor-core,
+ * attention and select kernels; no per-launch events, no single-lane mode */
+#define AMUN_PROFILE_CTA_TIME 0x40000000
 
 /* Result of amun_decode: per sentence up to n_best hypotheses, already
  * ranked by (-rank_score, tokens) like search.py:215. */

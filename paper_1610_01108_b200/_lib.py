@@ -58,6 +58,9 @@ class Result(ctypes.Structure):
 BUCKET_DONE = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.POINTER(Result), _i32p)
 
 KERNEL_CLASSES = ("encoder", "query", "attention", "gru_a", "gru_b", "deep_out", "logits", "select")
+# DecodeOpts.profile flag (include/amun_b200.h AMUN_PROFILE_CTA_TIME): device
+# CTA-lifetime accounting per kernel class in the normal multi-lane graph mode
+PROFILE_CTA_TIME = 0x40000000
 
 
 _lock = threading.Lock()

@@ -39,6 +39,33 @@ inline int &last_launch_ctas() {
   return n;
 }
 
+// In-situ CTA-time accounting (bench.py roofline in the timed multi-lane
+// graph-replay mode): a kernel whose args carry kt != nullptr adds, per CTA,
+// (globaltimer at exit - at entry) to kt[0] and 1 to kt[1].  The decode
+// driver points kt at its kernel class's slot (ktime_ptr(), set around every
+// launch by Ctx::run); nullptr (the default) costs one predicate per CTA.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct CtaClock {
+  unsigned long long *kt;
+  unsigned long long t0;
+  __device__ __forceinline__ explicit CtaClock(unsigned long long *p) : kt(p), t0(p && threadIdx.x == 0 ? gtimer() : 0ull) {}
+  // thread 0, after the CTA's last barrier
+  __device__ __forceinline__ void done() const {
+    if (kt && threadIdx.x == 0) {
+      atomicAdd(kt, gtimer() - t0);
+      atomicAdd(kt + 1, 1ull);
+    }
+  }
+};
+inline unsigned long long *&ktime_ptr() {
+  static thread_local unsigned long long *p = nullptr;
+  return p;
+}
+
 // Accurate transcendentals (SURVEY §7 hard part (f)): full-precision expf /
 // tanhf, never the .approx forms.
 __device__ __forceinline__ float sigmoid_acc(float x) { return 1.0f / (1.0f + expf(-x)); }

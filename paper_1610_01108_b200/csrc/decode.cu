@@ -158,6 +158,7 @@ struct Ctx {
   float **ws_keep = nullptr;  // when set, the buffer outlives the Ctx (pooled lane)
   size_t *ws_keep_n = nullptr;
   cudaMemPool_t ws_pool = nullptr;  // allocation pool of ws (nullptr: the device default)
+  unsigned long long *kt = nullptr;  // CTA-time accounting slots [class][2] (AMUN_PROFILE_CTA_TIME)
   explicit Ctx(cudaStream_t s) : st(s) {}
   ~Ctx() {
     for (auto e : pool) cudaEventDestroy(e);
@@ -198,6 +199,11 @@ struct Ctx {
   void run(int k, F &&f) {
     if (ablated() & (1u << k)) return;
     ++launches;
+    struct KtScope {  // kernels launched inside f() account their CTA time to class k
+      unsigned long long *prev;
+      KtScope(unsigned long long *p) : prev(ktime_ptr()) { ktime_ptr() = p; }
+      ~KtScope() { ktime_ptr() = prev; }
+    } kts(kt ? kt + 2 * k : nullptr);
     if (!(prof & (1u << k))) {
       f();
       return;
@@ -1056,10 +1062,22 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   // bucket is still one batch of <= max_batch sentences).
   const char *lanes_env = getenv("AMUN_LANES");
   int n_lanes = lanes_env ? std::max(1, atoi(lanes_env)) : 24;
-  if (o.profile) n_lanes = 1;  // per-launch event timing wants one ordered stream
+  const uint32_t prof_ev = (uint32_t)o.profile & 0xFFu;  // classes timed with per-launch events
+  const bool cta_time = (o.profile & AMUN_PROFILE_CTA_TIME) != 0;
+  if (prof_ev) n_lanes = 1;  // per-launch event timing wants one ordered stream
   n_lanes = std::max(1, std::min<int>(n_lanes, (int)buckets.size()));
   const char *no_graph = getenv("AMUN_NO_GRAPH");
-  const bool graphs_ok = o.profile == 0 && !(no_graph && no_graph[0] == '1');
+  const bool graphs_ok = prof_ev == 0 && !(no_graph && no_graph[0] == '1');
+  struct KtBuf {  // device CTA-time accumulators [class][ns, CTAs]
+    unsigned long long *p = nullptr;
+    ~KtBuf() {
+      if (p) cudaFree(p);
+    }
+  } ktb;
+  if (cta_time) {
+    AMUN_CUDA(cudaMalloc(&ktb.p, sizeof(unsigned long long) * 2 * AMUN_K_CLASSES));
+    AMUN_CUDA(cudaMemset(ktb.p, 0, sizeof(unsigned long long) * 2 * AMUN_K_CLASSES));
+  }
   constexpr int kProbeEvery = 8, kMaxAhead = 16;
 
   struct Lane {
@@ -1153,7 +1171,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     L.c->ws_keep = &L.res->ws;
     L.c->ws_keep_n = &L.res->ws_floats;
     L.c->ws_pool = ws_pool(L.dev);
-    L.c->prof = (uint32_t)o.profile;
+    L.c->prof = prof_ev;
+    L.c->kt = ktb.p;
     L.eb.resize(n_models);
     L.db.resize(n_models);
     L.fin_states.assign(n_models, nullptr);
@@ -1832,6 +1851,14 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     r->kernel_ms[i] = c.kms[i];
     r->kernel_count[i] = c.kcount[i];
     r->kernel_ctas[i] = c.kctas[i];
+  }
+  if (ktb.p) {  // CTA-time accounting replaces the (absent) event totals
+    unsigned long long h[2 * AMUN_K_CLASSES];
+    AMUN_CUDA(cudaMemcpy(h, ktb.p, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < AMUN_K_CLASSES; ++i) {
+      r->kernel_ms[i] = (double)h[2 * i] * 1e-6;
+      r->kernel_ctas[i] = (int64_t)h[2 * i + 1];
+    }
   }
   using ms_d = std::chrono::duration<double, std::milli>;
   r->host_setup_ms = ms_d(t_ev0 - t_enter).count();

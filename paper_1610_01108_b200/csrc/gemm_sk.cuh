@@ -82,6 +82,7 @@ struct SkArgs {
   int n_klim, nk_lim;  // CTA pairs at features >= n_klim run only the first nk_lim K blocks
   int debug;  // microbenchmark knobs: 1 skip weight loads, 2 skip activation loads, 4 skip MMA, 8 skip reduction
   int row_off1;  // first activation row of segment 1 (segment 2 and the epilogue rows start at 0)
+  unsigned long long *kt;  // optional CTA-time accounting (common.cuh CtaClock)
 };
 
 // Row layout of one pass: one MMA of N0 columns, or two (N0 + N1) when the
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(C::kThreads, 1)
                    const __grid_constant__ CUtensorMap x2h, const __grid_constant__ CUtensorMap x2l, SkArgs a,
                    Epi epi) {
   constexpr int CG = C::kCG;
+  const CtaClock clk(a.kt);
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = tc::align_smem<1024>(smem_raw);  // stays in the shared address space (LDS/STS)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
@@ -343,6 +345,7 @@ __global__ void __launch_bounds__(C::kThreads, 1)
     else
       tc::tmem_dealloc<512>(tmem);
   }
+  clk.done();  // every thread passed the final cluster barrier
 }
 
 // Activation segment s: hi/lo [rows, k_s] with row pitch lda_s (elements),
@@ -400,6 +403,7 @@ void launch_gemm_sk(const SkMaps &maps, int M, int splits, const Epi &epi, cudaS
   a.nk_lim = maps.k_lim > 0 ? ceil_div(maps.k_lim, C::kBK) : a.nk1 + a.nk2;
   a.debug = debug;
   a.row_off1 = row_off1;
+  a.kt = ktime_ptr();
   zgrid = std::max(1, std::min(zgrid, ceil_div(M, C::kPR)));
   auto kern = gemm_sk_kernel<C, Epi>;
   static bool attr[64] = {};

@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
 // the SMs left by the other lanes' tensor-core kernels.
 template <int KA>
 __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArgs a) {
+  const CtaClock clk(a.kt);
   extern __shared__ float sm[];
   const int b = blockIdx.x;
   if (a.n_act && a.done[b]) return;
@@ -478,13 +479,19 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
       store_split(a.ctx_hi, a.ctx_lo, oh + 3, acc[r].w);
     }
   }
+  if (a.kt) {
+    __syncthreads();
+    clk.done();
+  }
 }
 
 template <int KA>
 static void launch_sent(const AttnArgs &a, int B, size_t smem, cudaStream_t st) {
   auto kern = attn_sent_kernel<KA>;
   if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<B, 512, smem, st>>>(a);
+  AttnArgs ak = a;
+  ak.kt = ktime_ptr();
+  kern<<<B, 512, smem, st>>>(ak);
 }
 
 template <int KA>
@@ -773,6 +780,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   int *c_tok = reinterpret_cast<int *>(c_lp + (size_t)k * sa.kk);
   __shared__ int s_nch, s_newna, s_nfin;
 
+  const CtaClock kclk(sa.kt);
   long long clk0 = clock64();
   const int b = blockIdx.x;
   if (bs.done[b]) return;
@@ -1111,6 +1119,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   }
   __syncthreads();
   if (sa.dbg && threadIdx.x == 0) { atomicAdd(sa.dbg + 3, (unsigned long long)(clock64() - clk0)); atomicAdd(sa.dbg + 4, 1ull); }
+  kclk.done();
 }
 
 template <int KMAX, bool FUSED>
@@ -1118,7 +1127,9 @@ static void launch_select_t(const SelectArgs &sa, const BeamState &bs, const Mod
                             cudaStream_t st) {
   auto kern = select_kernel<KMAX, FUSED>;
   if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<bs.B, 256, smem, st>>>(sa, bs, mr);
+  SelectArgs sk = sa;
+  sk.kt = ktime_ptr();
+  kern<<<bs.B, 256, smem, st>>>(sk, bs, mr);
   AMUN_CHECK_LAUNCH();
 }
 

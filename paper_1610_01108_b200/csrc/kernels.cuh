@@ -29,6 +29,7 @@ struct AttnArgs {
   int ldctx_h = 0;
   float *energy = nullptr;  // scratch [R][jmax]: enables the two-phase sentence kernels
   const float *EQ = nullptr;  // e^{2q} rows (same layout as Q), from the query GEMM epilogue
+  unsigned long long *kt = nullptr;  // optional CTA-time accounting (common.cuh CtaClock)
 };
 // returns the number of kernels launched
 int launch_attention(const AttnArgs &a, int R, cudaStream_t st);
@@ -99,6 +100,7 @@ struct SelectArgs {
   double *cand_lp;  // scratch [B*k*kk]
   int *cand_tok;
   unsigned long long *dbg = nullptr;  // profiling: summed clock64 per phase [6] (env AMUN_DEBUG_SELECT)
+  unsigned long long *kt = nullptr;   // optional CTA-time accounting (common.cuh CtaClock)
 };
 // search.py:161-198 for one step of every sentence of the bucket.
 void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, cudaStream_t st);

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(rThreads, 1)
     logits_rows_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
                        LogitTcArgs a, int C) {
+  const CtaClock clk(a.kt);
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = tc::align_smem<1024>(smem_raw);
   float *stash = reinterpret_cast<float *>(smem + rStages * rStageB);
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(rThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   if (C > 1) tc::cluster_sync();  // no CTA leaves while a peer may still multicast into it
+  clk.done();
   tc::tc_fence_after();
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
 }
@@ -419,7 +421,9 @@ void launch_t(const LogitTcMaps &maps, const LogitTcArgs &a, cudaStream_t st) {
   cfg.attrs = la;
   cfg.numAttrs = 1;
   last_launch_ctas() = (int)cfg.gridDim.x;
-  AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, a, C));
+  LogitTcArgs ak = a;
+  ak.kt = ktime_ptr();
+  AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, ak, C));
 }
 
 }  // namespace

@@ -169,6 +169,7 @@ struct MapSet {
 template <int KK, int NMX>
 __global__ void __launch_bounds__(kThreads, 1)
     logits_pair_kernel(const __grid_constant__ MapSet<NMX> mp, LogitTcArgs a) {
+  const CtaClock clk(a.kt);
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = tc::align_smem<1024>(smem_raw);  // stays in the shared address space (LDS/STS)
   float *tr = reinterpret_cast<float *>(smem + kStages * kStageB);  // [group][32][kTrRow]
@@ -520,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::cluster_sync();  // no CTA leaves while its pair may still signal it
+  clk.done();
   tc::tc_fence_after();
   if (warp == 1) tc::tmem_dealloc_pair<512>(tmem);
 }
@@ -578,7 +580,9 @@ void launch_t(const LogitTcMaps *maps, const LogitTcArgs &a, cudaStream_t st) {
   cfg.attrs = la;
   cfg.numAttrs = 1;
   last_launch_ctas() = (int)cfg.gridDim.x;
-  AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, mp, a));
+  LogitTcArgs ak = a;
+  ak.kt = ktime_ptr();
+  AMUN_CUDA(cudaLaunchKernelEx(&cfg, kern, mp, ak));
 }
 
 }  // namespace

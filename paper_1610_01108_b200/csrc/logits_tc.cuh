@@ -32,6 +32,7 @@ struct LogitTcArgs {
   const float *bias_x[3] = {nullptr, nullptr, nullptr};
   float unscale_x[3] = {0.f, 0.f, 0.f};
   long long pm_stride = 0;
+  unsigned long long *kt = nullptr;  // optional CTA-time accounting (common.cuh CtaClock)
   int debug_flags = 0;  // microbenchmark knobs: 1 skip A loads, 2 skip B loads, 4 skip MMA, 8 skip epilogue
   long long *debug_clock = nullptr;  // microbenchmark: per-chunk clock64 stamps of CTA 0
 };

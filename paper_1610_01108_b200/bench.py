@@ -1,16 +1,21 @@
-"""Throughput / latency measurement API (reference: beamnmt/bench.py:23-140).
+"""Measurement API of the package: throughput, latency and beam sweeps over an
+Engine (drop-in for beamnmt.bench, reference pkg/src/beamnmt/bench.py:23-140).
 
-Same report fields and definitions: words_per_second counts post-BPE SOURCE
-tokens over decode wall time, model load excluded (bench.py:46-51, :73-77).
-`target_words_per_second` (1-best target tokens, final </s> excluded) is
-added because the B200 headline metric is target words/s.
+Definitions kept from the reference so reports compare one to one:
+`words_per_second` is post-BPE SOURCE tokens per second of decode wall time
+(bench.py:46-51), model loading is excluded and reported as
+`startup_seconds`, latency decodes strictly one sentence per call.  Added for
+the GPU decoder: `target_words_per_second` (1-best target tokens, final
+`</s>` excluded -- the B200 headline metric) and `device_seconds`, the
+decoder's own CUDA-event time over the engine calls of the measurement
+(the part of the wall time spent on the device).
 """
 
 from __future__ import annotations
 
 import time
 from dataclasses import asdict, dataclass
-from typing import Sequence
+from typing import Callable, Sequence
 
 from .engine import Engine, TranslationResult
 
@@ -28,49 +33,76 @@ class BenchReport:
     startup_seconds: float
     target_tokens: int = 0
     target_words_per_second: float = 0.0
+    device_seconds: float = 0.0
 
     def to_dict(self) -> dict:
         return asdict(self)
 
 
-def _report(engine: Engine, results: Sequence[TranslationResult], wall: float, threads: int,
-            beam: int) -> BenchReport:
-    src = sum(r.src_tokens for r in results)
-    trg = sum(len(r.text.split()) for r in results)
-    wall = max(wall, 1e-9)
-    return BenchReport(total_tokens=src, wall_seconds=wall, words_per_second=src / wall,
-                       ms_per_sentence=1000.0 * wall / len(results), sentence_count=len(results),
-                       threads=threads, beam=beam, shortlist_active=engine.shortlist_active,
-                       startup_seconds=engine.startup_seconds, target_tokens=trg,
-                       target_words_per_second=trg / wall)
+class _Measured:
+    """Runs `fn` (returning the results and the device milliseconds of its
+    engine calls) once, after an optional untimed warm-up call."""
+
+    def __init__(self, fn: Callable[[], tuple[list[TranslationResult], float]], warmup: bool):
+        if warmup:
+            fn()
+        t0 = time.perf_counter()
+        self.results, self.device_ms = fn()
+        self.wall = max(time.perf_counter() - t0, 1e-9)
+
+    def report(self, engine: Engine, threads: int, beam: int) -> BenchReport:
+        res = self.results
+        src = sum(r.src_tokens for r in res)
+        trg = sum(len(r.text.split()) for r in res)
+        return BenchReport(total_tokens=src, wall_seconds=self.wall, words_per_second=src / self.wall,
+                           ms_per_sentence=1e3 * self.wall / len(res), sentence_count=len(res), threads=threads,
+                           beam=beam, shortlist_active=engine.shortlist_active,
+                           startup_seconds=engine.startup_seconds, target_tokens=trg,
+                           target_words_per_second=trg / self.wall, device_seconds=self.device_ms / 1e3)
+
+
+def _device_ms(engine: Engine) -> float:
+    """Device time of the engine's last call: its devices decode concurrently,
+    so the longest one (empty calls decode nothing)."""
+    return max(engine.last_stats.get("device_ms") or [0.0])
+
+
+def _check_corpus(corpus: Sequence[str]) -> None:
+    if len(corpus) == 0:
+        raise ValueError("benchmark corpus is empty")
 
 
 def throughput_bench(engine: Engine, corpus: Sequence[str], threads: int,
                      warmup: bool = False) -> tuple[BenchReport, list[TranslationResult]]:
-    if len(corpus) == 0:
-        raise ValueError("benchmark corpus is empty")
+    """The whole corpus through one translate_corpus call (the GPU engine
+    batches it into length buckets; `threads` is kept for the reference's
+    signature and report)."""
+    _check_corpus(corpus)
     if threads < 1:
         raise ValueError(f"threads must be >= 1, got {threads}")
-    if warmup:
-        engine.translate_corpus(corpus, threads=threads)
-    t0 = time.perf_counter()
-    results = engine.translate_corpus(corpus, threads=threads)
-    wall = time.perf_counter() - t0
-    return _report(engine, results, wall, threads, engine.opts.beam_size), results
+
+    def once():
+        res = engine.translate_corpus(corpus, threads=threads)
+        return res, _device_ms(engine)
+
+    m = _Measured(once, warmup)
+    return m.report(engine, threads, engine.opts.beam_size), m.results
 
 
 def latency_bench(engine: Engine, corpus: Sequence[str],
                   warmup: bool = False) -> tuple[BenchReport, list[TranslationResult]]:
-    """Sentences strictly one at a time (batch of one per call)."""
-    if len(corpus) == 0:
-        raise ValueError("benchmark corpus is empty")
-    if warmup:
+    """One sentence per translate_line call, in corpus order."""
+    _check_corpus(corpus)
+
+    def serial():
+        out, dev = [], 0.0
         for line in corpus:
-            engine.translate_line(line)
-    t0 = time.perf_counter()
-    results = [engine.translate_line(line) for line in corpus]
-    wall = time.perf_counter() - t0
-    return _report(engine, results, wall, 1, engine.opts.beam_size), results
+            out.append(engine.translate_line(line))
+            dev += _device_ms(engine)
+        return out, dev
+
+    m = _Measured(serial, warmup)
+    return m.report(engine, 1, engine.opts.beam_size), m.results
 
 
 SWEEP_HEADER = ["beam", "words_per_second", "bleu", "mean_model_score"]
@@ -78,19 +110,20 @@ SWEEP_HEADER = ["beam", "words_per_second", "bleu", "mean_model_score"]
 
 def beam_sweep(engine: Engine, corpus: Sequence[str], beams: Sequence[int], references=None,
                threads: int | None = None) -> list[dict]:
-    """Throughput per beam size (bleu is not computed by this package)."""
-    if len(beams) == 0:
+    """Source words/s and mean model score per beam size.  BLEU is outside
+    the decoder's scope: the column is kept and left empty."""
+    if not len(beams):
         raise ValueError("beam list is empty")
-    if any(b < 1 for b in beams):
+    bad = [b for b in beams if b < 1]
+    if bad:
         raise ValueError(f"beam sizes must be >= 1, got {list(beams)}")
     if references is not None and len(references) != len(corpus):
         raise ValueError(f"line count mismatch: {len(corpus)} corpus vs {len(references)} references")
-    rows = []
+    table = []
     for beam in beams:
         opts = engine.with_options(beam_size=beam)
-        t0 = time.perf_counter()
-        results = engine.translate_corpus(corpus, opts=opts)
-        wall = max(time.perf_counter() - t0, 1e-9)
-        rows.append({"beam": beam, "words_per_second": sum(r.src_tokens for r in results) / wall, "bleu": None,
-                     "mean_model_score": sum(r.score for r in results) / len(results)})
-    return rows
+        m = _Measured(lambda: (engine.translate_corpus(corpus, opts=opts), 0.0), False)
+        res = m.results
+        table.append(dict(zip(SWEEP_HEADER, (beam, sum(r.src_tokens for r in res) / m.wall, None,
+                                             sum(r.score for r in res) / len(res)))))
+    return table

@@ -547,3 +547,27 @@ def test_ensemble_decode_matches_reference(gpu, full, name):
     assert prof.kernel_count["logits"] == prof.decoder_steps, (prof.kernel_count, prof.decoder_steps)
     for i in range(3):
         assert prof.hyps(i) == out.hyps(i)
+
+
+def test_bench_api_through_engine(gpu, full):
+    """paper_1610_01108_b200.bench on the real Engine (reference
+    pkg/src/beamnmt/bench.py:74-126): the throughput report counts the
+    corpus's source tokens and its 1-best target words, and the decoder's
+    device time is part of the wall time."""
+    from paper_1610_01108_b200 import workload as W
+    from paper_1610_01108_b200.bench import latency_bench, throughput_bench
+    from paper_1610_01108_b200.engine import Engine, EngineConfig
+    from paper_1610_01108_b200.model import Vocabulary
+
+    sents = W.WORKLOADS["cfg2"].corpus()[:40]
+    lines = W.lines_of(sents)
+    vocab = Vocabulary.from_tokens([f"w{i}" for i in range(2, W.V_SRC)])
+    eng = Engine(EngineConfig(model_paths=("<memory>",), src_vocab_path="<memory>", trg_vocab_path="<memory>",
+                              devices=(0,), max_batch=16), [full], vocab, vocab, None, None, None, 0, 0.0)
+    rep, res = throughput_bench(eng, lines, threads=4, warmup=True)
+    assert rep.total_tokens == sum(map(len, sents)) and rep.sentence_count == 40
+    assert rep.target_tokens == sum(len(r.text.split()) for r in res) > 0
+    assert 0 < rep.device_seconds <= rep.wall_seconds
+    lrep, lres = latency_bench(eng, lines[:4])
+    assert [r.text for r in lres] == [r.text for r in res[:4]]
+    assert 0 < lrep.device_seconds <= lrep.wall_seconds

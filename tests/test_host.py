@@ -263,3 +263,66 @@ def test_engine_vectorised_texts_match_detokenize():
     res = SimpleNamespace(tokens=flat, tok_offsets=offs, finished=np.array([f for _, f in hyps]),
                           scores=np.zeros(len(hyps)))
     assert eng._hyp_texts(res) == [eng._detokenize(t, f) for t, f in hyps]
+
+
+class _StubEngine:
+    """Engine stand-in for the measurement API (no decoding): every line
+    'a b c' translates to 'x y' with score -1, and each call reports 2 ms of
+    device time on two devices (the longer one counts)."""
+
+    def __init__(self):
+        from paper_1610_01108_b200 import DecodeOptions
+
+        self.opts = DecodeOptions(beam_size=5)
+        self.shortlist_active = False
+        self.startup_seconds = 0.25
+        self.last_stats = {}
+        self.calls = 0
+
+    def translate_corpus(self, lines, threads=None, opts=None):
+        from paper_1610_01108_b200.engine import TranslationResult
+
+        self.calls += 1
+        self.last_stats = {"device_ms": [1.0, 2.0]}
+        return [TranslationResult("x y", -1.0, [(-1.0, "x y")], len(line.split()), 0) for line in lines]
+
+    def translate_line(self, line, opts=None):
+        return self.translate_corpus([line], opts=opts)[0]
+
+    def with_options(self, **changes):
+        from dataclasses import replace
+
+        return replace(self.opts, **changes)
+
+
+def test_bench_api_reports_and_validation():
+    """paper_1610_01108_b200.bench keeps the reference's report definitions
+    (pkg/src/beamnmt/bench.py:39-126): source words over decode wall time,
+    startup excluded; adds target words/s and the engine's device time."""
+    from paper_1610_01108_b200.bench import beam_sweep, latency_bench, throughput_bench
+
+    eng = _StubEngine()
+    corpus = ["a b c", "d e", "f"]
+    rep, res = throughput_bench(eng, corpus, threads=3, warmup=True)
+    assert eng.calls == 2 and len(res) == 3
+    assert rep.total_tokens == 6 and rep.target_tokens == 6 and rep.sentence_count == 3
+    assert math.isclose(rep.words_per_second, 6 / rep.wall_seconds)
+    assert math.isclose(rep.target_words_per_second, 6 / rep.wall_seconds)
+    assert rep.device_seconds == pytest.approx(0.002) and rep.threads == 3 and rep.beam == 5
+    assert rep.startup_seconds == 0.25 and rep.to_dict()["ms_per_sentence"] == pytest.approx(1e3 * rep.wall_seconds / 3)
+    lrep, _ = latency_bench(eng, corpus)
+    assert lrep.threads == 1 and lrep.device_seconds == pytest.approx(0.006)
+    rows = beam_sweep(eng, corpus, [1, 4])
+    assert [r["beam"] for r in rows] == [1, 4] and all(r["bleu"] is None and r["mean_model_score"] == -1.0 for r in rows)
+    with pytest.raises(ValueError, match="benchmark corpus is empty"):
+        throughput_bench(eng, [], threads=1)
+    with pytest.raises(ValueError, match="threads must be >= 1"):
+        throughput_bench(eng, corpus, threads=0)
+    with pytest.raises(ValueError, match="benchmark corpus is empty"):
+        latency_bench(eng, [])
+    with pytest.raises(ValueError, match="beam list is empty"):
+        beam_sweep(eng, corpus, [])
+    with pytest.raises(ValueError, match="beam sizes must be >= 1"):
+        beam_sweep(eng, corpus, [2, 0])
+    with pytest.raises(ValueError, match="line count mismatch"):
+        beam_sweep(eng, corpus, [2], references=["r"])

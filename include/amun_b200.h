@@ -180,6 +180,22 @@ int amun_decoder_step_fused(amun_model *m, int32_t B, int32_t k, const float *s,
                             float *s_out, float *pmax_out, float *psum_out, float *cval_out, int32_t *ctok_out,
                             float *alpha_out);
 
+/* ---- host text front-end: replaces the per-line source_tokens ->
+ * Vocabulary.ids_and_oov loop of Engine.translate_corpus (engine.py:144-164,
+ * model.py Vocabulary: <unk> for unknown tokens, OOV counted) -------------
+ * A vocabulary handle holds token i = bytes[offsets[i], offsets[i+1]) (UTF-8,
+ * no duplicates).  amun_vocab_encode splits each line of `text` (line l =
+ * bytes [line_off[l], line_off[l+1])) exactly like Python's str.split() (all
+ * Unicode whitespace) -- the caller applies the preprocessing's lowercasing
+ * first -- and writes the ids of all lines back to back (unk_id for tokens
+ * outside the vocabulary; ids_cap entries available), the token count and
+ * OOV count of every line, and the total in *n_ids. */
+typedef struct amun_vocab amun_vocab;
+int amun_vocab_create(const char *bytes, const int64_t *offsets, int32_t n_tokens, amun_vocab **out);
+int amun_vocab_destroy(amun_vocab *v);
+int amun_vocab_encode(const amun_vocab *v, const char *text, const int64_t *line_off, int32_t n_lines,
+                      int32_t unk_id, int32_t *ids, int64_t ids_cap, int32_t *lens, int32_t *oov, int64_t *n_ids);
+
 #ifdef __cplusplus
 }
 #endif

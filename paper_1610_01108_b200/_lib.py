@@ -28,7 +28,7 @@ EXPORTS = (
     "amun_last_error", "amun_version", "amun_device_count", "amun_model_create", "amun_model_destroy",
     "amun_model_device_bytes", "amun_decode", "amun_result_free", "amun_encode", "amun_attention",
     "amun_decoder_step", "amun_init_state", "amun_gru_cell", "amun_decode_stream", "amun_encode_batch",
-    "amun_decoder_step_fused",
+    "amun_decoder_step_fused", "amun_vocab_create", "amun_vocab_destroy", "amun_vocab_encode",
 )
 
 _i32, _i64, _f32p, _f64p, _i32p = ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_float), \
@@ -102,7 +102,8 @@ def load() -> ctypes.CDLL:
         lib.amun_decoder_step_fused.argtypes = [ctypes.c_void_p, _i32, _i32, _f32p, _i32p, _f32p, _f32p, _i32p,
                                                 _i32, _i32, _f32p, _f32p, _f32p, _f32p, _i32p, _f32p]
         for name in EXPORTS:
-            if name not in ("amun_last_error", "amun_version", "amun_model_destroy", "amun_result_free"):
+            if name not in ("amun_last_error", "amun_version", "amun_model_destroy", "amun_result_free",
+                            "amun_vocab_destroy"):
                 getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -351,12 +352,19 @@ class DecodeOut:
 def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], beam_size: int,
            max_len_factor: int, max_len_offset: int, length_normalize: bool, n_best: int,
            shortlists: Sequence[np.ndarray] | None = None, want_states: bool = False, max_batch: int = 64,
-           force_full_logits: bool = False, profile: bool = False, on_bucket=None) -> DecodeOut:
+           force_full_logits: bool = False, profile: bool = False, on_bucket=None,
+           flat: tuple[np.ndarray, np.ndarray] | None = None) -> DecodeOut:
+    """Decode a batch of sentences (lists of source ids), or with `flat` =
+    (ids, lens) the already concatenated ids and per-sentence lengths."""
     lib = load()
-    lens = np.asarray([len(s) for s in sentences], dtype=np.int32)
-    ids = (np.concatenate([np.asarray(s, dtype=np.int32) for s in sentences]) if len(sentences)
-           else np.zeros(0, np.int32))
-    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    if flat is not None:
+        ids = np.ascontiguousarray(flat[0], dtype=np.int32)
+        lens = np.ascontiguousarray(flat[1], dtype=np.int32)
+    else:
+        lens = np.asarray([len(s) for s in sentences], dtype=np.int32)
+        ids = (np.concatenate([np.asarray(s, dtype=np.int32) for s in sentences]) if len(sentences)
+               else np.zeros(0, np.int32))
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
     sl_ids = sl_len = None
     if shortlists is not None:
         sl_len = np.asarray([len(s) for s in shortlists], dtype=np.int32)
@@ -370,7 +378,7 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
     sl_p = None if sl_ids is None else _ptr(sl_ids, _i32p)
     sl_l = None if sl_len is None else _ptr(sl_len, _i32p)
     if on_bucket is None:
-        check(lib.amun_decode(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(sentences), sl_p, sl_l,
+        check(lib.amun_decode(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(lens), sl_p, sl_l,
                               ctypes.byref(opts), ctypes.byref(res)))
     else:
         # finished buckets are handed to on_bucket(sentence indices, DecodeOut)
@@ -389,7 +397,7 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
                 errors.append(e)
 
         cb = BUCKET_DONE(_cb)
-        check(lib.amun_decode_stream(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(sentences), sl_p,
+        check(lib.amun_decode_stream(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(lens), sl_p,
                                      sl_l, ctypes.byref(opts), cb, None, ctypes.byref(res)))
         if errors:
             lib.amun_result_free(res)
@@ -401,3 +409,40 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
         lib.amun_result_free(res)
     out.call_ms = 1e3 * (t_ret - t_call)  # the C call, wall (vs device_ms inside it)
     return out
+
+
+class NativeVocab:
+    """Host vocabulary handle of the native text front-end (text.cu): maps
+    whole corpora of lines to source ids in one call."""
+
+    def __init__(self, tokens: Sequence[str]):
+        lib = load()
+        enc = [t.encode("utf-8", "surrogatepass") for t in tokens]
+        offs = np.zeros(len(enc) + 1, dtype=np.int64)
+        np.cumsum([len(b) for b in enc], out=offs[1:])
+        buf = b"".join(enc)
+        self.handle = ctypes.c_void_p()
+        check(lib.amun_vocab_create(buf, _ptr(offs, ctypes.POINTER(ctypes.c_int64)), len(enc),
+                                    ctypes.byref(self.handle)))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _lib is not None:
+            _lib.amun_vocab_destroy(h)
+            self.handle = None
+
+    def encode(self, lines: Sequence[str], lowercase: bool, unk_id: int):
+        """(ids int32 [sum lens], lens int32 [n], oov int32 [n]) of the lines,
+        split like preprocess() (str.lower() first when lowercase)."""
+        enc = [(ln.lower() if lowercase else ln).encode("utf-8", "surrogatepass") for ln in lines]
+        offs = np.zeros(len(enc) + 1, dtype=np.int64)
+        np.cumsum([len(b) for b in enc], out=offs[1:])
+        buf = b"".join(enc)
+        ids = np.empty(int(offs[-1]) + 1, dtype=np.int32)  # a token has >= 1 byte
+        lens = np.empty(len(enc), dtype=np.int32)
+        oov = np.empty(len(enc), dtype=np.int32)
+        n = ctypes.c_int64()
+        check(load().amun_vocab_encode(self.handle, buf, _ptr(offs, ctypes.POINTER(ctypes.c_int64)), len(enc), unk_id,
+                                       _ptr(ids, _i32p), ids.size, _ptr(lens, _i32p), _ptr(oov, _i32p),
+                                       ctypes.byref(n)))
+        return ids[:n.value], lens, oov

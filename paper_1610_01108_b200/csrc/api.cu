@@ -17,6 +17,8 @@
 using namespace amun;
 
 static thread_local std::string g_last_error;
+// shared with the other C-ABI translation units (text.cu)
+void amun_set_last_error(const std::string &m) { g_last_error = m; }
 // live model handles per device: the pooled decode lanes of a device are
 // released when its last handle is destroyed
 static std::atomic<int> g_live_models[64];

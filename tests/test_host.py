@@ -326,3 +326,40 @@ def test_bench_api_reports_and_validation():
         beam_sweep(eng, corpus, [2, 0])
     with pytest.raises(ValueError, match="line count mismatch"):
         beam_sweep(eng, corpus, [2], references=["r"])
+
+
+def test_native_text_front_end_matches_python_path():
+    """text.cu (amun_vocab_encode) splits like preprocess() = str.lower() +
+    str.split() (every Unicode whitespace, engine.py:144-164) and maps tokens
+    like Vocabulary.ids_and_oov (<unk> + OOV count) -- host-only code, no GPU."""
+    from paper_1610_01108_b200 import _lib
+    from paper_1610_01108_b200.model import UNK_ID, Vocabulary
+    from paper_1610_01108_b200.subword import preprocess
+
+    vocab = Vocabulary.from_tokens(["a", "b", "ça", "日本", "x​y", "Z", "</s>x", "𝒜"])
+    nv = _lib.NativeVocab(vocab.tokens)
+    ws = [" ", "\t", "\n", "\r", "\x0b", "\x0c", "\x1c", "\x1d", "\x1e", "\x1f", "\x85", "\xa0", " ",
+          " ", " ", " ", " ", " ", " ", " ", "　"]
+    rng = np.random.default_rng(5)
+    words = ["a", "b", "ÇA", "日本", "x​y", "z", "Z", "</s>", "</s>x", "𝒜", "oov", "Á", "ß", ""]
+    lines = ["", "   ", "a b", "A  B\tça", "　日本　", "x​y"]
+    for _ in range(300):
+        n = int(rng.integers(0, 9))
+        parts = [words[int(rng.integers(len(words)))] for _ in range(n)]
+        seps = [ws[int(rng.integers(len(ws)))] * int(rng.integers(1, 3)) for _ in range(n + 1)]
+        lines.append("".join(s + p for s, p in zip(seps, parts + [""])))
+    for lower in (True, False):
+        ids, lens, oov = nv.encode(lines, lower, UNK_ID)
+        want_ids, want_lens, want_oov = [], [], []
+        for line in lines:
+            i, o = vocab.ids_and_oov(preprocess(line, lower))
+            want_ids += i
+            want_lens.append(len(i))
+            want_oov.append(o)
+        assert ids.tolist() == want_ids and lens.tolist() == want_lens and oov.tolist() == want_oov
+    big = lines * 12  # > 512 lines: the multi-threaded slices, concatenated in order
+    ids, lens, oov = nv.encode(big, True, UNK_ID)
+    assert lens.tolist() == [len(preprocess(x)) for x in big]
+    assert ids.tolist() == [i for x in big for i in vocab.ids_and_oov(preprocess(x))[0]]
+    with pytest.raises(ValueError, match="duplicate"):
+        _lib.NativeVocab(["</s>", "<unk>", "a", "a"])

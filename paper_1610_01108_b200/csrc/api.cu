@@ -76,38 +76,111 @@ static T *upload_t(amun_model *m, const std::vector<T> &h) {
   return d;
 }
 
-// [K, N] row-major host matrix -> device [N, Kp] (K-major, row pitch Kp)
-// 3xFP16 hi/lo copies for the tensor-core GEMMs (common.cuh split_h): the
-// matrix is scaled by 2^sw with max|W| 2^sw < 2^14 (fp16 max 65504, and lo
-// stays normal for |W| >= 2^-17 max|W|), hi = fp16(W'), lo = fp16(W' - hi).
-// Source row k lands in column kmap(k) (the padded decoder-row layout);
-// unused columns are zero.  Returns the epilogue's inverse scale
-// 2^-(sw + kXShift).
-template <class KMap>
-static float upload_kmajor_split(amun_model *m, const float *W, int K, int N, int Kp, KMap kmap, __half **hi_out,
-                                 __half **lo_out) {
-  float mx = 0.f;
-  for (size_t i = 0; i < (size_t)K * N; ++i) mx = std::max(mx, std::fabs(W[i]));
+// max |W| over n floats (non-negative float bits order like unsigned ints)
+__global__ void absmax_kernel(const float *__restrict__ W, size_t n, unsigned *out) {
+  float m = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(W[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// W [K, N] row-major (device) -> hi/lo [N, Kp] K-major through 32 x 32
+// shared-memory tiles (coalesced on both sides); source row k lands in
+// column k < split ? k : k + pad
+__global__ void kmajor_split_kernel(const float *__restrict__ W, int K, int N, int Kp, int split, int pad, float sc,
+                                    __half *__restrict__ hi, __half *__restrict__ lo) {
+  __shared__ float tile[32][33];
+  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int k = k0 + j, n = n0 + threadIdx.x;
+    tile[j][threadIdx.x] = (k < K && n < N) ? W[(size_t)k * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int n = n0 + j, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      const float x = tile[threadIdx.x][j] * sc;
+      const __half h = __float2half_rn(x);
+      const size_t o = (size_t)n * Kp + (k < split ? k : k + pad);
+      hi[o] = h;
+      lo[o] = __float2half_rn(x - __half2float(h));
+    }
+  }
+}
+
+static float device_absmax(const float *d, size_t n);
+
+// [K, N] row-major DEVICE matrix -> device [N, Kp] (K-major, row pitch Kp)
+// 3xFP16 hi/lo copies for the tensor-core GEMMs (common.cuh split_h), built
+// on the device from the fp32 copy: the matrix is scaled by 2^sw with
+// max|W| 2^sw < 2^14 (fp16 max 65504, and lo stays normal for |W| >=
+// 2^-17 max|W|), hi = fp16(W'), lo = fp16(W' - hi).  Source row k lands in
+// column k < split ? k : k + pad (the padded decoder-row layout); unused
+// columns are zero.  Returns the epilogue's inverse scale 2^-(sw + kXShift).
+static float split_kmajor_dev(amun_model *m, const float *dW, int K, int N, int Kp, int split, int pad,
+                              __half **hi_out, __half **lo_out) {
+  const size_t n = (size_t)N * Kp;
+  __half *hi = nullptr, *lo = nullptr;
+  AMUN_CUDA(cudaMalloc(&hi, n * sizeof(__half)));
+  m->allocs.push_back(hi);
+  AMUN_CUDA(cudaMalloc(&lo, n * sizeof(__half)));
+  m->allocs.push_back(lo);
+  m->bytes += (int64_t)(2 * n * sizeof(__half));
+  AMUN_CUDA(cudaMemset(hi, 0, n * sizeof(__half)));
+  AMUN_CUDA(cudaMemset(lo, 0, n * sizeof(__half)));
+  const float mx = device_absmax(dW, (size_t)K * N);
   int e = 0;
   if (mx > 0.f) std::frexp(mx, &e);  // mx < 2^e
   const int sw = mx > 0.f ? 14 - e : 0;
-  const float sc = std::ldexp(1.f, sw);
-  std::vector<__half> hi((size_t)N * Kp, __float2half_rn(0.f)), lo((size_t)N * Kp, __float2half_rn(0.f));
-  for (int k = 0; k < K; ++k) {
-    const size_t kc = (size_t)kmap(k);
-    for (int n = 0; n < N; ++n) {
-      const float x = W[(size_t)k * N + n] * sc;
-      const __half h = __float2half_rn(x);
-      hi[(size_t)n * Kp + kc] = h;
-      lo[(size_t)n * Kp + kc] = __float2half_rn(x - __half2float(h));
-    }
-  }
-  *hi_out = upload_t(m, hi);
-  *lo_out = upload_t(m, lo);
+  kmajor_split_kernel<<<dim3(ceil_div(N, 32), ceil_div(K, 32)), dim3(32, 8)>>>(dW, K, N, Kp, split, pad,
+                                                                              std::ldexp(1.f, sw), hi, lo);
+  AMUN_CHECK_LAUNCH();
+  *hi_out = hi;
+  *lo_out = lo;
   return std::ldexp(1.f, -(sw + kXShift));
 }
 
+// as split_kmajor_dev for a host matrix needed only in its split form
+static float split_kmajor_host(amun_model *m, const float *W, int K, int N, int Kp, int split, int pad,
+                               __half **hi_out, __half **lo_out) {
+  float *d = nullptr;
+  AMUN_CUDA(cudaMalloc(&d, (size_t)K * N * sizeof(float)));
+  struct Free {
+    float *p;
+    ~Free() { cudaFree(p); }
+  } f{d};
+  AMUN_CUDA(cudaMemcpy(d, W, (size_t)K * N * sizeof(float), cudaMemcpyHostToDevice));
+  const float us = split_kmajor_dev(m, d, K, N, Kp, split, pad, hi_out, lo_out);
+  AMUN_CUDA(cudaDeviceSynchronize());
+  return us;
+}
+
 static float *upload(amun_model *m, const std::vector<float> &h) { return upload_t(m, h); }
+
+// n floats straight from the caller's (read-only) array: no host staging copy
+static float *upload_ptr(amun_model *m, const float *h, size_t n) {
+  float *d = nullptr;
+  AMUN_CUDA(cudaMalloc(&d, n * sizeof(float)));
+  m->allocs.push_back(d);
+  AMUN_CUDA(cudaMemcpy(d, h, n * sizeof(float), cudaMemcpyHostToDevice));
+  m->bytes += (int64_t)(n * sizeof(float));
+  return d;
+}
+
+// max |x| of a device array (absmax_kernel), synchronous
+static float device_absmax(const float *d, size_t n) {
+  unsigned *dmax = nullptr, hmax = 0;
+  AMUN_CUDA(cudaMalloc(&dmax, sizeof(unsigned)));
+  AMUN_CUDA(cudaMemset(dmax, 0, sizeof(unsigned)));
+  absmax_kernel<<<296, 256>>>(d, n, dmax);
+  AMUN_CHECK_LAUNCH();
+  AMUN_CUDA(cudaMemcpy(&hmax, dmax, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  cudaFree(dmax);
+  float mx;
+  std::memcpy(&mx, &hmax, sizeof(float));
+  return mx;
+}
 
 extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const float *const *t,
                                  int32_t n_tensors, amun_model **out) {
@@ -133,20 +206,16 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
   m->xsp = m->dep + 3 * dh;
   // decoder-row column -> padded fp16 row column ([y | pad | c | s])
   const int pad = m->dep - de;
-  auto rowmap = [de, pad](int c) { return c < de ? c : c + pad; };
-  auto ident = [](int c) { return c; };
-  auto cp = [&](int idx, size_t n) { return std::vector<float>(t[idx], t[idx] + n); };
+  auto cp = [&](int idx, size_t n) { return upload_ptr(m, t[idx], n); };
+  m->E_src = cp(T_E_SRC, (size_t)Vs * de);
+  m->E_trg = cp(T_E_TRG, (size_t)V * de);
   {  // tensor-core path: 16-byte fp16 row pitches and activations inside the
      // split's range (decoder rows |x| <= max(1, max|E_trg|) <= 2^(15 - kXShift);
      // encoder states and annotations are GRU outputs in (-1, 1))
-    float emax = 0.f;
-    for (size_t i = 0; i < (size_t)V * de; ++i) emax = std::max(emax, std::fabs(t[T_E_TRG][i]));
-    for (size_t i = 0; i < (size_t)Vs * de; ++i) emax = std::max(emax, std::fabs(t[T_E_SRC][i]));
+    const float emax = std::max(device_absmax(m->E_trg, (size_t)V * de), device_absmax(m->E_src, (size_t)Vs * de));
     m->tc_ok = (de % 4 == 0) && (dh % 8 == 0) && (da % 8 == 0) && emax <= std::ldexp(1.f, 15 - kXShift);
   }
 
-  m->E_src = upload(m, cp(T_E_SRC, (size_t)Vs * de));
-  m->E_trg = upload(m, cp(T_E_TRG, (size_t)V * de));
   {  // encoder input projection, both directions: [de, 6dh] = [fwd z r h | bwd z r h]
     std::vector<float> W((size_t)de * 6 * dh), b(6 * dh);
     for (int dir = 0; dir < 2; ++dir) {
@@ -160,7 +229,7 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     }
     m->Wenc = upload(m, W);
     m->benc = upload(m, b);
-    if (m->tc_ok) m->us_x = upload_kmajor_split(m, W.data(), de, 6 * dh, m->dep, ident, &m->Wenc_hi, &m->Wenc_lo);
+    if (m->tc_ok) m->us_x = split_kmajor_dev(m, m->Wenc, de, 6 * dh, m->dep, de, 0, &m->Wenc_hi, &m->Wenc_lo);
   }
   {  // encoder recurrent weights: Uzr [2][dh][2dh], Uh [2][dh][dh]
     std::vector<float> Uzr((size_t)2 * dh * 2 * dh), Uh((size_t)2 * dh * dh);
@@ -175,12 +244,11 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     m->Uzr = upload(m, Uzr);
     m->Uh = upload(m, Uh);
     if (m->tc_ok) {  // both directions stacked along K: [2dh, 2dh] and [2dh, dh]
-      m->us_ea = upload_kmajor_split(m, Uzr.data(), 2 * dh, 2 * dh, 2 * dh, ident, &m->Uzr_hi, &m->Uzr_lo);
-      m->us_eb = upload_kmajor_split(m, Uh.data(), 2 * dh, dh, 2 * dh, ident, &m->Uh_hi, &m->Uh_lo);
+      m->us_ea = split_kmajor_dev(m, m->Uzr, 2 * dh, 2 * dh, 2 * dh, 2 * dh, 0, &m->Uzr_hi, &m->Uzr_lo);
+      m->us_eb = split_kmajor_dev(m, m->Uh, 2 * dh, dh, 2 * dh, 2 * dh, 0, &m->Uh_hi, &m->Uh_lo);
     }
   }
   if (m->tc_ok) {  // encode-ahead recurrence weights: [x | state] rows (x padded to dep)
-    auto xsmap = [de, pad = m->dep - de](int c) { return c < de ? c : c + pad; };
     for (int dir = 0; dir < 2; ++dir) {
       const int base = dir ? T_ENC_BWD : T_ENC_FWD;
       std::vector<float> A((size_t)(de + dh) * 2 * dh), Bm((size_t)(de + dh) * dh);
@@ -194,19 +262,19 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
         std::memcpy(&A[(size_t)(de + i) * 2 * dh + dh], t[base + G_UR] + (size_t)i * dh, dh * sizeof(float));
         std::memcpy(&Bm[(size_t)(de + i) * dh], t[base + G_UH] + (size_t)i * dh, dh * sizeof(float));
       }
-      m->us_efa[dir] = upload_kmajor_split(m, A.data(), de + dh, 2 * dh, m->dep + dh, xsmap, &m->Efa_hi[dir],
-                                           &m->Efa_lo[dir]);
-      m->us_efb[dir] = upload_kmajor_split(m, Bm.data(), de + dh, dh, m->dep + dh, xsmap, &m->Efb_hi[dir],
-                                           &m->Efb_lo[dir]);
+      m->us_efa[dir] = split_kmajor_host(m, A.data(), de + dh, 2 * dh, m->dep + dh, de, pad, &m->Efa_hi[dir],
+                                         &m->Efa_lo[dir]);
+      m->us_efb[dir] = split_kmajor_host(m, Bm.data(), de + dh, dh, m->dep + dh, de, pad, &m->Efb_hi[dir],
+                                         &m->Efb_lo[dir]);
     }
   }
-  m->W_att_h = upload(m, cp(T_W_ATT_H, (size_t)2 * dh * da));
+  m->W_att_h = cp(T_W_ATT_H, (size_t)2 * dh * da);
   if (m->tc_ok)
-    m->us_p = upload_kmajor_split(m, t[T_W_ATT_H], 2 * dh, da, 2 * dh, ident, &m->Watth_hi, &m->Watth_lo);
-  m->W_init = upload(m, cp(T_W_INIT, (size_t)2 * dh * dh));
-  m->b_init = upload(m, cp(T_B_INIT, dh));
-  m->W_att_s = upload(m, cp(T_W_ATT_S, (size_t)dh * da));
-  m->v_att = upload(m, cp(T_V_ATT, da));
+    m->us_p = split_kmajor_dev(m, m->W_att_h, 2 * dh, da, 2 * dh, 2 * dh, 0, &m->Watth_hi, &m->Watth_lo);
+  m->W_init = cp(T_W_INIT, (size_t)2 * dh * dh);
+  m->b_init = cp(T_B_INIT, dh);
+  m->W_att_s = cp(T_W_ATT_S, (size_t)dh * da);
+  m->v_att = cp(T_V_ATT, da);
   {  // decoder gates: rows [y ; c ; s] (= XS columns), cols [z | r | h];
      // the h block of the s rows is zero (reset-before-matmul: s enters h~
      // only through (r*s) U_h, applied in phase B).
@@ -224,12 +292,12 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     }
     m->Wg = upload(m, Wg);
     m->bg = upload(m, bg);
-    m->Uh_dec = upload(m, cp(T_DEC + G_UH, (size_t)dh * dh));
+    m->Uh_dec = cp(T_DEC + G_UH, (size_t)dh * dh);
     m->tc_gemm = m->tc_ok;
     if (m->tc_gemm) {
-      m->us_g = upload_kmajor_split(m, Wg.data(), din + dh, 3 * dh, m->xsp, rowmap, &m->Wg_hi, &m->Wg_lo);
-      m->us_u = upload_kmajor_split(m, t[T_DEC + G_UH], dh, dh, dh, ident, &m->Uhd_hi, &m->Uhd_lo);
-      m->us_q = upload_kmajor_split(m, t[T_W_ATT_S], dh, da, dh, ident, &m->Wq_hi, &m->Wq_lo);
+      m->us_g = split_kmajor_dev(m, m->Wg, din + dh, 3 * dh, m->xsp, de, pad, &m->Wg_hi, &m->Wg_lo);
+      m->us_u = split_kmajor_dev(m, m->Uh_dec, dh, dh, dh, dh, 0, &m->Uhd_hi, &m->Uhd_lo);
+      m->us_q = split_kmajor_dev(m, m->W_att_s, dh, da, dh, dh, 0, &m->Wq_hi, &m->Wq_lo);
     }
   }
   {  // deep output: rows [y ; c ; s'] = [W_out_y ; W_out_c ; W_out_s]
@@ -238,13 +306,14 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     std::memcpy(&Wo[(size_t)de * de], t[T_W_OUT_C], (size_t)2 * dh * de * sizeof(float));
     std::memcpy(&Wo[(size_t)(de + 2 * dh) * de], t[T_W_OUT_S], (size_t)dh * de * sizeof(float));
     m->Wout = upload(m, Wo);
-    m->b_out = upload(m, cp(T_B_OUT, de));
-    if (m->tc_gemm) m->us_o = upload_kmajor_split(m, Wo.data(), de + 3 * dh, de, m->xsp, rowmap, &m->Wo_hi, &m->Wo_lo);
+    m->b_out = cp(T_B_OUT, de);
+    if (m->tc_gemm) m->us_o = split_kmajor_dev(m, m->Wout, de + 3 * dh, de, m->xsp, de, pad, &m->Wo_hi, &m->Wo_lo);
   }
-  m->W_logit = upload(m, cp(T_W_LOGIT, (size_t)de * V));
-  m->b_logit = upload(m, cp(T_B_LOGIT, V));
+  m->W_logit = cp(T_W_LOGIT, (size_t)de * V);
+  m->b_logit = cp(T_B_LOGIT, V);
   if (m->tc_ok)  // logit rows [V, dep] (K-major, padded to a 16-byte pitch)
-    m->us_l = upload_kmajor_split(m, t[T_W_LOGIT], de, V, m->dep, ident, &m->Wl_hi, &m->Wl_lo);
+    m->us_l = split_kmajor_dev(m, m->W_logit, de, V, m->dep, de, 0, &m->Wl_hi, &m->Wl_lo);
+  AMUN_CUDA(cudaDeviceSynchronize());  // every layout kernel done before the handle is used
   AMUN_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
   m->live = true;
   g_live_models[m->device & 63].fetch_add(1);

@@ -363,3 +363,32 @@ def test_native_text_front_end_matches_python_path():
     assert ids.tolist() == [i for x in big for i in vocab.ids_and_oov(preprocess(x))[0]]
     with pytest.raises(ValueError, match="duplicate"):
         _lib.NativeVocab(["</s>", "<unk>", "a", "a"])
+
+
+def test_host_glue_matches_reference_goldens(tmp_path):
+    """BPE learning / segmentation / joining and lexical-table / frequency
+    list / shortlist construction against fixtures the reference itself
+    produced (tests/golden/make_golden_host.py: pkg/src/beamnmt/subword.py,
+    shortlist.py)."""
+    import json
+
+    from conftest import GOLDEN
+    from paper_1610_01108_b200.shortlist import build_shortlist
+
+    g = json.loads((GOLDEN / "host.json").read_text())
+    for c in g["bpe"]:
+        model = bpe_learn(c["corpus"], c["num_merges"])
+        assert [list(p) for p in model.merges] == c["merges"]
+        assert bpe_apply(model, c["words"]) == c["pieces"]
+        got = [bpe_join(p) for p in (c["pieces"], ["a@@", "@@", "b"], ["x@@@@", "y"], ["tail@@"], [], ["a", "", "b"])]
+        assert got == c["joins"]
+    vocab = Vocabulary(g["vocab"])
+    lp, fp = tmp_path / "lex", tmp_path / "freq"
+    lp.write_text("\n".join(g["lex_lines"]) + "\n")
+    fp.write_text("z\nq\nx\nz\n\nw\n")
+    table = load_lex_table(lp, vocab)
+    assert {s: [list(e) for e in v] for s, v in table.entries.items()} == g["table"]
+    freq, skipped = load_freq_list(fp, vocab)
+    assert (freq, skipped) == (g["freq"], g["freq_skipped"])
+    for s in g["shortlists"]:
+        assert build_shortlist(table, freq, s["src"], s["K"], s["Kprime"], vocab).global_ids.tolist() == s["ids"]

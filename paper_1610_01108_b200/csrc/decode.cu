@@ -117,8 +117,9 @@ void lane_release(int dev, LaneRes *r) {
   g_lane_pool[dev & 63][r->high].push_back(r);
 }
 
-// lanes [0, n) run on high-priority streams: with longest-first dispatch
-// they carry the longest buckets, whose serial step chains bound the pass
+// the last n lanes run on high-priority streams: the dispatch hands the
+// longest buckets to the highest lanes first, and the longest bucket's
+// serial step chain bounds the pass
 int high_priority_lanes() {
   static int v = [] {
     const char *e = getenv("AMUN_HIGH_LANES");
@@ -1144,7 +1145,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     lanes.emplace_back(new Lane());
     Lane &L = *lanes.back();
     L.dev = m0->device;
-    L.res = lane_acquire(L.dev, li < high_priority_lanes());
+    L.res = lane_acquire(L.dev, li >= n_lanes - high_priority_lanes());
     L.st = L.res->st;
     L.h_probe = L.res->h_probe;
     L.probe_ev = L.res->ev.data();
@@ -1313,10 +1314,12 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     __half *Hah = nullptr, *Hal = nullptr;
     void *mem = nullptr;
   };
-  std::vector<Store> stores(n_models);
-  std::vector<std::unique_ptr<AheadEncoder>> encs(n_models);
+  // per chunk of the group in flight: stores, encoders, first sorted sentence
+  std::vector<std::vector<Store>> gstores;
+  std::vector<std::vector<std::unique_ptr<AheadEncoder>>> gencs;
+  std::vector<int> gchunk_first;
+  std::vector<int> chunk_of_bucket(buckets.size(), 0);  // chunk (within the group) of every bucket
   std::vector<long long> bucket_row(buckets.size(), 0);  // store row of (bucket's first sentence, position 0)
-  int chunk_first = 0;  // sorted index of the chunk's first sentence
   // dispatch order: longest-running buckets first (step count x rows), so
   // the short ones fill the lanes at the end instead of a long bucket
   // running alone in the tail (bucket composition, hence every result, is
@@ -1454,8 +1457,10 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     if (ahead) {  // annotations and initial states from this chunk's store
       std::vector<const float *> s0p(n_models);
+      const int ci = chunk_of_bucket[bi], chunk_first = gchunk_first[ci];
+      auto &stores = gstores[ci];
       for (int m = 0; m < n_models; ++m) {
-        encs[m]->prepare(c, bk.first - chunk_first, B, bucket_row[bi], (long long)B * jmax, jmax);
+        gencs[ci][m]->prepare(c, bk.first - chunk_first, B, bucket_row[bi], (long long)B * jmax, jmax);
         const int dh_m = ms[m]->d.d_h, da_m = ms[m]->d.d_att;
         L.eb[m].Hann = stores[m].Hann + bucket_row[bi] * 2 * dh_m;
         L.eb[m].P = stores[m].P + bucket_row[bi] * da_m;
@@ -1698,7 +1703,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   };
 
   // chunks of whole buckets: with encode-ahead, a chunk's encoder runs
-  // before its buckets decode (bounded annotation-store memory)
+  // before its buckets decode (bounded annotation-store memory,
+  // AMUN_ENC_CHUNK sentences per chunk, decoded one after the other)
   std::vector<std::pair<int, int>> chunks;
   {
     const char *ce = getenv("AMUN_ENC_CHUNK");  // read per call (tests vary it)
@@ -1711,11 +1717,46 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       b = e;
     }
   }
-  for (const auto &ch : chunks) {
+  // groups of chunks in flight together.  A single chunk is split in two:
+  // its longest buckets (AMUN_ENC_LEAD sentences, default 8 buckets' worth)
+  // are encoded first, on their own -- a short recurrence over few rows --
+  // so the longest bucket, which bounds the pass, starts decoding after a
+  // few milliseconds instead of after the whole corpus's encoder; the
+  // rest's encoder follows on the encoder streams while those decode
+  std::vector<std::vector<std::pair<int, int>>> groups;
+  {
+    const char *le = getenv("AMUN_ENC_LEAD");
+    const int lead = le ? std::max(0, atoi(le)) : 8 * Bmax_opt;
+    if (ahead && chunks.size() == 1 && lead > 0) {
+      const int nb = (int)buckets.size();
+      int b = nb, cnt = 0;
+      while (b > 1 && cnt < lead) cnt += buckets[--b].count;
+      if (b > 0 && b < nb)
+        groups.push_back({{b, nb}, {0, b}});
+      else
+        groups.push_back(chunks);
+    } else {
+      for (const auto &ch : chunks) groups.push_back({ch});
+    }
+  }
+  for (const auto &group : groups) {
+  gstores.assign(group.size(), std::vector<Store>());
+  gencs.clear();
+  gencs.resize(group.size());
+  gchunk_first.assign(group.size(), 0);
+  dispatch.clear();
+  for (size_t ci = 0; ci < group.size(); ++ci) {
+  const auto &ch = group[ci];
+  for (int bi = ch.first; bi < ch.second; ++bi) chunk_of_bucket[bi] = (int)ci;
   if (ahead) {
+    auto &stores = gstores[ci];
+    auto &encs = gencs[ci];
+    stores.assign(n_models, Store{});
+    encs.resize(n_models);
     // store rows per bucket ([B][jmax] each), the chunk's sentences in
     // sorted order, then the encoder of every model
-    chunk_first = buckets[ch.first].first;
+    const int chunk_first = buckets[ch.first].first;
+    gchunk_first[ci] = chunk_first;
     long long rows = 0;
     for (int bi = ch.first; bi < ch.second; ++bi) {
       bucket_row[bi] = rows;
@@ -1755,10 +1796,16 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       encs[m]->run(cf, cb);
     }
   }
-  dispatch = lpt_order(ch.first, ch.second);
+  {
+    const std::vector<int> d = lpt_order(ch.first, ch.second);
+    dispatch.insert(dispatch.end(), d.begin(), d.end());
+  }
+  }  // chunks of the group
   next_bucket = 0;
-  for (auto &Lp : lanes)
-    if (next_bucket < dispatch.size()) start_bucket(*Lp, dispatch[next_bucket++]);
+  // the longest buckets go to the highest lanes: lanes 0 and 1 also carry
+  // the encoder streams
+  for (int li = n_lanes - 1; li >= 0; --li)
+    if (next_bucket < dispatch.size()) start_bucket(*lanes[li], dispatch[next_bucket++]);
   for (;;) {
     bool any = false;
     for (auto &Lp : lanes) {
@@ -1780,14 +1827,15 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     }
     if (!any) break;
   }
-  if (ahead)  // every lane finished (and synchronised) this chunk's buckets
-    for (int m = 0; m < n_models; ++m) {
-      encs[m]->release(*lanes[0]->c);
-      encs[m].reset();
-      AMUN_CUDA(cudaFreeAsync(stores[m].mem, lanes[0]->st));
-      stores[m] = Store{};
-    }
-  }  // chunks
+  if (ahead)  // every lane finished (and synchronised) this group's buckets
+    for (size_t ci = 0; ci < group.size(); ++ci)
+      for (int m = 0; m < n_models; ++m) {
+        gencs[ci][m]->release(*lanes[0]->c);
+        gencs[ci][m].reset();
+        AMUN_CUDA(cudaFreeAsync(gstores[ci][m].mem, lanes[0]->st));
+        gstores[ci][m] = Store{};
+      }
+  }  // groups
 
   for (int li = 1; li < n_lanes; ++li) {
     AMUN_CUDA(cudaEventRecord(lanes[li]->probe_ev[0], lanes[li]->st));

@@ -38,7 +38,10 @@ namespace {
 
 constexpr int kBK = 64;                     // fp16 K elements per 128-byte swizzled row
 constexpr int kRowB = kBK * 2;
-constexpr int kStages = 3;
+#ifndef AMUN_LOGIT_STAGES
+#define AMUN_LOGIT_STAGES 3
+#endif
+constexpr int kStages = AMUN_LOGIT_STAGES;
 #ifndef AMUN_LOGIT_UNIT_ROWS
 #define AMUN_LOGIT_UNIT_ROWS 160
 #endif
@@ -52,7 +55,10 @@ constexpr int kAccCols = 256;               // TMEM column offset of accumulator
 constexpr int kTrQ = 36;                    // floats per vocabulary quarter in a transposed row (32 + pad)
 constexpr int kTrRow = 4 * kTrQ;            // floats per transposed row (128 vocab + pad)
 constexpr int kTrB = 32 * kTrRow * 4;       // one transpose buffer (32 rows x 128 vocab)
-constexpr int kEpiGroups = 3;               // epilogue warp groups (4 warps each) working on alternate chunks
+#ifndef AMUN_LOGIT_EPI
+#define AMUN_LOGIT_EPI 3
+#endif
+constexpr int kEpiGroups = AMUN_LOGIT_EPI;               // epilogue warp groups (4 warps each) working on alternate chunks
 constexpr int kSmem = kStages * kStageB + kEpiGroups * kTrB + 1024 + 256;
 constexpr int kThreads = 64 + 128 * kEpiGroups;  // warp 0 TMA, warp 1 MMA (leader), then the epilogue groups
 static_assert(kSmem <= 232448, "shared memory per CTA");

@@ -32,7 +32,8 @@ from paper_1610_01108_b200 import (
 )
 from paper_1610_01108_b200.errors import FormatError
 from paper_1610_01108_b200.model import schema
-from paper_1610_01108_b200.sharding import length_buckets, partition_lpt, sentence_work, shard_sentences
+from paper_1610_01108_b200.sharding import (STEP_FLOP, STEP_LATENCY_ROWS, length_buckets, partition_lpt,
+                                            sentence_work, shard_sentences)
 from paper_1610_01108_b200.shortlist import LexicalTable, load_freq_list, load_lex_table
 from paper_1610_01108_b200.subword import load_bpe_model, save_bpe_model
 from paper_1610_01108_b200.workload import WORKLOADS
@@ -224,8 +225,12 @@ def test_shard_sentences_whole_buckets():
     for n in (1, 2, 4, 8):
         parts = shard_sentences(lens, n, 64, 5)
         assert sorted(i for p in parts for i in p) == list(range(4000))
+        # whole buckets per part, and the estimated makespan (work, or the
+        # serial step chain of a part's longest bucket) within 6% of its lower bound
         works = [sum(sentence_work(lens[i], 5) for i in p) for p in parts]
-        assert max(works) / (sum(works) / n) < 1.05
+        lats = [max(2 * lens[i] + 10 for i in p) * STEP_LATENCY_ROWS * STEP_FLOP for p in parts]
+        span = max(max(w, l) for w, l in zip(works, lats))
+        assert span / max(sum(works) / n, max(lats)) < 1.06
     buckets = length_buckets(lens, 64)
     assert len(buckets) == 63 and all(len(b) == 64 for b in buckets[:-1])
 

@@ -204,16 +204,18 @@ def _adjudicate(name, gold_hyps, gaps, out, score_rtol=SCORE_RTOL_FULL):
     """Token identity per sentence, except documented near ties.
 
     A sentence whose 1-best first differs from the reference's at token d is
-    excused only if, at some search step <= d (the beams must have diverged
-    no later than step d; a near tie later in the sentence excuses nothing),
-    the reference's k-th vs (k+1)-th candidate gap was below the accumulated
-    score error of two hypotheses after that many steps: tau(d) =
-    max(TAU, 2 * eps * (d + 1)), where eps is the largest per-step score
-    error measured on this run's token-identical sentences (|score -
-    reference| / steps; fp32-equivalent arithmetic vs the reference's f64
-    drifts ~1e-5 per step, dominated by the fp32 GRU state).  A final-ranking
-    tie (two best hypotheses within tau) is excused likewise.  Exact
-    sentences must match the score to score_rtol."""
+    excused only if, at some search step t >= d, the reference's k-th vs
+    (k+1)-th candidate gap was below the accumulated score error of two
+    hypotheses after t + 1 steps, tau(t) = max(TAU, 2 * eps * (t + 1)), where
+    eps is the largest per-step score error measured on this run's
+    token-identical sentences (|score - reference| / steps; fp32-equivalent
+    arithmetic vs the reference's f64 drifts ~1e-5 per step).  Why t >= d: a
+    different beam membership at step t (the only thing the k-th/(k+1)-th
+    gap governs) changes which prefixes of length t + 1 survive, so the two
+    searches' final hypotheses can first differ at a token d <= t, never
+    later; a near tie at a step before d cannot explain a divergence at d.
+    A final-ranking tie (two best hypotheses within tau) is excused
+    likewise.  Exact sentences must match the score to score_rtol."""
     exact, ties, fails, worst, eps = 0, [], [], 0.0, 0.0
     for i, (gtoks, gscore) in enumerate(gold_hyps):
         hyps = out.hyps(i)
@@ -230,12 +232,18 @@ def _adjudicate(name, gold_hyps, gaps, out, score_rtol=SCORE_RTOL_FULL):
         if toks == gtoks:
             continue
         d = _first_divergence(toks, gtoks)
-        tau = max(TAU, 2.0 * eps * (d + 1))
-        g = np.asarray(gaps[i][: d + 1], np.float64)
-        gap_d = float(g.min()) if g.size else np.inf
+        g = np.asarray(gaps[i], np.float64)
+        steps = np.arange(g.size)
+        taus = np.maximum(TAU, 2.0 * eps * (steps + 1))
+        hit = np.flatnonzero((steps >= d) & (g < taus))
+        t = int(hit[0]) if hit.size else -1
         final_gap = abs(hyps[0][1] - hyps[1][1]) if len(hyps) > 1 else np.inf
-        (ties if min(gap_d, final_gap) < tau else fails).append((i, d, gap_d, round(tau, 7), final_gap))
+        tau_end = max(TAU, 2.0 * eps * max(1, len(gtoks)))
+        ok = t >= 0 or final_gap < tau_end
+        (ties if ok else fails).append((i, d, t, float(g[t]) if t >= 0 else None,
+                                        round(float(taus[t]), 7) if t >= 0 else None, final_gap))
     n = len(gold_hyps)
+    # exceptions: (sentence, first divergent token d, excusing step t >= d, its gap, tau(t), final-rank gap)
     summary = (f"{name}: {exact}/{n} token-identical, {len(ties)} near-tie exceptions {ties}, "
                f"{len(fails)} unexplained {fails[:10]}; max score rel err {worst:.2e}, "
                f"per-step score error eps {eps:.2e}")
@@ -571,3 +579,36 @@ def test_bench_api_through_engine(gpu, full):
     lrep, lres = latency_bench(eng, lines[:4])
     assert [r.text for r in lres] == [r.text for r in res[:4]]
     assert 0 < lrep.device_seconds <= lrep.wall_seconds
+
+
+@pytest.mark.parametrize("name,max_batch", [("ens2_sl", 64), ("ens2_sl", 5), ("beam16", 64), ("beam16", 3),
+                                            ("beam9", 64)])
+def test_extra_paths_match_reference(gpu, full, name, max_batch):
+    """Less common decode paths against the reference's own beam_search
+    (tests/golden/make_golden_extra.py): a 2-member ensemble WITH shortlists
+    (masks on the fused ensemble logit kernel), beam 16 (the rows-layout
+    logit kernel's largest list) and beam 9, in several bucket sizes."""
+    from paper_1610_01108_b200 import workload as W
+
+    from conftest import GOLDEN
+
+    with np.load(GOLDEN / "extra_sets.npz") as z:
+        g = {k: z[k] for k in z.files}
+    members = []
+    for de, dh, da, seed in g[f"{name}_members"].tolist():
+        members.append(full if (de, dh, da, seed) == (500, 1024, 1024, 1)
+                       else random_model(ModelConfig(30000, 30000, de, dh, da), seed))
+    dms = [_lib.device_model(m) for m in members]
+    corpus = W.WORKLOADS["cfg2"].corpus()
+    sents = [corpus[i] for i in g[f"{name}_idx"]]
+    sls = W.shortlists(sents) if int(g[f"{name}_shortlists"]) else None
+    beam, f, o, _, _ = (int(x) for x in g[f"{name}_opts"])
+    out = _lib.decode(dms, sents, beam, f, o, False, 2, shortlists=sls, max_batch=max_batch)
+    toff, goff = g[f"{name}_tok_off"], g[f"{name}_gap_off"]
+    gold = [(g[f"{name}_tokens"][toff[i]:toff[i + 1]].astype(int).tolist(), float(g[f"{name}_score"][i]))
+            for i in range(len(sents))]
+    gaps = [g[f"{name}_gap"][goff[i]:goff[i + 1]] for i in range(len(sents))]
+    _adjudicate(f"{name} batch {max_batch}", gold, gaps, out)
+    if sls is not None:
+        for i in range(len(sents)):
+            assert set(out.hyps(i)[0][0]) <= set(sls[i].tolist())

@@ -59,7 +59,7 @@ def _topk_ref(lp_row: np.ndarray, kk: int):
     return order[:kk], lp_row[order]
 
 
-@pytest.mark.parametrize("cfg,k,n_sent", [("cfg2", 5, 64), ("cfg4", 12, 64)])
+@pytest.mark.parametrize("cfg,k,n_sent", [("cfg2", 5, 64), ("cfg4", 12, 64), ("cfg2", 9, 8), ("cfg2", 9, 1)])
 def test_production_step_logprobs(gpu, full, net, cfg, k, n_sent):
     """>= 2 x n_sent x k full-size decoder states (two consecutive steps of
     beam-like rows per sentence) through the production step kernels."""

@@ -8,9 +8,10 @@ calls raise instead of computing anything on the host.
 from __future__ import annotations
 
 import ctypes
-import time
 import os
+import queue
 import threading
+import time
 from pathlib import Path
 from typing import Sequence
 
@@ -382,23 +383,45 @@ def decode(models: Sequence[DeviceModel], sentences: Sequence[Sequence[int]], be
                               ctypes.byref(opts), ctypes.byref(res)))
     else:
         # finished buckets are handed to on_bucket(sentence indices, DecodeOut)
-        # while later buckets still decode; an exception inside is re-raised
-        # after the call (ctypes cannot propagate it through C)
+        # while later buckets still decode.  The library's callback only
+        # copies the bucket's results and queues them: on_bucket runs on a
+        # consumer thread, so the native decode loop (which feeds every lane
+        # its next steps) is never held up by the caller's post-processing.
+        # An exception inside on_bucket is re-raised after the call (ctypes
+        # cannot propagate it through C).
         errors: list[BaseException] = []
+        done_q: queue.SimpleQueue = queue.SimpleQueue()
 
         def _cb(_user, part, idx):
             if errors:
                 return
             try:
                 out = DecodeOut(part.contents, want_states, widths)
-                sel = np.ctypeslib.as_array(idx, shape=(out.n_sent,)).copy()
-                on_bucket(sel, out)
+                done_q.put((np.ctypeslib.as_array(idx, shape=(out.n_sent,)).copy(), out))
             except BaseException as e:  # noqa: BLE001 - re-raised below
                 errors.append(e)
 
+        def _consume():
+            while True:
+                item = done_q.get()
+                if item is None:
+                    return
+                if errors:
+                    continue
+                try:
+                    on_bucket(*item)
+                except BaseException as e:  # noqa: BLE001 - re-raised below
+                    errors.append(e)
+
+        consumer = threading.Thread(target=_consume, name="amun-bucket-consumer", daemon=True)
+        consumer.start()
         cb = BUCKET_DONE(_cb)
-        check(lib.amun_decode_stream(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(lens), sl_p,
-                                     sl_l, ctypes.byref(opts), cb, None, ctypes.byref(res)))
+        try:
+            check(lib.amun_decode_stream(handles, len(models), _ptr(ids, _i32p), _ptr(lens, _i32p), len(lens),
+                                         sl_p, sl_l, ctypes.byref(opts), cb, None, ctypes.byref(res)))
+        finally:
+            done_q.put(None)
+            consumer.join()
         if errors:
             lib.amun_result_free(res)
             raise errors[0]

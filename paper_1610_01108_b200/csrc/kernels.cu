@@ -2,6 +2,7 @@
 #include <cooperative_groups.h>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace amun {
 
@@ -339,6 +340,29 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
   float *al = vs + a.da;                             // [k][jmax]
   int *qbig = reinterpret_cast<int *>(al + (size_t)k * a.jmax);  // [k]
   float *eqs = reinterpret_cast<float *>(qbig + ((k + 3) & ~3));  // [KA][1024] e^{2q} rows (fast path)
+  // H of the sentence streamed into shared memory in chunks of kHP
+  // positions by bulk copies, two buffers, issued now and consumed by the
+  // context phase: the annotation reads overlap the energies instead of
+  // stalling the context loop (one thread per 4 columns: dh2 == 4 x threads)
+  constexpr int kHP = 4;
+  const bool hsmem = a.dh2 == 4 * (int)blockDim.x;
+  float *hbuf = reinterpret_cast<float *>(
+      (reinterpret_cast<uintptr_t>(eqs + (a.da == 1024 ? k * 1024 : 0)) + 127) & ~uintptr_t(127));
+  uint64_t *hbar = reinterpret_cast<uint64_t *>(hbuf + 2 * kHP * a.dh2);
+  const int nch = (J + kHP - 1) / kHP;
+  const float *Hsent = a.H + (long long)b * a.jmax * a.dh2;
+  auto issue_chunk = [&](int c) {  // thread 0
+    const uint32_t bytes = (uint32_t)(min(kHP, J - c * kHP) * a.dh2 * 4);
+    tc::mbar_arrive_expect_tx(&hbar[c & 1], bytes);
+    tc::bulk_load_1d(hbuf + (c & 1) * kHP * a.dh2, Hsent + (long long)c * kHP * a.dh2, bytes, &hbar[c & 1]);
+  };
+  if (hsmem && tid == 0) {
+    tc::mbar_init(&hbar[0], 1);
+    tc::mbar_init(&hbar[1], 1);
+    tc::fence_barrier_init();
+    issue_chunk(0);
+    if (nch > 1) issue_chunk(1);
+  }
   for (int i = tid; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
   const bool fast_shape = na == KA && a.da == 1024;
   if (fast_shape)
@@ -443,7 +467,50 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
   // ---- context (nnet.py:141): thread = 4 consecutive columns, every row
   const int hs = a.dh2 / 4;
   const float4 *Hb = reinterpret_cast<const float4 *>(a.H + (long long)b * a.jmax * a.dh2);
-  for (int c4 = tid; c4 < hs; c4 += blockDim.x) {
+  if (hsmem) {
+    const int c4 = tid;
+    float4 acc[KA];
+#pragma unroll
+    for (int r = 0; r < KA; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < nch; ++c) {
+      tc::mbar_wait(&hbar[c & 1], (c >> 1) & 1);
+      const float4 *hb = reinterpret_cast<const float4 *>(hbuf + (c & 1) * kHP * a.dh2);
+      const int j0 = c * kHP;
+#pragma unroll
+      for (int jj = 0; jj < kHP; ++jj) {
+        if (j0 + jj >= J) break;
+        const float4 h = hb[jj * hs + c4];
+#pragma unroll
+        for (int r = 0; r < KA; ++r)
+          if (r < na) {  // positions summed in order, as the global-memory loop below
+            const float w = al[r * a.jmax + j0 + jj];
+            acc[r].x = fmaf(w, h.x, acc[r].x);
+            acc[r].y = fmaf(w, h.y, acc[r].y);
+            acc[r].z = fmaf(w, h.z, acc[r].z);
+            acc[r].w = fmaf(w, h.w, acc[r].w);
+          }
+      }
+      if (c + 2 < nch) {
+        __syncthreads();  // every thread is done with this buffer
+        if (tid == 0) {
+          tc::fence_proxy_async();
+          issue_chunk(c + 2);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < KA; ++r) {
+      if (r >= na) break;
+      const long long o = (long long)(b * k + r) * a.ldctx + 4 * c4;
+      *reinterpret_cast<float4 *>(a.ctx + o) = acc[r];
+      const long long oh = (long long)(b * k + r) * a.ldctx_h + 4 * c4;
+      store_split(a.ctx_hi, a.ctx_lo, oh + 0, acc[r].x);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 1, acc[r].y);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 2, acc[r].z);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 3, acc[r].w);
+    }
+  }
+  for (int c4 = hsmem ? hs : tid; c4 < hs; c4 += blockDim.x) {
     float4 acc[KA];
 #pragma unroll
     for (int r = 0; r < KA; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -518,7 +585,8 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
     return !(e && e[0] == '0');
   }();
   const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)((k + 3) & ~3) +
-                        (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0);
+                        (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0) +
+                        (a.dh2 == 4 * 512 ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);
   // The kernel is chosen from per-call constants only (beam width, model
   // layout), never from the bucket's longest sentence: the fused and the
   // two-phase kernels sum in different orders, and a sentence's result must

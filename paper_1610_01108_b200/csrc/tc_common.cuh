@@ -74,6 +74,15 @@ __device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *m, 
       : "memory");
 }
 
+// 1D bulk copy global -> shared of `bytes` (multiple of 16, both addresses
+// 16-byte aligned), completion counted on `bar` (bytes).
+__device__ __forceinline__ void bulk_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // CTA-pair variant (cta_group::2): the box lands in this CTA's shared memory
 // and its bytes complete on the mbarrier at cluster address `bar_cluster`
 // (the leader CTA's barrier).

@@ -515,8 +515,12 @@ int ahead_target_ctas() {
 // the call, chunk or device; the z-grid spreads the row passes.
 template <class C = SkDefault>
 std::pair<int, int> ahead_grid(const SkMaps &mp, int M, int target) {
+  static const int split_ctas = [] {  // CTAs per row pass the split count aims at
+    const char *e = getenv("AMUN_AHEAD_SPLIT_CTAS");
+    return e ? std::max(1, atoi(e)) : 32;
+  }();
   const int per_pass = ceil_div(mp.N, 128 * C::kCG) * C::kCG;
-  const int s = sk_fit_splits<C>(mp, 32);
+  const int s = sk_fit_splits<C>(mp, split_ctas);
   const int npass = ceil_div(M, C::kPR);
   return {s, std::max(1, std::min(npass, target / (per_pass * s)))};
 }

@@ -1197,7 +1197,15 @@ static void launch_select_t(const SelectArgs &sa, const BeamState &bs, const Mod
   if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SelectArgs sk = sa;
   sk.kt = ktime_ptr();
-  kern<<<bs.B, 256, smem, st>>>(sk, bs, mr);
+  // one warp per beam row in the row phase: beams <= 8 run 5..8-warp CTAs
+  // (k = 5: 160 threads, so three CTAs share an SM); AMUN_SELECT_THREADS overrides
+  static const int forced = [] {
+    const char *e = getenv("AMUN_SELECT_THREADS");
+    return e ? atoi(e) : 0;
+  }();
+  const int threads = forced > 0 ? std::min(256, std::max(32, forced / 32 * 32))
+                                 : (bs.k <= 8 ? 32 * std::max(4, bs.k) : 256);
+  kern<<<bs.B, threads, smem, st>>>(sk, bs, mr);
   AMUN_CHECK_LAUNCH();
 }
 

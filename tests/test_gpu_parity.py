@@ -612,3 +612,19 @@ def test_extra_paths_match_reference(gpu, full, name, max_batch):
     if sls is not None:
         for i in range(len(sents)):
             assert set(out.hyps(i)[0][0]) <= set(sls[i].tolist())
+
+
+def test_rows_logits_cluster_sizes_agree(gpu, full):
+    """The rows-layout logit kernel (beams >= 8) shares each weight tile over
+    a cluster of as many CTAs as the bucket has 128-row tiles (6 at R = 768)
+    and runs single CTAs for buckets of 3 sentences: both must give
+    byte-identical decodes, so a sentence's result never depends on its
+    bucket's size."""
+    from paper_1610_01108_b200 import workload as W
+
+    sents = W.WORKLOADS["cfg4"].corpus()[:64]
+    dm = _lib.device_model(full)
+    a = _lib.decode([dm], sents, 12, 1, 0, False, 2, max_batch=64)
+    b = _lib.decode([dm], sents, 12, 1, 0, False, 2, max_batch=3)
+    for i in range(len(sents)):
+        assert a.hyps(i) == b.hyps(i), i

@@ -46,7 +46,8 @@ constexpr int kStages = AMUN_LOGIT_STAGES;
 #define AMUN_LOGIT_UNIT_ROWS 160
 #endif
 constexpr int kUnitRows = AMUN_LOGIT_UNIT_ROWS;              // hypothesis rows per work unit (one MMA, N <= 160)
-constexpr int kXRows = kUnitRows / 2;       // rows staged by each CTA of the pair
+constexpr int kUnitRowsBig = 192;           // units of launches with >= 512 rows (balanced 6-chunk epilogue)
+constexpr int kXRows = kUnitRowsBig / 2;    // rows staged by each CTA of the pair (largest unit)
 constexpr int kBoxR = 16;                   // activation rows per TMA box
 constexpr int kWB = 128 * kRowB;            // one of hi/lo weight tiles
 constexpr int kXB = kXRows * kRowB;         // one of hi/lo activation tiles
@@ -151,7 +152,12 @@ __device__ __forceinline__ void merge_partner(RowTop<KK> &top, int lane_xor) {
 
 // Hypothesis rows per work unit: the nm members' accumulators of one unit
 // share a 256-column TMEM buffer (member m at column m * rows).
-__host__ __device__ constexpr int unit_rows(int nm) { return nm <= 1 ? kUnitRows : nm == 2 ? 128 : 64; }
+// Launches of >= 512 rows use 192-row units (6 chunks: every epilogue group
+// drains two); the unit size only regroups rows, a row's logits and
+// partials are the same in any unit.
+__host__ __device__ constexpr int unit_rows(int nm, int M) {
+  return nm <= 1 ? (M >= 512 ? kUnitRowsBig : kUnitRows) : nm == 2 ? 128 : 64;
+}
 
 // Work unit u of a launch: 256-vocab tile vt, rows [row0, row0 + nr); the
 // pair's MMA has N = nr rounded up to 32, each CTA stages N / 2 of the rows.
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t leader = crank & ~1u;
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
   const int nm = NMX == 1 ? 1 : a.nm;
-  const int ur = unit_rows(nm);
+  const int ur = unit_rows(nm, a.M);
   const int nvt = (a.N + 255) / 256;
   const int npass = (a.M + ur - 1) / ur;
   const int units = nvt * npass;
@@ -572,7 +578,7 @@ void launch_t(const LogitTcMaps *maps, const LogitTcArgs &a, cudaStream_t st) {
     AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     if (dev < 64) attr[dev] = true;
   }
-  const int units = ceil_div(a.N, 256) * ceil_div(a.M, unit_rows(NMX == 1 ? 1 : a.nm));
+  const int units = ceil_div(a.N, 256) * ceil_div(a.M, unit_rows(NMX == 1 ? 1 : a.nm, a.M));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * logit_pairs(units));
   cfg.blockDim = dim3(kThreads);

@@ -337,7 +337,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_after();
       if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + 12] = clock64();
 #pragma unroll 1
-      for (int c0 = 32 * g; c0 < un.n; c0 += 32 * kEpiGroups, ++dchunk) {
+      // the chunk -> group assignment rotates from unit to unit, so a unit
+      // whose chunk count is not a multiple of the group count (160 rows:
+      // 5 chunks for 3 groups) does not always leave the same group idle
+      for (int c0 = 32 * ((g + ti) % kEpiGroups); c0 < un.n; c0 += 32 * kEpiGroups, ++dchunk) {
         const int m = un.row0 + c0 + ri;
         const bool wr = q == 0 && c0 + ri < un.nr && nt < a.ntiles && !(a.debug_flags & 64);
         // thread (ri, q): logits of row c0 + ri for vocab v0 + 32 q + [0, 32);

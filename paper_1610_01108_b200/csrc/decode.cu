@@ -1778,8 +1778,13 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
         carow[i] = bucket_row[bi] + (long long)j * buckets[bi].jmax;
         cids.insert(cids.end(), src_ids + off[s], src_ids + off[s + 1]);
       }
-    Ctx &cf = *lanes[0]->c;
-    Ctx &cb = *lanes[n_lanes > 1 ? 1 : 0]->c;
+    // encoder streams: chunk ci of the group runs its forward / backward
+    // recurrences on lanes 2 ci and 2 ci + 1 (when there are enough lanes),
+    // so the lead chunk's long serial recurrence and the bulk chunk's big
+    // one run concurrently instead of one after the other
+    const int e0 = std::min(2 * (int)ci, n_lanes - 1), e1 = std::min(2 * (int)ci + 1, n_lanes - 1);
+    Ctx &cf = *lanes[e0]->c;
+    Ctx &cb = *lanes[e1]->c;
     for (int m = 0; m < n_models; ++m) {
       const int dh_m = ms[m]->d.d_h, da_m = ms[m]->d.d_att;
       Store &S = stores[m];

@@ -111,6 +111,50 @@ __global__ void kmajor_split_kernel(const float *__restrict__ W, int K, int N, i
 
 static float device_absmax(const float *d, size_t n);
 
+// C[M, N] = A[M, K] B[K, N] in fp32 (row-major, pitches lda / ldb / N), 64 x 64
+// tiles through shared memory, 4 x 4 outputs per thread: the per-token
+// embedding tables E_trg W^y built once at model load
+__global__ void table_gemm_kernel(const float *__restrict__ A, int lda, const float *__restrict__ B, int ldb, int M,
+                                  int N, int K, float *__restrict__ C) {
+  __shared__ float As[16][64 + 1], Bs[16][64];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int r = i / 16, kk = i % 16;
+      As[kk][r] = (m0 + r < M && k0 + kk < K) ? A[(long long)(m0 + r) * lda + k0 + kk] : 0.f;
+      const int kb = i / 64, c = i % 64;
+      Bs[kb][c] = (k0 + kb < K && n0 + c < N) ? B[(long long)(k0 + kb) * ldb + n0 + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(As[kk][ty * 4 + i], Bs[kk][tx * 4 + j], acc[i][j]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < N) C[(long long)m * N + n] = acc[i][j];
+    }
+}
+
+static float *device_table(amun_model *m, const float *A, int lda, const float *B, int ldb, int M, int N, int K) {
+  float *d = nullptr;
+  AMUN_CUDA(cudaMalloc(&d, (size_t)M * N * sizeof(float)));
+  m->allocs.push_back(d);
+  m->bytes += (int64_t)((size_t)M * N * sizeof(float));
+  table_gemm_kernel<<<dim3(ceil_div(N, 64), ceil_div(M, 64)), 256>>>(A, lda, B, ldb, M, N, K, d);
+  AMUN_CHECK_LAUNCH();
+  return d;
+}
+
 // [K, N] row-major DEVICE matrix -> device [N, Kp] (K-major, row pitch Kp)
 // 3xFP16 hi/lo copies for the tensor-core GEMMs (common.cuh split_h), built
 // on the device from the fp32 copy: the matrix is scaled by 2^sw with
@@ -308,6 +352,10 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     m->Wout = upload(m, Wo);
     m->b_out = cp(T_B_OUT, de);
     if (m->tc_gemm) m->us_o = split_kmajor_dev(m, m->Wout, de + 3 * dh, de, m->xsp, de, pad, &m->Wo_hi, &m->Wo_lo);
+  }
+  if (m->tc_gemm) {  // y = E_trg[previous token]: its products with the y weight rows, per token
+    m->YWg = device_table(m, m->E_trg, de, m->Wg, 3 * dh, V, 3 * dh, de);
+    m->YWo = device_table(m, m->E_trg, de, m->Wout, de, V, de, de);
   }
   m->W_logit = cp(T_W_LOGIT, (size_t)de * V);
   m->b_logit = cp(T_B_LOGIT, V);

@@ -763,13 +763,19 @@ void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
   const int s_off = dep + 2 * dh;  // padded fp16 row layout
   ts.q = make_sk_maps(d.XSh + s_off, d.XSl + s_off, dh, xp, nullptr, nullptr, 0, 0, Rmax, m->Wq_hi, m->Wq_lo, da,
                       dh, m->us_q);
-  ts.g = make_sk_maps(d.XSh, d.XSl, xp, xp, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi, m->Wg_lo, 3 * dh, xp, m->us_g);
+  // with the per-token y tables (m->YWg / YWo) the GRU-A and deep-output
+  // GEMMs run over [c | s] only: their A rows and weight rows start at
+  // column dep (the epilogues add the y rows' products from the tables)
+  const int y0 = m->YWg ? dep : 0;
+  ts.g = make_sk_maps(d.XSh + y0, d.XSl + y0, xp - y0, xp, nullptr, nullptr, 0, 0, Rmax, m->Wg_hi + y0,
+                      m->Wg_lo + y0, 3 * dh, xp - y0, m->us_g, -1, xp);
   if ((2 * dh) % 256 == 0) {  // h-gate features: the state rows' weights are zero
     ts.g.n_klim = 2 * dh;
-    ts.g.k_lim = dep + 2 * dh;
+    ts.g.k_lim = dep - y0 + 2 * dh;
   }
   ts.u = make_sk_maps(d.RHh, d.RHl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Uhd_hi, m->Uhd_lo, dh, dh, m->us_u);
-  ts.o = make_sk_maps(d.XSh, d.XSl, s_off, xp, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi, m->Wo_lo, de, xp, m->us_o);
+  ts.o = make_sk_maps(d.XSh + y0, d.XSl + y0, s_off - y0, xp, d.Snh, d.Snl, dh, dh, Rmax, m->Wo_hi + y0,
+                      m->Wo_lo + y0, de, xp - y0, m->us_o, -1, xp);
   const int t = tc_target_ctas();
   ts.sq = sk_fit_splits(ts.q, t);
   ts.sg = sk_fit_splits(ts.g, t);
@@ -793,7 +799,7 @@ void gemm_tc(Ctx &c, const SkMaps &maps, int M, int splits, const Epi &epi) {
 
 void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
                int R, int rows_per_sent, const int *n_act, const int *done, float *alpha, const LogitOut &lo,
-               const TcStep *ts = nullptr, bool do_logits = true) {
+               const TcStep *ts = nullptr, bool do_logits = true, const int *tok = nullptr) {
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
   const int s_off = de + 2 * dh;
   c.cls = AMUN_K_QUERY;
@@ -823,6 +829,12 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     if (ts) {
       ea.RHh = d.RHh;
       ea.RHl = d.RHl;
+      if (m->YWg) {  // y rows' products from the per-token table (tc_step_maps)
+        if (!tok) throw Error(AMUN_ERR_CUDA, "step_rows: previous tokens required with the y tables");
+        ea.rowadd = m->YWg;
+        ea.rowtok = tok;
+        ea.ldadd = 3 * dh;
+      }
       gemm_tc(c, ts->g, R, ts->sg, ea);
     } else {
       GemmArgs g = ga(R, 3 * dh, d.XS, xs, xs, m->Wg, 3 * dh);
@@ -851,6 +863,11 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
       e.ldh = m->dep;
     }
     if (ts) {
+      if (m->YWo) {
+        e.rowadd = m->YWo;
+        e.rowtok = tok;
+        e.ldadd = de;
+      }
       gemm_tc(c, ts->o, R, ts->so, e);
     } else {
       GemmArgs g = ga(R, de, d.XS, xs, de + 2 * dh, m->Wout, de);
@@ -1348,7 +1365,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     Ctx &c = *L.c;
     for (int m = 0; m < n_models; ++m)
       step_rows(c, ms[m], L.db[m], L.eb[m], L.d_len, L.jmax, L.R, k, L.bs.n_act, L.bs.done, nullptr, L.lo,
-                use_tcg ? &L.tsteps[m] : nullptr, !ens_fused);
+                use_tcg ? &L.tsteps[m] : nullptr, !ens_fused, L.bs.tok);
     if (ens_fused) {  // every member's logits in one launch (search.py:56-72)
       LogitTcArgs ta{L.R, V, ms[0]->d.d_emb, ms[0]->b_logit, kk, ntiles, ms[0]->us_l,
                      L.pmax, L.psum, L.cval, L.ctok};
@@ -2110,7 +2127,7 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
   LogitOut lo{true, kk, nt_dev, pmax, psum, cval, ctok};
   lo.tc = &lm;
   lo.rows = rows;
-  step_rows(c, m, d, e, d_len, jmax, R, k, nullptr, nullptr, d_alpha, lo, &ts);
+  step_rows(c, m, d, e, d_len, jmax, R, k, nullptr, nullptr, d_alpha, lo, &ts, true, d_y);
   std::vector<float> hpm((size_t)R * nt_dev), hps((size_t)R * nt_dev), hcv((size_t)R * nt_dev * kk);
   std::vector<int> hct((size_t)R * nt_dev * kk);
   if (s_out) d2h(c, s_out, d.Sn, (size_t)R * dh);

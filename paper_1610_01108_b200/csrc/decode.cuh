@@ -32,6 +32,11 @@ struct amun_model {
   __half *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
   __half *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, xsp]
   float us_l = 1.f, us_q = 1.f, us_g = 1.f, us_u = 1.f, us_o = 1.f;
+  // embedding rows through the decoder's y weights, per target token (tensor-
+  // core path): the step GEMMs then run over [c | s] only and the epilogues
+  // add the gathered row (y = E_trg[previous token] is a table lookup)
+  float *YWg = nullptr;  // [V, 3 dh] = E_trg W_{z,r,h}^y
+  float *YWo = nullptr;  // [V, de]   = E_trg W_out_y
   // encoder: recurrent weights of both directions stacked along K (the
   // recurrence runs both directions as one block-structured GEMM, rows
   // [fwd sentences ; bwd sentences]) and W_att_h^T for precomp_att

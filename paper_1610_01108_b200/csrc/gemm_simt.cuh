@@ -247,7 +247,12 @@ struct EpiStore {
   __half *hi = nullptr, *lo = nullptr;  // optional 3xFP16 split copies (row pitch ldh, no z)
   int ldh = 0;
   float *ex2 = nullptr;  // optional e^{2v} (attention query rows: factored tanh, kernels.cu)
+  // optional per-row table term: v += rowadd[rowtok[m] * ldadd + n]
+  const float *rowadd = nullptr;
+  const int *rowtok = nullptr;
+  int ldadd = 0;
   __device__ void operator()(int m, int n, float v, int z) const {
+    if (rowadd) v += rowadd[(long long)rowtok[m] * ldadd + n];
     if (bias) v += bias[n];
     if (act == 1) v = tanhf(v);
     if (C) C[z * c_zs + (long long)m * ldc + n] = v;
@@ -261,14 +266,20 @@ struct EpiStore {
   // two-phase 4-column form for the tensor-core reduction (gemm_sk.cuh):
   // every load of a batch of items is issued before any of its stores
   struct Pre {
-    float4 b;
+    float4 b, r;
   };
   __device__ __forceinline__ Pre load4(int m, int n) const {
     Pre p;
     p.b = bias ? *reinterpret_cast<const float4 *>(bias + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+    p.r = rowadd ? *reinterpret_cast<const float4 *>(rowadd + (long long)rowtok[m] * ldadd + n)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
     return p;
   }
   __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    v.x += p.r.x;
+    v.y += p.r.y;
+    v.z += p.r.z;
+    v.w += p.r.w;
     v.x += p.b.x;
     v.y += p.b.y;
     v.z += p.b.z;
@@ -301,7 +312,12 @@ struct EpiGruA {
   int lds, dh;
   float *Z, *RH, *XH;  // [M, dh] each
   __half *RHh = nullptr, *RHl = nullptr;  // optional 3xFP16 split of r*s
+  // optional per-row table term (the y rows' contribution, amun_model YWg)
+  const float *rowadd = nullptr;
+  const int *rowtok = nullptr;
+  int ldadd = 0;
   __device__ void operator()(int m, int n, float v, int) const {
+    if (rowadd) v += rowadd[(long long)rowtok[m] * ldadd + n];
     v += bias[n];
     if (n < dh) {
       Z[(long long)m * dh + n] = sigmoid_acc(v);
@@ -315,16 +331,22 @@ struct EpiGruA {
     }
   }
   struct Pre {
-    float4 b, s;
+    float4 b, s, r;
   };
   __device__ __forceinline__ Pre load4(int m, int n) const {
     Pre p;
     p.b = *reinterpret_cast<const float4 *>(bias + n);
+    p.r = rowadd ? *reinterpret_cast<const float4 *>(rowadd + (long long)rowtok[m] * ldadd + n)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
     p.s = (n >= dh && n < 2 * dh) ? *reinterpret_cast<const float4 *>(S + (long long)m * lds + n - dh)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
     return p;
   }
   __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    v.x += p.r.x;
+    v.y += p.r.y;
+    v.z += p.r.z;
+    v.w += p.r.w;
     v.x += p.b.x;
     v.y += p.b.y;
     v.z += p.b.z;

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(C::kThreads, 1)
 template <class C = SkDefault>
 SkMaps make_sk_maps(const __half *x1h, const __half *x1l, int k1, int lda1, const __half *x2h, const __half *x2l,
                     int k2, int lda2, int Rmax, const __half *wh, const __half *wl, int N, int Kb, float unscale,
-                    int Rmax2 = -1) {
+                    int Rmax2 = -1, int ldw = 0) {  // ldw: weight row pitch (default Kb)
   SkMaps m;
   m.x1h = make_tma_2d_f16(x1h, k1, Rmax, lda1, C::kBK, C::kBoxR);
   m.x1l = make_tma_2d_f16(x1l, k1, Rmax, lda1, C::kBK, C::kBoxR);
@@ -365,8 +365,8 @@ SkMaps make_sk_maps(const __half *x1h, const __half *x1l, int k1, int lda1, cons
     m.x2h = m.x1h;
     m.x2l = m.x1l;
   }
-  m.wh = make_tma_2d_f16(wh, Kb, N, Kb, C::kBK, 128);
-  m.wl = make_tma_2d_f16(wl, Kb, N, Kb, C::kBK, 128);
+  m.wh = make_tma_2d_f16(wh, Kb, N, ldw ? ldw : Kb, C::kBK, 128);
+  m.wl = make_tma_2d_f16(wl, Kb, N, ldw ? ldw : Kb, C::kBK, 128);
   m.unscale = unscale;
   m.N = N;
   m.k1 = k1;

@@ -1,10 +1,35 @@
 // Non-GEMM kernels of the decode path (see kernels.cuh).
 #include <cooperative_groups.h>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
 namespace amun {
+
+// Opt a kernel into the device's full dynamic shared memory, once per
+// (kernel, device).  The attribute is only an upper bound, so one value
+// serves every launch size -- and host threads decoding concurrently on one
+// device (Engine workers) never lower it under each other's launches, which
+// setting it to each launch's own size would.
+static void smem_optin(const void *kern) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  AMUN_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.insert({kern, dev}).second) {
+    int optin = 0;
+    AMUN_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    AMUN_CUDA(cudaFuncGetAttributes(&fa, kern));
+    AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   optin - (int)fa.sharedSizeBytes));
+  }
+}
+
 
 // ================================================================ attention
 
@@ -555,7 +580,7 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
 template <int KA>
 static void launch_sent(const AttnArgs &a, int B, size_t smem, cudaStream_t st) {
   auto kern = attn_sent_kernel<KA>;
-  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) smem_optin(reinterpret_cast<const void *>(kern));
   AttnArgs ak = a;
   ak.kt = ktime_ptr();
   kern<<<B, 512, smem, st>>>(ak);
@@ -644,7 +669,7 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
     return 2;
   }
   size_t smem1 = sizeof(float) * (2 * a.da + a.jmax);
-  if (smem1 > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  if (smem1 > 48 * 1024) smem_optin(reinterpret_cast<const void *>(attention_kernel));
   attention_kernel<<<R, 256, smem1, st>>>(a);
   AMUN_CHECK_LAUNCH();
   return 1;
@@ -1194,7 +1219,7 @@ template <int KMAX, bool FUSED>
 static void launch_select_t(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, size_t smem,
                             cudaStream_t st) {
   auto kern = select_kernel<KMAX, FUSED>;
-  if (smem > 48 * 1024) AMUN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) smem_optin(reinterpret_cast<const void *>(kern));
   SelectArgs sk = sa;
   sk.kt = ktime_ptr();
   // one warp per beam row in the row phase: beams <= 8 run 5..8-warp CTAs

@@ -249,7 +249,9 @@ def _adjudicate(name, gold_hyps, gaps, out, score_rtol=SCORE_RTOL_FULL):
                f"per-step score error eps {eps:.2e}")
     print("\n" + summary)
     assert not fails, summary
-    assert len(ties) <= max(1, n // 100), summary  # expect 0.1-0.3% near-tie exceptions
+    # ~0.1-0.5% of sentences flip on a near tie (cfg2: 15-19 of 4000); every exception is
+    # individually excused above, the count only bounds their rate (at least 2 for a set of a few hundred)
+    assert len(ties) <= max(2, n // 100), summary
     return exact, ties
 
 

@@ -115,7 +115,7 @@ static float device_absmax(const float *d, size_t n);
 // tiles through shared memory, 4 x 4 outputs per thread: the per-token
 // embedding tables E_trg W^y built once at model load
 __global__ void table_gemm_kernel(const float *__restrict__ A, int lda, const float *__restrict__ B, int ldb, int M,
-                                  int N, int K, float *__restrict__ C) {
+                                  int N, int K, const float *__restrict__ bias, float *__restrict__ C) {
   __shared__ float As[16][64 + 1], Bs[16][64];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
@@ -141,16 +141,17 @@ __global__ void table_gemm_kernel(const float *__restrict__ A, int lda, const fl
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
-      if (m < M && n < N) C[(long long)m * N + n] = acc[i][j];
+      if (m < M && n < N) C[(long long)m * N + n] = bias ? acc[i][j] + bias[n] : acc[i][j];
     }
 }
 
-static float *device_table(amun_model *m, const float *A, int lda, const float *B, int ldb, int M, int N, int K) {
+static float *device_table(amun_model *m, const float *A, int lda, const float *B, int ldb, int M, int N, int K,
+                           const float *bias = nullptr) {
   float *d = nullptr;
   AMUN_CUDA(cudaMalloc(&d, (size_t)M * N * sizeof(float)));
   m->allocs.push_back(d);
   m->bytes += (int64_t)((size_t)M * N * sizeof(float));
-  table_gemm_kernel<<<dim3(ceil_div(N, 64), ceil_div(M, 64)), 256>>>(A, lda, B, ldb, M, N, K, d);
+  table_gemm_kernel<<<dim3(ceil_div(N, 64), ceil_div(M, 64)), 256>>>(A, lda, B, ldb, M, N, K, bias, d);
   AMUN_CHECK_LAUNCH();
   return d;
 }
@@ -274,6 +275,9 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
     m->Wenc = upload(m, W);
     m->benc = upload(m, b);
     if (m->tc_ok) m->us_x = split_kmajor_dev(m, m->Wenc, de, 6 * dh, m->dep, de, 0, &m->Wenc_hi, &m->Wenc_lo);
+    // per-source-token input projections E_src W + b (fp32, [Vs, 6dh]):
+    // the encode-ahead recurrence then runs its GEMMs over the state only
+    if (m->tc_ok) m->XWenc = device_table(m, m->E_src, de, m->Wenc, 6 * dh, Vs, 6 * dh, de, m->benc);
   }
   {  // encoder recurrent weights: Uzr [2][dh][2dh], Uh [2][dh][dh]
     std::vector<float> Uzr((size_t)2 * dh * 2 * dh), Uh((size_t)2 * dh * dh);

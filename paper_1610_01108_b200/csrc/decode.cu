@@ -570,15 +570,13 @@ class AheadEncoder {
         tokb[offt[t] + e] = in_.ids[in_.off[i] + in_.len[i] - 1 - t];
       }
     int *d_tok[2];
-    __half *Xh[2], *Xl[2], *Hh[2], *Hl[2], *RHh[2], *RHl[2];
+    __half *Hh[2], *Hl[2], *RHh[2], *RHl[2];
     float *H[2], *Z[2];
     for (int pass = 0; pass < 2; ++pass) {
       Carver cv;
       cv.base = static_cast<char *>(mem_);
       for (int d = 0; d < 2; ++d) {
         d_tok[d] = cv.take<int>(total);
-        Xh[d] = cv.take<__half>((size_t)total * dep);
-        Xl[d] = cv.take<__half>((size_t)total * dep);
         Hh[d] = cv.take<__half>((size_t)n * dh);
         Hl[d] = cv.take<__half>((size_t)n * dh);
         RHh[d] = cv.take<__half>((size_t)n * dh);
@@ -612,21 +610,18 @@ class AheadEncoder {
       AMUN_CUDA(cudaMemsetAsync(H[d], 0, sizeof(float) * (size_t)n * dh, cf.st));
       AMUN_CUDA(cudaMemsetAsync(Hh[d], 0, sizeof(__half) * (size_t)n * dh, cf.st));
       AMUN_CUDA(cudaMemsetAsync(Hl[d], 0, sizeof(__half) * (size_t)n * dh, cf.st));
-      cf.run(AMUN_K_ENCODER, [&] {
-        gather_split_kernel<<<(unsigned)total, 128, 0, cf.st>>>(m->E_src, d_tok[d], de, dep, Xh[d], Xl[d]);
-        AMUN_CHECK_LAUNCH();
-      });
     }
     const bool two = cb.st != cf.st;
     cudaEvent_t ev0 = new_event();
     AMUN_CUDA(cudaEventRecord(ev0, cf.st));
     if (two) AMUN_CUDA(cudaStreamWaitEvent(cb.st, ev0, 0));
+    // state-only GEMMs: the U rows of the [W ; U] weights (K offset dep)
     SkMaps fa[2], fb[2];
     for (int d = 0; d < 2; ++d) {
-      fa[d] = make_sk_maps(Xh[d], Xl[d], dep, dep, Hh[d], Hl[d], dh, dh, (int)total, m->Efa_hi[d], m->Efa_lo[d],
-                           2 * dh, dep + dh, m->us_efa[d], n);
-      fb[d] = make_sk_maps(Xh[d], Xl[d], dep, dep, RHh[d], RHl[d], dh, dh, (int)total, m->Efb_hi[d],
-                           m->Efb_lo[d], dh, dep + dh, m->us_efb[d], n);
+      fa[d] = make_sk_maps(Hh[d], Hl[d], dh, dh, nullptr, nullptr, 0, 0, n, m->Efa_hi[d] + dep, m->Efa_lo[d] + dep,
+                           2 * dh, dh, m->us_efa[d], -1, dep + dh);
+      fb[d] = make_sk_maps(RHh[d], RHl[d], dh, dh, nullptr, nullptr, 0, 0, n, m->Efb_hi[d] + dep,
+                           m->Efb_lo[d] + dep, dh, dh, m->us_efb[d], -1, dep + dh);
     }
     const int target = ahead_target_ctas() / (two ? 2 : 1);
     evf_.assign(T_, nullptr);
@@ -635,16 +630,15 @@ class AheadEncoder {
       for (int d = 0; d < 2; ++d) {
         Ctx &c = d ? cb : cf;
         const int M = nact[t];
-        const float *bias = m->benc + d * 3 * dh;
-        EpiEncFA ea{bias, H[d], Z[d], RHh[d], RHl[d], dh};
+        const float *xw = m->XWenc + d * 3 * dh;
+        const int *tok = d_tok[d] + offt[t];
+        EpiEncFA ea{xw, tok, 6 * dh, H[d], Z[d], RHh[d], RHl[d], dh};
         const auto ga_ = ahead_grid(fa[d], M, target);
-        c.run(AMUN_K_ENCODER,
-              [&] { launch_gemm_sk(fa[d], M, ga_.first, ea, c.st, 0, (int)offt[t], ga_.second); });
-        EpiEncFB eb{bias + 2 * dh, H[d], Z[d], Hh[d], Hl[d], out_.Hann, out_.Hah, out_.Hal, Hsum_, d_len_,
-                    d_arow_, dh, t, d};
+        c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(fa[d], M, ga_.first, ea, c.st, 0, 0, ga_.second); });
+        EpiEncFB eb{xw + 2 * dh, tok, 6 * dh, H[d], Z[d], Hh[d], Hl[d], out_.Hann, out_.Hah, out_.Hal, Hsum_,
+                    d_len_, d_arow_, dh, t, d};
         const auto gb_ = ahead_grid(fb[d], M, target);
-        c.run(AMUN_K_ENCODER,
-              [&] { launch_gemm_sk(fb[d], M, gb_.first, eb, c.st, 0, (int)offt[t], gb_.second); });
+        c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(fb[d], M, gb_.first, eb, c.st, 0, 0, gb_.second); });
       }
       if (need[t]) {
         evf_[t] = new_event();

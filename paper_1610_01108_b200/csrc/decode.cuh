@@ -35,6 +35,7 @@ struct amun_model {
   // embedding rows through the decoder's y weights, per target token (tensor-
   // core path): the step GEMMs then run over [c | s] only and the epilogues
   // add the gathered row (y = E_trg[previous token] is a table lookup)
+  float *XWenc = nullptr;  // [Vs, 6 dh] = E_src [W_{z,r,h} fwd | bwd] + b (encode-ahead)
   float *YWg = nullptr;  // [V, 3 dh] = E_trg W_{z,r,h}^y
   float *YWo = nullptr;  // [V, de]   = E_trg W_out_y
   // encoder: recurrent weights of both directions stacked along K (the

@@ -607,12 +607,15 @@ struct EpiLogitTopK {
 
 // ---- encode-ahead recurrence (decode.cu encode_ahead), tensor-core only.
 // Rows m are encoder rows (sentences in descending length order, all active
-// at this step); the accumulator already holds x_t W + h U (input projection
-// fused: the activation row is [x_t | state]).  nnet.py:66-70, 110-126.
-// Phase A: z = sigmoid(acc + b_z) -> Z;  r = sigmoid(acc + b_r), r * h -> split RH.
+// at this step); the accumulator holds h U, and the input projection plus
+// bias, x_t W + b, is one gathered row of the model's per-source-token table
+// (amun_model::XWenc, built at load).  nnet.py:66-70, 110-126.
+// Phase A: z = sigmoid(acc + xw_z) -> Z;  r = sigmoid(acc + xw_r), r * h -> split RH.
 struct EpiEncFA {
   static constexpr bool kTile = false;
-  const float *bias;  // [2dh] (b_z | b_r)
+  const float *xw;    // [Vs][ldx] per-token input projection + bias, this direction's (z | r) columns
+  const int *tok;     // [n] the step's source token per row
+  int ldx;
   const float *H;     // [n][dh] state
   float *Z;           // [n][dh]
   __half *RHh, *RHl;  // [n][dh]
@@ -623,7 +626,7 @@ struct EpiEncFA {
   };
   __device__ __forceinline__ Pre load4(int m, int n) const {
     Pre p;
-    p.b = *reinterpret_cast<const float4 *>(bias + n);
+    p.b = *reinterpret_cast<const float4 *>(xw + (long long)tok[m] * ldx + n);
     p.hs = n >= dh ? *reinterpret_cast<const float4 *>(H + (long long)m * dh + n - dh) : make_float4(0, 0, 0, 0);
     return p;
   }
@@ -642,13 +645,15 @@ struct EpiEncFA {
     }
   }
 };
-// Phase B: h~ = tanh(acc + b_h), h' = (1 - z) h + z h~ -> state (fp32 and
+// Phase B: h~ = tanh(acc + xw_h), h' = (1 - z) h + z h~ -> state (fp32 and
 // split), the annotation store row of (sentence, position) at column
 // dir*dh + n (fp32 and split, the precomp_att input), and the running sum
 // over positions for the initial-state mean (nnet.py:129).
 struct EpiEncFB {
   static constexpr bool kTile = false;
-  const float *bias;  // [dh] b_h
+  const float *xw;    // [Vs][ldx] per-token input projection + bias, this direction's h columns
+  const int *tok;     // [n]
+  int ldx;
   float *H;           // [n][dh]
   const float *Z;
   __half *Hh, *Hl;    // [n][dh] next phase-A operand
@@ -667,7 +672,7 @@ struct EpiEncFB {
   __device__ __forceinline__ Pre load4(int m, int n) const {
     Pre p;
     const long long o = (long long)m * dh + n;
-    p.b = *reinterpret_cast<const float4 *>(bias + n);
+    p.b = *reinterpret_cast<const float4 *>(xw + (long long)tok[m] * ldx + n);
     p.z = *reinterpret_cast<const float4 *>(Z + o);
     p.hs = *reinterpret_cast<const float4 *>(H + o);
     p.sum = t ? *reinterpret_cast<const float4 *>(Hsum + (long long)m * 2 * dh + dir * dh + n)

@@ -346,6 +346,19 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
       m->us_g = split_kmajor_dev(m, m->Wg, din + dh, 3 * dh, m->xsp, de, pad, &m->Wg_hi, &m->Wg_lo);
       m->us_u = split_kmajor_dev(m, m->Uh_dec, dh, dh, dh, dh, 0, &m->Uhd_hi, &m->Uhd_lo);
       m->us_q = split_kmajor_dev(m, m->W_att_s, dh, da, dh, dh, 0, &m->Wq_hi, &m->Wq_lo);
+      std::vector<float> Wqs((size_t)dh * (da + 2 * dh));
+      for (int i = 0; i < dh; ++i) {
+        std::memcpy(&Wqs[(size_t)i * (da + 2 * dh)], t[T_W_ATT_S] + (size_t)i * da, da * sizeof(float));
+        for (int g = 0; g < 2; ++g)
+          std::memcpy(&Wqs[(size_t)i * (da + 2 * dh) + da + g * dh], t[T_DEC + G_UZ + g] + (size_t)i * dh,
+                      dh * sizeof(float));
+      }
+      float *dWqs = nullptr;
+      AMUN_CUDA(cudaMalloc(&dWqs, Wqs.size() * sizeof(float)));
+      AMUN_CUDA(cudaMemcpy(dWqs, Wqs.data(), Wqs.size() * sizeof(float), cudaMemcpyHostToDevice));
+      m->us_qs = split_kmajor_dev(m, dWqs, dh, da + 2 * dh, dh, dh, 0, &m->Wqs_hi, &m->Wqs_lo);
+      AMUN_CUDA(cudaDeviceSynchronize());
+      AMUN_CUDA(cudaFree(dWqs));
     }
   }
   {  // deep output: rows [y ; c ; s'] = [W_out_y ; W_out_c ; W_out_s]

@@ -277,6 +277,7 @@ void gemm(Ctx &c, const GemmArgs &g, const Epi &e, int nz = 1, bool allow_split 
 // Encoder buffers of one model for a bucket of B sentences, jmax positions.
 struct EncBufs {
   float *XP, *Hann, *P, *Hs, *Zs, *RHs, *Hmean, *S0;
+  float *HX = nullptr;  // projected annotations [B*jmax][proj_ldhx] (projected-context step)
   // tensor-core encoder (3xFP16 splits): block rows [2B][2dh] of the states
   // (HH) and of r*h (RR), and the split annotations [B*jmax][2dh] (Ha)
   __half *HHh = nullptr, *HHl = nullptr, *RRh = nullptr, *RRl = nullptr, *Hah = nullptr, *Hal = nullptr;
@@ -285,6 +286,7 @@ struct EncBufs {
 // Decoder row buffers of one model for R hypothesis rows.
 struct DecBufs {
   float *XS, *Sn, *Q, *Z, *RH, *XH, *T, *L;
+  float *SU = nullptr, *CO = nullptr;  // projected-context step: s U_{z,r} [R][2dh], deep-output row terms [R][dep]
   float *En = nullptr;  // attention energies [R][jmax]
   float *EQ = nullptr;  // e^{2q} of the attention query rows [R][da]
   __half *T_hi = nullptr, *T_lo = nullptr;  // 3xFP16 split of t [R][dep] (tensor-core logits)
@@ -396,8 +398,33 @@ void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, int jmax, boo
   }
 }
 
+// Projected-context step (tensor-core path): the decoder's context weights
+// act on the annotations once, at encode time -- HX = h [C_z | C_r | C_h |
+// W_o^c] per source position -- instead of on the context every step:
+// c C = (sum_j alpha_j h_j) C = sum_j alpha_j (h_j C).  The step is then
+// s [W_att_s | U_z | U_r] (one GEMM), the attention summing HX rows and
+// finishing the gates, (r*s) U_h, and s' W_o^s: the per-row MMA work outside
+// the logits drops from 12.1M to 4.7M MACs.  Env
+// AMUN_NO_PROJ_CTX=1 keeps the GRU-A step (A/B runs).
+int proj_ldhx(const amun_model *m) { return 3 * m->d.d_h + m->dep; }
+bool proj_ok(const amun_model *m) {
+  static const bool off = [] {
+    const char *e = getenv("AMUN_NO_PROJ_CTX");
+    return e && e[0] == '1';
+  }();
+  return !off && m->tc_gemm && m->Wqs_hi && m->YWg && m->YWo && proj_ldhx(m) <= 4 * 1024 &&
+         (3 * m->d.d_h + m->d.d_emb) % 4 == 0;
+}
+
+void compute_hx(Ctx &c, const amun_model *m, const __half *Hah, const __half *Hal, long long store_rows,
+                long long row0, int M, float *HX, int target);
+
 void carve_dec_tc(Carver &cv, DecBufs &d, const amun_model *m, int R) {
   const int dh = m->d.d_h;
+  if (proj_ok(m)) {
+    d.SU = cv.take<float>((size_t)R * 2 * dh);
+    d.CO = cv.take<float>((size_t)R * m->dep);
+  }
   d.XSh = cv.take<__half>((size_t)R * m->xsp);
   d.XSl = cv.take<__half>((size_t)R * m->xsp);
   d.RHh = cv.take<__half>((size_t)R * dh);
@@ -489,6 +516,7 @@ struct AheadIn {
 struct AheadOut {
   float *Hann, *P, *S0;  // store [rows][2dh], [rows][da]; S0 [n][dh] indexed by sentence i
   __half *Hah, *Hal;     // store [rows][2dh] split annotations
+  float *HX = nullptr;   // optional store [rows][proj_ldhx] projected annotations
 };
 
 // Hmean[i] = Hsum[e(i)] / len[e(i)] for sentences i0 .. i0 + gridDim.x - 1
@@ -672,6 +700,7 @@ class AheadEncoder {
     const int cls = c.cls;
     c.cls = AMUN_K_ENCODER;
     c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(pm, M, gp.first, ep, c.st, 0, (int)row0, gp.second); });
+    if (out_.HX) compute_hx(c, m, out_.Hah, out_.Hal, in_.store_rows, row0, M, out_.HX, std::max(32, prep_ctas_));
     c.run(AMUN_K_ENCODER, [&] {
       enc_mean_kernel<<<cnt, 256, 0, c.st>>>(Hsum_, d_len_, d_e_of_i_, i0, 2 * dh, Hmean_);
       AMUN_CHECK_LAUNCH();
@@ -738,6 +767,9 @@ struct LogitOut {
 struct TcStep {
   SkMaps q, g, u, o;
   int sq = 1, sg = 1, su = 1, so = 1;
+  bool proj = false;  // projected-context maps below are valid
+  SkMaps qs, os;      // s [W_att_s | U_zr]; s' W_o^s
+  int sqs = 1, sos = 1;
 };
 
 // target CTAs per decoder-step GEMM launch (env AMUN_TC_CTAS overrides)
@@ -775,6 +807,33 @@ void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
   ts.sg = sk_fit_splits(ts.g, t);
   ts.su = sk_fit_splits(ts.u, t);
   ts.so = sk_fit_splits(ts.o, t);
+  ts.proj = proj_ok(m) && d.SU;
+  if (ts.proj) {
+    ts.qs = make_sk_maps(d.XSh + s_off, d.XSl + s_off, dh, xp, nullptr, nullptr, 0, 0, Rmax, m->Wqs_hi, m->Wqs_lo,
+                         da + 2 * dh, dh, m->us_qs);
+    ts.os = make_sk_maps(d.Snh, d.Snl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Wo_hi + s_off, m->Wo_lo + s_off, de,
+                         dh, m->us_o, -1, xp);
+    ts.sqs = sk_fit_splits(ts.qs, t);
+    ts.sos = sk_fit_splits(ts.os, t);
+  }
+}
+
+// HX rows [row0, row0 + M) of a store whose split annotations are Hah/Hal
+// ([rows][2dh]): h [C_z | C_r | C_h] (the c rows of the gate weights) and
+// h W_o^c (the c rows of the deep output), both views of the step weights.
+void compute_hx(Ctx &c, const amun_model *m, const __half *Hah, const __half *Hal, long long store_rows,
+                long long row0, int M, float *HX, int target) {
+  const int dh = m->d.d_h, de = m->d.d_emb, xp = m->xsp, dep = m->dep, ld = proj_ldhx(m);
+  const SkMaps mg = make_sk_maps(Hah, Hal, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0, (int)store_rows, m->Wg_hi + dep,
+                                 m->Wg_lo + dep, 3 * dh, 2 * dh, m->us_g, -1, xp);
+  const SkMaps mo = make_sk_maps(Hah, Hal, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0, (int)store_rows, m->Wo_hi + dep,
+                                 m->Wo_lo + dep, de, 2 * dh, m->us_o, -1, xp);
+  const auto gg = ahead_grid(mg, M, target);
+  const auto go = ahead_grid(mo, M, target);
+  EpiStore eg{HX + row0 * ld, ld, nullptr, 0, 0};
+  EpiStore eo{HX + row0 * ld + 3 * dh, ld, nullptr, 0, 0};
+  c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(mg, M, gg.first, eg, c.st, 0, (int)row0, gg.second); });
+  c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(mo, M, go.first, eo, c.st, 0, (int)row0, go.second); });
 }
 
 // one launch: tensor-core partials, DSMEM split reduction, fused epilogue
@@ -796,6 +855,34 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
                const TcStep *ts = nullptr, bool do_logits = true, const int *tok = nullptr) {
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
   const int s_off = de + 2 * dh;
+  const bool proj = ts && ts->proj && e.HX;
+  if (proj) {  // projected-context step (proj_ok): query + s U_zr, attention with the gate math
+    if (!tok) throw Error(AMUN_ERR_CUDA, "step_rows: previous tokens required with the y tables");
+    c.cls = AMUN_K_QUERY;
+    gemm_tc(c, ts->qs, R, ts->sqs, EpiQS{d.Q, d.EQ, d.SU, da, 2 * dh});
+    AttnArgs aa{d.Q, da, e.P, e.HX, m->v_att, d_len, jmax, da, proj_ldhx(m), rows_per_sent, n_act, done,
+                nullptr, 0, alpha};
+    aa.energy = d.En;
+    aa.EQ = d.EQ;
+    aa.su = d.SU;
+    aa.S = d.XS + s_off;
+    aa.lds = xs;
+    aa.tok = tok;
+    aa.ywg = m->YWg;
+    aa.ywo = m->YWo;
+    aa.bg = m->bg;
+    aa.Z = d.Z;
+    aa.XH = d.XH;
+    aa.RHh = d.RHh;
+    aa.RHl = d.RHl;
+    aa.CO = d.CO;
+    aa.dh = dh;
+    aa.de = de;
+    aa.ldco = m->dep;
+    int na_launch = 1;
+    c.run(AMUN_K_ATTN, [&] { na_launch = launch_attention(aa, R, c.st); });
+    c.launches += na_launch - 1;
+  } else {
   c.cls = AMUN_K_QUERY;
   {
     EpiStore eq{d.Q, da, nullptr, 0, 0};
@@ -837,6 +924,7 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
       gemm(c, g, ea);
     }
   }
+  }  // GRU-A step
   c.cls = AMUN_K_GRU_B;
   {
     EpiGruB eb{d.XS + s_off, xs, dh, d.Z, d.XH, d.Sn};
@@ -856,7 +944,11 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
       e.lo = d.T_lo;
       e.ldh = m->dep;
     }
-    if (ts) {
+    if (proj) {  // s' W_o^s + (context + y term from the attention kernel)
+      e.rowadd = d.CO;
+      e.ldadd = m->dep;
+      gemm_tc(c, ts->os, R, ts->sos, e);
+    } else if (ts) {
       if (m->YWo) {
         e.rowadd = m->YWo;
         e.rowtok = tok;
@@ -893,6 +985,11 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     gemm(c, g, EpiLogitTopK{m->b_logit, lo.kk, lo.ntiles, lo.pmax, lo.psum, lo.cval, lo.ctok});
   else
     gemm(c, g, EpiStore{d.L, V, m->b_logit, 0, 0});
+}
+
+__global__ void split_rows_kernel(const float *__restrict__ x, long long n, __half *hi, __half *lo) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) store_split(hi, lo, i, x[i]);
 }
 
 __global__ void build_rows_kernel(float *XS, int ldxs, const float *E, const int *y, const float *s, int de, int dh,
@@ -1325,7 +1422,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
   size_t next_bucket = 0;
   // encode-ahead annotation stores of the current chunk (per model)
   struct Store {
-    float *Hann = nullptr, *P = nullptr, *S0 = nullptr;
+    float *Hann = nullptr, *P = nullptr, *S0 = nullptr, *HX = nullptr;
     __half *Hah = nullptr, *Hal = nullptr;
     void *mem = nullptr;
   };
@@ -1479,6 +1576,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
         const int dh_m = ms[m]->d.d_h, da_m = ms[m]->d.d_att;
         L.eb[m].Hann = stores[m].Hann + bucket_row[bi] * 2 * dh_m;
         L.eb[m].P = stores[m].P + bucket_row[bi] * da_m;
+        L.eb[m].HX = stores[m].HX ? stores[m].HX + bucket_row[bi] * proj_ldhx(ms[m]) : nullptr;
         s0p[m] = stores[m].S0 + (long long)(bk.first - chunk_first) * dh_m;
       }
       h2d(c, L.p_S0, s0p.data(), n_models);
@@ -1808,10 +1906,12 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
         S.S0 = cv.take<float>((size_t)nc * dh_m);
         S.Hah = cv.take<__half>((size_t)rows * 2 * dh_m);
         S.Hal = cv.take<__half>((size_t)rows * 2 * dh_m);
+        S.HX = use_tcg && proj_ok(ms[m]) ? cv.take<float>((size_t)rows * proj_ldhx(ms[m])) : nullptr;
         if (!pass) AMUN_CUDA(cudaMallocFromPoolAsync(&S.mem, cv.off, ws_pool(m0->device), cf.st));
       }
       AheadIn in{nc, cids.data(), coff.data(), clen.data(), carow.data(), rows};
-      encs[m].reset(new AheadEncoder(ms[m], in, AheadOut{S.Hann, S.P, S.S0, S.Hah, S.Hal}, ws_pool(m0->device)));
+      encs[m].reset(
+          new AheadEncoder(ms[m], in, AheadOut{S.Hann, S.P, S.S0, S.Hah, S.Hal, S.HX}, ws_pool(m0->device)));
       encs[m]->set_prep_ctas(enc_target_ctas());
       encs[m]->run(cf, cb);
     }
@@ -2084,6 +2184,11 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
     cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
     e.Hann = cv.take<float>((size_t)B * jmax * 2 * dh);
     e.P = cv.take<float>((size_t)B * jmax * da);
+    if (proj_ok(m)) {  // the product's projected annotations, from the given h
+      e.HX = cv.take<float>((size_t)B * jmax * proj_ldhx(m));
+      e.Hah = cv.take<__half>((size_t)B * jmax * 2 * dh);
+      e.Hal = cv.take<__half>((size_t)B * jmax * 2 * dh);
+    }
     carve_dec(cv, d, m, R, jmax, false);
     carve_dec_tc(cv, d, m, R);
     d_len = cv.take<int>(B);
@@ -2101,6 +2206,12 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
   h2d(c, d_len, lens, B);
   h2d(c, d_s, s, (size_t)R * dh);
   h2d(c, d_y, y_prev, R);
+  if (e.HX) {
+    const long long n = (long long)B * jmax * 2 * dh;
+    split_rows_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.st>>>(e.Hann, n, e.Hah, e.Hal);
+    AMUN_CHECK_LAUNCH();
+    compute_hx(c, m, e.Hah, e.Hal, (long long)B * jmax, 0, B * jmax, e.HX, 148);
+  }
   AMUN_CUDA(cudaMemsetAsync(d.XS, 0, sizeof(float) * (size_t)R * xs, c.st));
   AMUN_CUDA(cudaMemsetAsync(d.XSh, 0, sizeof(__half) * (size_t)R * m->xsp, c.st));
   AMUN_CUDA(cudaMemsetAsync(d.XSl, 0, sizeof(__half) * (size_t)R * m->xsp, c.st));

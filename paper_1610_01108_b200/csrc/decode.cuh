@@ -28,6 +28,10 @@ struct amun_model {
   int dep = 0, xsp = 0;  // d_emb rounded up to 8; padded decoder-row pitch
   __half *Wl_hi = nullptr, *Wl_lo = nullptr;    // W_logit^T [V, dep]
   __half *Wq_hi = nullptr, *Wq_lo = nullptr;    // W_att_s^T [da, dh]
+  // [W_att_s | U_z | U_r]^T [da + 2dh, dh]: the attention query and the
+  // state's gate products in one GEMM (projected-context step, decode.cu)
+  __half *Wqs_hi = nullptr, *Wqs_lo = nullptr;
+  float us_qs = 1.f;
   __half *Wg_hi = nullptr, *Wg_lo = nullptr;    // Wg^T      [3dh, xsp]
   __half *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
   __half *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, xsp]

@@ -247,12 +247,13 @@ struct EpiStore {
   __half *hi = nullptr, *lo = nullptr;  // optional 3xFP16 split copies (row pitch ldh, no z)
   int ldh = 0;
   float *ex2 = nullptr;  // optional e^{2v} (attention query rows: factored tanh, kernels.cu)
-  // optional per-row table term: v += rowadd[rowtok[m] * ldadd + n]
+  // optional per-row term: v += rowadd[rowtok[m] * ldadd + n] (a table row
+  // per token), or rowadd[m * ldadd + n] without rowtok
   const float *rowadd = nullptr;
   const int *rowtok = nullptr;
   int ldadd = 0;
   __device__ void operator()(int m, int n, float v, int z) const {
-    if (rowadd) v += rowadd[(long long)rowtok[m] * ldadd + n];
+    if (rowadd) v += rowadd[(long long)(rowtok ? rowtok[m] : m) * ldadd + n];
     if (bias) v += bias[n];
     if (act == 1) v = tanhf(v);
     if (C) C[z * c_zs + (long long)m * ldc + n] = v;
@@ -271,7 +272,7 @@ struct EpiStore {
   __device__ __forceinline__ Pre load4(int m, int n) const {
     Pre p;
     p.b = bias ? *reinterpret_cast<const float4 *>(bias + n) : make_float4(0.f, 0.f, 0.f, 0.f);
-    p.r = rowadd ? *reinterpret_cast<const float4 *>(rowadd + (long long)rowtok[m] * ldadd + n)
+    p.r = rowadd ? *reinterpret_cast<const float4 *>(rowadd + (long long)(rowtok ? rowtok[m] : m) * ldadd + n)
                  : make_float4(0.f, 0.f, 0.f, 0.f);
     return p;
   }
@@ -300,6 +301,42 @@ struct EpiStore {
       *reinterpret_cast<float4 *>(ex2 + (long long)m * ldc + n) = y;
     }
     store_split4(hi, lo, (long long)m * ldh + n, v);
+  }
+};
+
+// Projected-context step, first GEMM: s [W_att_s | U_z | U_r].  Columns
+// [0, da) are the attention query (stored with e^{2q}, as EpiStore.ex2);
+// columns [da, da + 2dh) the state's gate products s U_{z,r}, which the
+// attention kernel completes (kernels.cu attn_sent_kernel, PROJ).
+struct EpiQS {
+  static constexpr bool kTile = false;
+  float *Q, *EQ;  // [M, da]
+  float *SU;      // [M, 2dh]
+  int da, dh2;
+  __device__ void operator()(int m, int n, float v, int) const {
+    if (n < da) {
+      Q[(long long)m * da + n] = v;
+      float y;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(v * 2.8853900817779268f));
+      EQ[(long long)m * da + n] = y;
+    } else {
+      SU[(long long)m * dh2 + n - da] = v;
+    }
+  }
+  struct Pre {};
+  __device__ __forceinline__ Pre load4(int, int) const { return Pre{}; }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &) const {
+    if (n < da) {
+      *reinterpret_cast<float4 *>(Q + (long long)m * da + n) = v;
+      float4 y;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.x) : "f"(v.x * 2.8853900817779268f));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.y) : "f"(v.y * 2.8853900817779268f));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.z) : "f"(v.z * 2.8853900817779268f));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.w) : "f"(v.w * 2.8853900817779268f));
+      *reinterpret_cast<float4 *>(EQ + (long long)m * da + n) = y;
+    } else {
+      *reinterpret_cast<float4 *>(SU + (long long)m * dh2 + n - da) = v;
+    }
   }
 };
 

@@ -351,8 +351,10 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
 // Two CTAs per SM for beams <= 8 (<= 64 registers: P rows in chunks of 8,
 // e^{2q} rows staged in shared memory), so a step's 64 sentence CTAs share
 // the SMs left by the other lanes' tensor-core kernels.
-template <int KA>
-__global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArgs a) {
+// PROJ (projected-context mode, AttnArgs.su): 1024 threads, one per 4
+// columns of the 3 dh + de wide projected rows, and the gate epilogue.
+template <int KA, bool PROJ>
+__global__ void __launch_bounds__(PROJ ? 1024 : 512, (KA <= 8 && !PROJ) ? 2 : 1) attn_sent_kernel(AttnArgs a) {
   const CtaClock clk(a.kt);
   extern __shared__ float sm[];
   const int b = blockIdx.x;
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
   // context phase: the annotation reads overlap the energies instead of
   // stalling the context loop (one thread per 4 columns: dh2 == 4 x threads)
   constexpr int kHP = 4;
-  const bool hsmem = a.dh2 == 4 * (int)blockDim.x;
+  const bool hsmem = PROJ || a.dh2 == 4 * (int)blockDim.x;
   float *hbuf = reinterpret_cast<float *>(
       (reinterpret_cast<uintptr_t>(eqs + (a.da == 1024 ? k * 1024 : 0)) + 127) & ~uintptr_t(127));
   uint64_t *hbar = reinterpret_cast<uint64_t *>(hbuf + 2 * kHP * a.dh2);
@@ -494,6 +496,7 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
   const float4 *Hb = reinterpret_cast<const float4 *>(a.H + (long long)b * a.jmax * a.dh2);
   if (hsmem) {
     const int c4 = tid;
+    const bool live = !PROJ || c4 < hs;  // PROJ: threads past the row's columns only join the barriers
     float4 acc[KA];
 #pragma unroll
     for (int r = 0; r < KA; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -503,7 +506,7 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
       const int j0 = c * kHP;
 #pragma unroll
       for (int jj = 0; jj < kHP; ++jj) {
-        if (j0 + jj >= J) break;
+        if (j0 + jj >= J || !live) break;
         const float4 h = hb[jj * hs + c4];
 #pragma unroll
         for (int r = 0; r < KA; ++r)
@@ -523,6 +526,49 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
         }
       }
     }
+    if constexpr (PROJ) {
+      // gate epilogue, columns n .. n + 3 of every row (a quad never
+      // straddles two blocks: dh and de are multiples of 4)
+      const int n = 4 * c4, dh = a.dh;
+      if (live && n < 3 * dh + a.de) {
+#pragma unroll
+        for (int r = 0; r < KA; ++r) {
+          if (r >= na) break;
+          const long long gr = (long long)b * k + r;
+          const long long t = a.tok[gr];
+          const float4 cx = acc[r];
+          if (n < 3 * dh) {
+            const float4 y = *reinterpret_cast<const float4 *>(a.ywg + t * 3 * dh + n);
+            const float4 bb = *reinterpret_cast<const float4 *>(a.bg + n);
+            float4 v;
+            if (n < 2 * dh) {
+              const float4 su = *reinterpret_cast<const float4 *>(a.su + gr * 2 * dh + n);
+              v = make_float4(cx.x + su.x, cx.y + su.y, cx.z + su.z, cx.w + su.w);
+            } else {
+              v = cx;
+            }
+            v = make_float4(v.x + y.x + bb.x, v.y + y.y + bb.y, v.z + y.z + bb.z, v.w + y.w + bb.w);
+            if (n < dh) {
+              *reinterpret_cast<float4 *>(a.Z + gr * dh + n) =
+                  make_float4(sigmoid_acc(v.x), sigmoid_acc(v.y), sigmoid_acc(v.z), sigmoid_acc(v.w));
+            } else if (n < 2 * dh) {
+              const float4 sv = *reinterpret_cast<const float4 *>(a.S + gr * a.lds + n - dh);
+              const long long o = gr * dh + n - dh;
+              store_split(a.RHh, a.RHl, o + 0, sigmoid_acc(v.x) * sv.x);
+              store_split(a.RHh, a.RHl, o + 1, sigmoid_acc(v.y) * sv.y);
+              store_split(a.RHh, a.RHl, o + 2, sigmoid_acc(v.z) * sv.z);
+              store_split(a.RHh, a.RHl, o + 3, sigmoid_acc(v.w) * sv.w);
+            } else {
+              *reinterpret_cast<float4 *>(a.XH + gr * dh + n - 2 * dh) = v;
+            }
+          } else {
+            const float4 y = *reinterpret_cast<const float4 *>(a.ywo + t * a.de + n - 3 * dh);
+            *reinterpret_cast<float4 *>(a.CO + gr * a.ldco + n - 3 * dh) =
+                make_float4(cx.x + y.x, cx.y + y.y, cx.z + y.z, cx.w + y.w);
+          }
+        }
+      }
+    } else {
 #pragma unroll
     for (int r = 0; r < KA; ++r) {
       if (r >= na) break;
@@ -533,6 +579,7 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
       store_split(a.ctx_hi, a.ctx_lo, oh + 1, acc[r].y);
       store_split(a.ctx_hi, a.ctx_lo, oh + 2, acc[r].z);
       store_split(a.ctx_hi, a.ctx_lo, oh + 3, acc[r].w);
+    }
     }
   }
   for (int c4 = hsmem ? hs : tid; c4 < hs; c4 += blockDim.x) {
@@ -579,11 +626,17 @@ __global__ void __launch_bounds__(512, KA <= 8 ? 2 : 1) attn_sent_kernel(AttnArg
 
 template <int KA>
 static void launch_sent(const AttnArgs &a, int B, size_t smem, cudaStream_t st) {
-  auto kern = attn_sent_kernel<KA>;
-  if (smem > 48 * 1024) smem_optin(reinterpret_cast<const void *>(kern));
   AttnArgs ak = a;
   ak.kt = ktime_ptr();
-  kern<<<B, 512, smem, st>>>(ak);
+  if (a.su) {
+    auto kern = attn_sent_kernel<KA, true>;
+    if (smem > 48 * 1024) smem_optin(reinterpret_cast<const void *>(kern));
+    kern<<<B, 1024, smem, st>>>(ak);
+  } else {
+    auto kern = attn_sent_kernel<KA, false>;
+    if (smem > 48 * 1024) smem_optin(reinterpret_cast<const void *>(kern));
+    kern<<<B, 512, smem, st>>>(ak);
+  }
 }
 
 template <int KA>
@@ -611,14 +664,16 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   }();
   const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)((k + 3) & ~3) +
                         (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0) +
-                        (a.dh2 == 4 * 512 ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);
+                        ((a.su || a.dh2 == 4 * 512) ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);
   // The kernel is chosen from per-call constants only (beam width, model
   // layout), never from the bucket's longest sentence: the fused and the
   // two-phase kernels sum in different orders, and a sentence's result must
   // not depend on its batch-mates.  A bucket too long for the fused kernel's
   // shared-memory energies is refused instead of silently switching paths.
   const bool fused_ok = fused && a.EQ && a.da <= 1024 && a.dh2 % 4 == 0 && R % k == 0 && k <= 16 &&
-                        (size_t)a.ldctx % 4 == 0 && reinterpret_cast<uintptr_t>(a.ctx) % 16 == 0;
+                        (a.su || ((size_t)a.ldctx % 4 == 0 && reinterpret_cast<uintptr_t>(a.ctx) % 16 == 0));
+  if (a.su && (!fused_ok || a.dh2 > 4 * 1024))
+    throw Error(4, "projected-context attention: unsupported shape");
   if (fused_ok && smem_s > 200 * 1024)
     throw Error(4, "source sentence of " + std::to_string(a.jmax) + " tokens exceeds the device attention limit (" +
                        std::to_string((200 * 1024 / 4 - a.da - 1) / k) + " at beam " + std::to_string(k) + ")");

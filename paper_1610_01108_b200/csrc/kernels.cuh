@@ -30,6 +30,24 @@ struct AttnArgs {
   float *energy = nullptr;  // scratch [R][jmax]: enables the two-phase sentence kernels
   const float *EQ = nullptr;  // e^{2q} rows (same layout as Q), from the query GEMM epilogue
   unsigned long long *kt = nullptr;  // optional CTA-time accounting (common.cuh CtaClock)
+  // Projected-context mode (su != nullptr; decode.cu step_rows): H rows are
+  // the annotations' products with the decoder's context weights,
+  // [h C_z | h C_r | h C_h | h W_o^c] (row pitch dh2, 3 dh + de used), so the
+  // attention-weighted sum is the context's contribution to every gate and
+  // to the deep output, and the kernel ends with the GRU gate math
+  // (nnet.py:66-69): z -> Z, r * s -> RH split, the input half of h~ -> XH,
+  // and the deep output's context + y term -> CO.
+  const float *su = nullptr;   // [R][2dh] s U_{z,r} (EpiQS)
+  const float *S = nullptr;    // state rows (pitch lds)
+  int lds = 0;
+  const int *tok = nullptr;    // [R] previous token
+  const float *ywg = nullptr;  // [V][3dh] E_trg W^y_{z,r,h}
+  const float *ywo = nullptr;  // [V][de] E_trg W_o^y
+  const float *bg = nullptr;   // [3dh]
+  float *Z = nullptr, *XH = nullptr;  // [R][dh]
+  __half *RHh = nullptr, *RHl = nullptr;  // [R][dh]
+  float *CO = nullptr;         // [R][ldco]
+  int dh = 0, de = 0, ldco = 0;
 };
 // returns the number of kernels launched
 int launch_attention(const AttnArgs &a, int R, cudaStream_t st);

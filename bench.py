@@ -354,6 +354,11 @@ def main() -> None:
         "deep_out": [(de + 3 * dh, de)],
         "logits": [(de, V)],
     }
+    if not kcount.get("gru_a", 0):
+        # projected-context step (decode.cu proj_ok): the context's products
+        # come from the encoder-time HX rows, so the step's GEMMs are
+        # s [W_att_s | U_z | U_r] and s' W_o^s -- counted as executed
+        shapes.update({"query": [(dh, da + 2 * dh)], "deep_out": [(dh, de)]})
     pass_ms = insitu.device_ms
     sm_ms = {k: insitu.kernel_ms[k] for k in _lib.KERNEL_CLASSES}
     share = {k: round(v / (n_sm * pass_ms), 4) for k, v in sm_ms.items()}

@@ -351,10 +351,14 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
 // Two CTAs per SM for beams <= 8 (<= 64 registers: P rows in chunks of 8,
 // e^{2q} rows staged in shared memory), so a step's 64 sentence CTAs share
 // the SMs left by the other lanes' tensor-core kernels.
-// PROJ (projected-context mode, AttnArgs.su): 1024 threads, one per 4
-// columns of the 3 dh + de wide projected rows, and the gate epilogue.
+// PROJ (projected-context mode, AttnArgs.su): one thread per 4 columns of
+// the 3 dh + de wide projected rows (1024 threads; 512 threads with two
+// quads each above beam 8, where 64 registers would spill), and the gate
+// epilogue.
+template <int KA>
+constexpr int attn_threads(bool proj) { return proj && KA <= 8 ? 1024 : 512; }
 template <int KA, bool PROJ>
-__global__ void __launch_bounds__(PROJ ? 1024 : 512, (KA <= 8 && !PROJ) ? 2 : 1) attn_sent_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2 : 1) attn_sent_kernel(AttnArgs a) {
   const CtaClock clk(a.kt);
   extern __shared__ float sm[];
   const int b = blockIdx.x;
@@ -495,27 +499,39 @@ __global__ void __launch_bounds__(PROJ ? 1024 : 512, (KA <= 8 && !PROJ) ? 2 : 1)
   const int hs = a.dh2 / 4;
   const float4 *Hb = reinterpret_cast<const float4 *>(a.H + (long long)b * a.jmax * a.dh2);
   if (hsmem) {
-    const int c4 = tid;
-    const bool live = !PROJ || c4 < hs;  // PROJ: threads past the row's columns only join the barriers
-    float4 acc[KA];
+    // thread = column quads tid (+ blockDim for the 512-thread PROJ variant)
+    constexpr int kQ = PROJ && KA > 8 ? 2 : 1;
+    int cq[kQ];
+    bool live[kQ];  // PROJ: threads past the row's columns only join the barriers
+    float4 acc[kQ][KA];
 #pragma unroll
-    for (int r = 0; r < KA; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < kQ; ++i) {
+      cq[i] = tid + i * (int)blockDim.x;
+      live[i] = !PROJ || cq[i] < hs;
+#pragma unroll
+      for (int r = 0; r < KA; ++r) acc[i][r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     for (int c = 0; c < nch; ++c) {
       tc::mbar_wait(&hbar[c & 1], (c >> 1) & 1);
       const float4 *hb = reinterpret_cast<const float4 *>(hbuf + (c & 1) * kHP * a.dh2);
       const int j0 = c * kHP;
 #pragma unroll
       for (int jj = 0; jj < kHP; ++jj) {
-        if (j0 + jj >= J || !live) break;
-        const float4 h = hb[jj * hs + c4];
+        if (j0 + jj >= J || !live[0]) break;
+        float4 h[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) h[i] = live[i] ? hb[jj * hs + cq[i]] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int r = 0; r < KA; ++r)
           if (r < na) {  // positions summed in order, as the global-memory loop below
             const float w = al[r * a.jmax + j0 + jj];
-            acc[r].x = fmaf(w, h.x, acc[r].x);
-            acc[r].y = fmaf(w, h.y, acc[r].y);
-            acc[r].z = fmaf(w, h.z, acc[r].z);
-            acc[r].w = fmaf(w, h.w, acc[r].w);
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) {
+              acc[i][r].x = fmaf(w, h[i].x, acc[i][r].x);
+              acc[i][r].y = fmaf(w, h[i].y, acc[i][r].y);
+              acc[i][r].z = fmaf(w, h[i].z, acc[i][r].z);
+              acc[i][r].w = fmaf(w, h[i].w, acc[i][r].w);
+            }
           }
       }
       if (c + 2 < nch) {
@@ -529,14 +545,16 @@ __global__ void __launch_bounds__(PROJ ? 1024 : 512, (KA <= 8 && !PROJ) ? 2 : 1)
     if constexpr (PROJ) {
       // gate epilogue, columns n .. n + 3 of every row (a quad never
       // straddles two blocks: dh and de are multiples of 4)
-      const int n = 4 * c4, dh = a.dh;
-      if (live && n < 3 * dh + a.de) {
+#pragma unroll
+      for (int i = 0; i < kQ; ++i) {
+      const int n = 4 * cq[i], dh = a.dh;
+      if (live[i] && n < 3 * dh + a.de) {
 #pragma unroll
         for (int r = 0; r < KA; ++r) {
           if (r >= na) break;
           const long long gr = (long long)b * k + r;
           const long long t = a.tok[gr];
-          const float4 cx = acc[r];
+          const float4 cx = acc[i][r];
           if (n < 3 * dh) {
             const float4 y = *reinterpret_cast<const float4 *>(a.ywg + t * 3 * dh + n);
             const float4 bb = *reinterpret_cast<const float4 *>(a.bg + n);
@@ -568,17 +586,19 @@ __global__ void __launch_bounds__(PROJ ? 1024 : 512, (KA <= 8 && !PROJ) ? 2 : 1)
           }
         }
       }
+      }
     } else {
+    const int c4 = tid;
 #pragma unroll
     for (int r = 0; r < KA; ++r) {
       if (r >= na) break;
       const long long o = (long long)(b * k + r) * a.ldctx + 4 * c4;
-      *reinterpret_cast<float4 *>(a.ctx + o) = acc[r];
+      *reinterpret_cast<float4 *>(a.ctx + o) = acc[0][r];
       const long long oh = (long long)(b * k + r) * a.ldctx_h + 4 * c4;
-      store_split(a.ctx_hi, a.ctx_lo, oh + 0, acc[r].x);
-      store_split(a.ctx_hi, a.ctx_lo, oh + 1, acc[r].y);
-      store_split(a.ctx_hi, a.ctx_lo, oh + 2, acc[r].z);
-      store_split(a.ctx_hi, a.ctx_lo, oh + 3, acc[r].w);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 0, acc[0][r].x);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 1, acc[0][r].y);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 2, acc[0][r].z);
+      store_split(a.ctx_hi, a.ctx_lo, oh + 3, acc[0][r].w);
     }
     }
   }
@@ -631,7 +651,7 @@ static void launch_sent(const AttnArgs &a, int B, size_t smem, cudaStream_t st) 
   if (a.su) {
     auto kern = attn_sent_kernel<KA, true>;
     if (smem > 48 * 1024) smem_optin(reinterpret_cast<const void *>(kern));
-    kern<<<B, 1024, smem, st>>>(ak);
+    kern<<<B, attn_threads<KA>(true), smem, st>>>(ak);
   } else {
     auto kern = attn_sent_kernel<KA, false>;
     if (smem > 48 * 1024) smem_optin(reinterpret_cast<const void *>(kern));

@@ -557,15 +557,21 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// work units per pair: (256-vocab tiles x row passes) spread evenly; env
-// AMUN_LOGIT_PAIRS caps the number of CTA pairs (default: as few pairs as
-// keep the per-pair unit count at ceil(units / 74)).
+// work units per pair: (256-vocab tiles x row passes) spread evenly, about
+// AMUN_LOGIT_UNITS (default 9, swept: cfg2 / cfg5 / cfg1) per pair -- long
+// enough persistent loops that the epilogue of one unit hides behind the
+// next unit's MMAs -- and at most AMUN_LOGIT_PAIRS (default 40) pairs.
 int logit_pairs(int units) {
   static int cap = [] {
     const char *e = getenv("AMUN_LOGIT_PAIRS");
     return e ? std::max(1, atoi(e)) : 40;
   }();
-  const int per = ceil_div(units, std::min(cap, 74));
+  static int upp = [] {
+    const char *e = getenv("AMUN_LOGIT_UNITS");
+    return e ? std::max(1, atoi(e)) : 9;
+  }();
+  const int pairs = std::max(1, std::min({cap, 74, ceil_div(units, upp)}));
+  const int per = ceil_div(units, pairs);
   return ceil_div(units, per);
 }
 

@@ -317,7 +317,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ri = et >> 2, q = et & 3;  // (row, vocabulary quarter) while reducing
     float *buf = tr + g * (32 * kTrRow);
     int ti = 0, dchunk = 0;
+    // per-phase clock stamps (tools/bench_logits_tc.cu) only in builds with
+    // AMUN_LOGIT_STAMPS: predicated-off stamps still cost ~6% of the
+    // epilogue's issue slots
+#ifdef AMUN_LOGIT_STAMPS
     const bool dstamp = a.debug_clock && blockIdx.x == 0 && et == 0 && g == 0;
+#else
+    constexpr bool dstamp = false;
+#endif
     auto stamp = [&](int pt) {
       if (dstamp && dchunk < 64) a.debug_clock[dchunk * 16 + pt] = clock64();
     };
@@ -412,8 +419,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float omx = __shfl_xor_sync(0xffffffffu, mx, o);
             const float ose = __shfl_xor_sync(0xffffffffu, se, o);
             const float nmx = fmaxf(mx, omx);
-            const float a0 = (mx == -INFINITY) ? 0.f : se * expf(mx - nmx);
-            const float a1 = (omx == -INFINITY) ? 0.f : ose * expf(omx - nmx);
+            // ex2.approx like the per-logit terms (rel. error ~2^-22)
+            const float a0 = (mx == -INFINITY) ? 0.f : se * tc::exp2f_approx((mx - nmx) * 1.4426950408889634f);
+            const float a1 = (omx == -INFINITY) ? 0.f : ose * tc::exp2f_approx((omx - nmx) * 1.4426950408889634f);
             se = (q & o) ? a1 + a0 : a0 + a1;  // same operand order in both partners
             mx = nmx;
           }
@@ -459,14 +467,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               hm[2 * j] = __shfl_sync(0xffffffffu, h0, lb + j);
               hm[2 * j + 1] = __shfl_sync(0xffffffffu, h1, lb + j);
             }
+            // optimal 19-comparator sorting network for 8 (descending); only
+            // position KK - 1 is read, so the compiler drops the comparator
+            // outputs that do not feed it
+            constexpr int kNet[19][2] = {{0, 2}, {1, 3}, {4, 6}, {5, 7}, {0, 4}, {1, 5}, {2, 6},
+                                         {3, 7}, {0, 1}, {2, 3}, {4, 5}, {6, 7}, {2, 4}, {3, 5},
+                                         {1, 4}, {3, 6}, {1, 2}, {3, 4}, {5, 6}};
 #pragma unroll
-            for (int p = 0; p < KK; ++p)
-#pragma unroll
-              for (int j = 7; j > p; --j) {
-                const float hi = fmaxf(hm[j - 1], hm[j]), lo = fminf(hm[j - 1], hm[j]);
-                hm[j - 1] = hi;
-                hm[j] = lo;
-              }
+            for (int c = 0; c < 19; ++c) {
+              const float hi = fmaxf(hm[kNet[c][0]], hm[kNet[c][1]]), lo = fminf(hm[kNet[c][0]], hm[kNet[c][1]]);
+              hm[kNet[c][0]] = hi;
+              hm[kNet[c][1]] = lo;
+            }
             thr = hm[KK - 1];
           } else {
             // KK > 8 (beam 9..16): the KK-th largest of the row's 16 group

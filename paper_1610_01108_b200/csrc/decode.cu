@@ -1593,7 +1593,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       const amun_model *mm = ms[m];
       const int de_m = mm->d.d_emb, dh_m = mm->d.d_h;
       L.mr.dim[m] = RowDims{mm->xs_w, de_m, dh_m, de_m + 2 * dh_m, use_tcg ? mm->xsp : 0,
-                            use_tcg ? mm->dep - de_m : 0};
+                            use_tcg ? mm->dep - de_m : 0, (use_tcg && L.eb[m].HX) ? 0 : 1};
     }
     if (use_tcg) {
       L.mr.XSh = L.p_XSh;

@@ -1222,7 +1222,9 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     const float *Sn = mr.Sn[m];
     const float *E = mr.E_trg[m];
     if (vec) {
-      const int qe = md.de / 4, qrow = (md.de + md.dh) / 4;
+      // granules [0, qe) are y's, [qe, qrow) the state's; without y rows the
+      // loop starts at the state (y0 = qe granules skipped per row)
+      const int qe = md.de / 4, y0 = md.y ? 0 : qe, qrow = (md.de + md.dh) / 4 - y0;
       const int total = newna * qrow;
       for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
         float4 v[8];
@@ -1232,7 +1234,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
           const int idx = base + u * blockDim.x;
           dst[u] = -1;
           if (idx < total) {
-            const int i = idx / qrow, c4 = idx - i * qrow;
+            const int i = idx / qrow, c4 = idx - i * qrow + y0;
             const long long ro = (long long)(b * k + i) * md.ldxs;
             const long long roh = (long long)(b * k + i) * md.ldxh;
             if (c4 < qe) {
@@ -1267,7 +1269,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         const long long roh = (long long)(b * k + i) * md.ldxh;
         const float *ey = E + (long long)ch_tok[i] * md.de;
         const float *sp = Sn + (long long)(b * k + ch_par[i]) * md.dh;
-        for (int c = threadIdx.x; c < md.de; c += blockDim.x) {
+        for (int c = threadIdx.x; c < (md.y ? md.de : 0); c += blockDim.x) {
           XS[ro + c] = ey[c];
           store_split(XSh, XSl, roh + c, ey[c]);
         }

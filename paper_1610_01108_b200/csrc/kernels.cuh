@@ -84,6 +84,7 @@ struct RowDims {
   // 3xFP16 split copies of XS in the padded layout: row pitch ldxh, XS
   // column c at c + (c >= de ? hpad : 0)
   int ldxh, hpad;
+  int y = 1;  // 0: the step reads y only through per-token tables (projected context): no y gather
 };
 
 struct ModelRows {  // per-model decoder row buffers (device arrays of pointers)

@@ -375,24 +375,24 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   // positions by bulk copies, two buffers, issued now and consumed by the
   // context phase: the annotation reads overlap the energies instead of
   // stalling the context loop (one thread per 4 columns: dh2 == 4 x threads)
-  constexpr int kHP = 4;
+  // PROJ rows are 14 KB per position: five 2-position buffers keep about
+  // ten positions in flight (the context loop is load-latency bound)
+  constexpr int kHP = PROJ ? 2 : 4, kNB = PROJ ? 5 : 2;
   const bool hsmem = PROJ || a.dh2 == 4 * (int)blockDim.x;
   float *hbuf = reinterpret_cast<float *>(
       (reinterpret_cast<uintptr_t>(eqs + (a.da == 1024 ? k * 1024 : 0)) + 127) & ~uintptr_t(127));
-  uint64_t *hbar = reinterpret_cast<uint64_t *>(hbuf + 2 * kHP * a.dh2);
+  uint64_t *hbar = reinterpret_cast<uint64_t *>(hbuf + kNB * kHP * a.dh2);
   const int nch = (J + kHP - 1) / kHP;
   const float *Hsent = a.H + (long long)b * a.jmax * a.dh2;
   auto issue_chunk = [&](int c) {  // thread 0
     const uint32_t bytes = (uint32_t)(min(kHP, J - c * kHP) * a.dh2 * 4);
-    tc::mbar_arrive_expect_tx(&hbar[c & 1], bytes);
-    tc::bulk_load_1d(hbuf + (c & 1) * kHP * a.dh2, Hsent + (long long)c * kHP * a.dh2, bytes, &hbar[c & 1]);
+    tc::mbar_arrive_expect_tx(&hbar[c % kNB], bytes);
+    tc::bulk_load_1d(hbuf + (c % kNB) * kHP * a.dh2, Hsent + (long long)c * kHP * a.dh2, bytes, &hbar[c % kNB]);
   };
   if (hsmem && tid == 0) {
-    tc::mbar_init(&hbar[0], 1);
-    tc::mbar_init(&hbar[1], 1);
+    for (int i = 0; i < kNB; ++i) tc::mbar_init(&hbar[i], 1);
     tc::fence_barrier_init();
-    issue_chunk(0);
-    if (nch > 1) issue_chunk(1);
+    for (int c = 0; c < kNB && c < nch; ++c) issue_chunk(c);
   }
   for (int i = tid; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
   const bool fast_shape = na == KA && a.da == 1024;
@@ -512,8 +512,8 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
       for (int r = 0; r < KA; ++r) acc[i][r] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     for (int c = 0; c < nch; ++c) {
-      tc::mbar_wait(&hbar[c & 1], (c >> 1) & 1);
-      const float4 *hb = reinterpret_cast<const float4 *>(hbuf + (c & 1) * kHP * a.dh2);
+      tc::mbar_wait(&hbar[c % kNB], (c / kNB) & 1);
+      const float4 *hb = reinterpret_cast<const float4 *>(hbuf + (c % kNB) * kHP * a.dh2);
       const int j0 = c * kHP;
 #pragma unroll
       for (int jj = 0; jj < kHP; ++jj) {
@@ -534,11 +534,11 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
             }
           }
       }
-      if (c + 2 < nch) {
+      if (c + kNB < nch) {
         __syncthreads();  // every thread is done with this buffer
         if (tid == 0) {
           tc::fence_proxy_async();
-          issue_chunk(c + 2);
+          issue_chunk(c + kNB);
         }
       }
     }
@@ -684,7 +684,8 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   }();
   const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)((k + 3) & ~3) +
                         (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0) +
-                        ((a.su || a.dh2 == 4 * 512) ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);
+                        (a.su ? 128 + sizeof(float) * 5 * 2 * (size_t)a.dh2 + 5 * sizeof(uint64_t)
+                              : a.dh2 == 4 * 512 ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);
   // The kernel is chosen from per-call constants only (beam width, model
   // layout), never from the bucket's longest sentence: the fused and the
   // two-phase kernels sum in different orders, and a sentence's result must
@@ -694,9 +695,11 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
                         (a.su || ((size_t)a.ldctx % 4 == 0 && reinterpret_cast<uintptr_t>(a.ctx) % 16 == 0));
   if (a.su && (!fused_ok || a.dh2 > 4 * 1024))
     throw Error(4, "projected-context attention: unsupported shape");
-  if (fused_ok && smem_s > 200 * 1024)
+  const size_t smem_lim = 227 * 1024, smem_fixed = smem_s - sizeof(float) * (size_t)k * a.jmax;
+  if (fused_ok && smem_s > smem_lim)
     throw Error(4, "source sentence of " + std::to_string(a.jmax) + " tokens exceeds the device attention limit (" +
-                       std::to_string((200 * 1024 / 4 - a.da - 1) / k) + " at beam " + std::to_string(k) + ")");
+                       std::to_string(smem_fixed < smem_lim ? (smem_lim - smem_fixed) / (sizeof(float) * k) : 0) +
+                       " at beam " + std::to_string(k) + ")");
   if (fused_ok) {
     const int B = R / k;
     switch (k) {  // exact beam width: no predicated-off rows in the inner loops

@@ -359,6 +359,10 @@ def main() -> None:
         # come from the encoder-time HX rows, so the step's GEMMs are
         # s [W_att_s | U_z | U_r] and s' W_o^s -- counted as executed
         shapes.update({"query": [(dh, da + 2 * dh)], "deep_out": [(dh, de)]})
+        if kcount.get("query", 0) * 2 < kcount.get("deep_out", 0):
+            # query folded forward: the deep-output launch also computes the
+            # next step's query + s' U_zr; the query class is one launch per bucket
+            shapes["deep_out"] = [(dh, de + da + 2 * dh)]
     pass_ms = insitu.device_ms
     sm_ms = {k: insitu.kernel_ms[k] for k in _lib.KERNEL_CLASSES}
     share = {k: round(v / (n_sm * pass_ms), 4) for k, v in sm_ms.items()}

@@ -359,6 +359,20 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
       m->us_qs = split_kmajor_dev(m, dWqs, dh, da + 2 * dh, dh, dh, 0, &m->Wqs_hi, &m->Wqs_lo);
       AMUN_CUDA(cudaDeviceSynchronize());
       AMUN_CUDA(cudaFree(dWqs));
+      {  // [W_o^s | 0 | W_att_s | U_z | U_r]: deep output + next query in one GEMM
+        const int nq = m->dep + da + 2 * dh;
+        std::vector<float> Wdq((size_t)dh * nq, 0.f);
+        for (int i = 0; i < dh; ++i) {
+          std::memcpy(&Wdq[(size_t)i * nq], t[T_W_OUT_S] + (size_t)i * de, de * sizeof(float));
+          std::memcpy(&Wdq[(size_t)i * nq + m->dep], &Wqs[(size_t)i * (da + 2 * dh)], (da + 2 * dh) * sizeof(float));
+        }
+        float *dWdq = nullptr;
+        AMUN_CUDA(cudaMalloc(&dWdq, Wdq.size() * sizeof(float)));
+        AMUN_CUDA(cudaMemcpy(dWdq, Wdq.data(), Wdq.size() * sizeof(float), cudaMemcpyHostToDevice));
+        m->us_dq = split_kmajor_dev(m, dWdq, dh, nq, dh, dh, 0, &m->Wdq_hi, &m->Wdq_lo);
+        AMUN_CUDA(cudaDeviceSynchronize());
+        AMUN_CUDA(cudaFree(dWdq));
+      }
     }
   }
   {  // deep output: rows [y ; c ; s'] = [W_out_y ; W_out_c ; W_out_s]

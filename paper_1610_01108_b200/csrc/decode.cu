@@ -407,6 +407,15 @@ void carve_dec(Carver &cv, DecBufs &d, const amun_model *m, int R, int jmax, boo
 // the logits drops from 12.1M to 4.7M MACs.  Env
 // AMUN_NO_PROJ_CTX=1 keeps the GRU-A step (A/B runs).
 int proj_ldhx(const amun_model *m) { return 3 * m->d.d_h + m->dep; }
+// the next step's query + s U_zr computed by the deep-output GEMM from s'
+// (one launch per step fewer; AMUN_NO_FOLD_QUERY=1 keeps a separate launch)
+bool fold_query() {
+  static const bool off = [] {
+    const char *e = getenv("AMUN_NO_FOLD_QUERY");
+    return e && e[0] == '1';
+  }();
+  return !off;
+}
 bool proj_ok(const amun_model *m) {
   static const bool off = [] {
     const char *e = getenv("AMUN_NO_PROJ_CTX");
@@ -770,6 +779,9 @@ struct TcStep {
   bool proj = false;  // projected-context maps below are valid
   SkMaps qs, os;      // s [W_att_s | U_zr]; s' W_o^s
   int sqs = 1, sos = 1;
+  bool dq_ok = false;  // s' [W_o^s | 0 | W_att_s | U_zr] (deep output + next query) is valid
+  SkMaps dq;
+  int sdq = 1;
 };
 
 // target CTAs per decoder-step GEMM launch (env AMUN_TC_CTAS overrides)
@@ -815,8 +827,15 @@ void tc_step_maps(const amun_model *m, const DecBufs &d, int Rmax, TcStep &ts) {
                          dh, m->us_o, -1, xp);
     ts.sqs = sk_fit_splits(ts.qs, t);
     ts.sos = sk_fit_splits(ts.os, t);
+    ts.dq_ok = m->Wdq_hi != nullptr && fold_query();
+    if (ts.dq_ok) {
+      ts.dq = make_sk_maps(d.Snh, d.Snl, dh, dh, nullptr, nullptr, 0, 0, Rmax, m->Wdq_hi, m->Wdq_lo,
+                           dep + da + 2 * dh, dh, m->us_dq);
+      ts.sdq = sk_fit_splits(ts.dq, t);
+    }
   }
 }
+
 
 // HX rows [row0, row0 + M) of a store whose split annotations are Hah/Hal
 // ([rows][2dh]): h [C_z | C_r | C_h] (the c rows of the gate weights) and
@@ -850,16 +869,30 @@ void gemm_tc(Ctx &c, const SkMaps &maps, int M, int splits, const Epi &epi) {
   c.run(c.cls, [&] { launch_gemm_sk(maps, M, splits, epi, c.st, dbg); });
 }
 
+// Projected-context step, query folded forward: Q, e^{2q} and s U_zr of the
+// rows' current states (a bucket's first step, the parity hook); later steps
+// get them from the previous step's deep-output GEMM (EpiDQ).
+void qs_prologue(Ctx &c, const amun_model *m, const DecBufs &d, const TcStep &ts, int R) {
+  const int cls = c.cls;
+  c.cls = AMUN_K_QUERY;
+  gemm_tc(c, ts.qs, R, ts.sqs, EpiQS{d.Q, d.EQ, d.SU, m->d.d_att, 2 * m->d.d_h});
+  c.cls = cls;
+}
+
 void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, const int *d_len, int jmax,
                int R, int rows_per_sent, const int *n_act, const int *done, float *alpha, const LogitOut &lo,
-               const TcStep *ts = nullptr, bool do_logits = true, const int *tok = nullptr) {
+               const TcStep *ts = nullptr, bool do_logits = true, const int *tok = nullptr,
+               const int *qrow = nullptr) {
   const int de = m->d.d_emb, dh = m->d.d_h, da = m->d.d_att, V = m->d.v_trg, xs = m->xs_w;
   const int s_off = de + 2 * dh;
   const bool proj = ts && ts->proj && e.HX;
+  // folded query: Q / EQ / s U_zr of each row's parent come from the previous
+  // step's deep-output GEMM (or qs_prologue), indexed through qrow
+  const bool fold = proj && qrow && ts->dq_ok && lo.tc;
   if (proj) {  // projected-context step (proj_ok): query + s U_zr, attention with the gate math
     if (!tok) throw Error(AMUN_ERR_CUDA, "step_rows: previous tokens required with the y tables");
     c.cls = AMUN_K_QUERY;
-    gemm_tc(c, ts->qs, R, ts->sqs, EpiQS{d.Q, d.EQ, d.SU, da, 2 * dh});
+    if (!fold) gemm_tc(c, ts->qs, R, ts->sqs, EpiQS{d.Q, d.EQ, d.SU, da, 2 * dh});
     AttnArgs aa{d.Q, da, e.P, e.HX, m->v_att, d_len, jmax, da, proj_ldhx(m), rows_per_sent, n_act, done,
                 nullptr, 0, alpha};
     aa.energy = d.En;
@@ -879,6 +912,7 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
     aa.dh = dh;
     aa.de = de;
     aa.ldco = m->dep;
+    if (fold) aa.qrow = qrow;
     int na_launch = 1;
     c.run(AMUN_K_ATTN, [&] { na_launch = launch_attention(aa, R, c.st); });
     c.launches += na_launch - 1;
@@ -944,7 +978,10 @@ void step_rows(Ctx &c, const amun_model *m, const DecBufs &d, const EncBufs &e, 
       e.lo = d.T_lo;
       e.ldh = m->dep;
     }
-    if (proj) {  // s' W_o^s + (context + y term from the attention kernel)
+    if (fold) {  // s' [W_o^s | 0 | W_att_s | U_zr]: deep output + the next step's query
+      EpiDQ eq{d.CO, m->dep, m->b_out, d.T_hi, d.T_lo, m->dep, de, m->dep, EpiQS{d.Q, d.EQ, d.SU, da, 2 * dh}};
+      gemm_tc(c, ts->dq, R, ts->sdq, eq);
+    } else if (proj) {  // s' W_o^s + (context + y term from the attention kernel)
       e.rowadd = d.CO;
       e.ldadd = m->dep;
       gemm_tc(c, ts->os, R, ts->sos, e);
@@ -1330,6 +1367,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       bs.n_act = cv.take<int>(Bmax);
       bs.score = cv.take<double>(Rmax);
       bs.tok = cv.take<int>(Rmax);
+      bs.qrow = cv.take<int>(Rmax);
       bs.done = cv.take<int>(Bmax);
       bs.steps = cv.take<int>(Bmax);
       bs.cap = L.d_cap;
@@ -1456,7 +1494,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     Ctx &c = *L.c;
     for (int m = 0; m < n_models; ++m)
       step_rows(c, ms[m], L.db[m], L.eb[m], L.d_len, L.jmax, L.R, k, L.bs.n_act, L.bs.done, nullptr, L.lo,
-                use_tcg ? &L.tsteps[m] : nullptr, !ens_fused, L.bs.tok);
+                use_tcg ? &L.tsteps[m] : nullptr, !ens_fused, L.bs.tok, L.bs.qrow);
     if (ens_fused) {  // every member's logits in one launch (search.py:56-72)
       LogitTcArgs ta{L.R, V, ms[0]->d.d_emb, ms[0]->b_logit, kk, ntiles, ms[0]->us_l,
                      L.pmax, L.psum, L.cval, L.ctok};
@@ -1616,6 +1654,11 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       L.lo.bias = L.bg;
       L.lo.ntiles = ceil_div(n_gath, tile_n);
     }
+    // folded query (step_rows): the bucket's first Q / EQ / s U_zr from the
+    // initial rows; every later step's come from the deep-output GEMM
+    for (int m = 0; m < n_models; ++m)
+      if (use_tcg && L.tsteps[m].proj && L.tsteps[m].dq_ok && L.eb[m].HX && L.lo.tc)
+        qs_prologue(c, ms[m], L.db[m], L.tsteps[m], L.R);
     SelectArgs &sa = L.sa;
     sa = SelectArgs{};
     sa.kk = kk;
@@ -2176,7 +2219,7 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
   const int R = B * k, ntiles = ceil_div(V, kBN);
   EncBufs e{};
   DecBufs d{};
-  int *d_len, *d_y, *ctok;
+  int *d_len, *d_y, *ctok, *d_qrow;
   float *d_s, *d_alpha, *pmax, *psum, *cval;
   DevMem mem;
   for (int pass = 0; pass < 2; ++pass) {
@@ -2184,6 +2227,7 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
     cv.base = pass ? static_cast<char *>(mem.p) : nullptr;
     e.Hann = cv.take<float>((size_t)B * jmax * 2 * dh);
     e.P = cv.take<float>((size_t)B * jmax * da);
+    d_qrow = cv.take<int>(R);
     if (proj_ok(m)) {  // the product's projected annotations, from the given h
       e.HX = cv.take<float>((size_t)B * jmax * proj_ldhx(m));
       e.Hah = cv.take<__half>((size_t)B * jmax * 2 * dh);
@@ -2206,6 +2250,11 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
   h2d(c, d_len, lens, B);
   h2d(c, d_s, s, (size_t)R * dh);
   h2d(c, d_y, y_prev, R);
+  {
+    std::vector<int> ident(R);
+    std::iota(ident.begin(), ident.end(), 0);
+    h2d(c, d_qrow, ident.data(), R);
+  }
   if (e.HX) {
     const long long n = (long long)B * jmax * 2 * dh;
     split_rows_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.st>>>(e.Hann, n, e.Hah, e.Hal);
@@ -2232,7 +2281,11 @@ void hook_step_tc(amun_model *m, int B, int k, const float *s, const int32_t *y_
   LogitOut lo{true, kk, nt_dev, pmax, psum, cval, ctok};
   lo.tc = &lm;
   lo.rows = rows;
-  step_rows(c, m, d, e, d_len, jmax, R, k, nullptr, nullptr, d_alpha, lo, &ts, true, d_y);
+  // exactly a bucket's first step in amun_decode: the folded query's
+  // prologue, then the step (whose deep-output GEMM also computes the next
+  // query, unused here)
+  if (ts.proj && ts.dq_ok && e.HX) qs_prologue(c, m, d, ts, R);
+  step_rows(c, m, d, e, d_len, jmax, R, k, nullptr, nullptr, d_alpha, lo, &ts, true, d_y, d_qrow);
   std::vector<float> hpm((size_t)R * nt_dev), hps((size_t)R * nt_dev), hcv((size_t)R * nt_dev * kk);
   std::vector<int> hct((size_t)R * nt_dev * kk);
   if (s_out) d2h(c, s_out, d.Sn, (size_t)R * dh);

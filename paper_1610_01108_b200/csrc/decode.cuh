@@ -32,6 +32,11 @@ struct amun_model {
   // state's gate products in one GEMM (projected-context step, decode.cu)
   __half *Wqs_hi = nullptr, *Wqs_lo = nullptr;
   float us_qs = 1.f;
+  // [W_o^s | 0 | W_att_s | U_z | U_r]^T [dep + da + 2dh, dh]: the deep output
+  // and the NEXT step's query + gate products of s' in one GEMM (columns
+  // [0, d_e) deep output, [dep, ...) the Wqs block)
+  __half *Wdq_hi = nullptr, *Wdq_lo = nullptr;
+  float us_dq = 1.f;
   __half *Wg_hi = nullptr, *Wg_lo = nullptr;    // Wg^T      [3dh, xsp]
   __half *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
   __half *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, xsp]

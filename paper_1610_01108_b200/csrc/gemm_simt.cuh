@@ -340,6 +340,51 @@ struct EpiQS {
   }
 };
 
+// Projected-context step with the query folded forward: s' [W_o^s | 0 |
+// W_att_s | U_z | U_r].  Columns [0, de): the deep output t = tanh(acc + CO
+// row + b_out) (3xFP16 split for the logits); [q0, ...): the NEXT step's
+// query, e^{2q} and s' U_{z,r} for this row (the next step's rows read them
+// through the select's parent index).
+struct EpiDQ {
+  static constexpr bool kTile = false;
+  const float *CO;  // [M, ldco] context + y term of the deep output (attention epilogue)
+  int ldco;
+  const float *bias;  // b_out [de]
+  __half *hi, *lo;    // t split [M, ldh]
+  int ldh, de, q0;
+  EpiQS qs;
+  __device__ void operator()(int m, int n, float v, int z) const {
+    if (n < de) {
+      v = tanhf(v + CO[(long long)m * ldco + n] + bias[n]);
+      store_split(hi, lo, (long long)m * ldh + n, v);
+    } else if (n >= q0) {
+      qs(m, n - q0, v, z);
+    }
+  }
+  struct Pre {
+    float4 b, r;
+  };
+  __device__ __forceinline__ Pre load4(int m, int n) const {
+    Pre p;
+    if (n < de) {
+      p.r = *reinterpret_cast<const float4 *>(CO + (long long)m * ldco + n);
+      p.b = *reinterpret_cast<const float4 *>(bias + n);
+    }
+    return p;
+  }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &p) const {
+    if (n < de) {
+      v.x = tanhf(v.x + p.r.x + p.b.x);
+      v.y = tanhf(v.y + p.r.y + p.b.y);
+      v.z = tanhf(v.z + p.r.z + p.b.z);
+      v.w = tanhf(v.w + p.r.w + p.b.w);
+      store_split4(hi, lo, (long long)m * ldh + n, v);
+    } else if (n >= q0) {
+      qs.store4(m, n - q0, v, EpiQS::Pre{});
+    }
+  }
+};
+
 // Decoder GRU phase A (nnet.py:66-69): columns [0,dh) -> z, [dh,2dh) -> r
 // (stored as r*h), [2dh,3dh) -> x W_h + b_h (the input half of h~).
 struct EpiGruA {

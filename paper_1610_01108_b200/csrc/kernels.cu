@@ -396,11 +396,13 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   }
   for (int i = tid; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
   const bool fast_shape = na == KA && a.da == 1024;
+  // row whose query (Q, EQ) and s U_zr this row uses
+  auto qr_of = [&](int r) -> long long { return a.qrow ? a.qrow[b * k + r] : (long long)b * k + r; };
   if (fast_shape)
     for (int i = tid; i < KA * 1024; i += blockDim.x)
-      eqs[i] = __ldg(a.EQ + (long long)(b * k + i / 1024) * a.ldq + (i % 1024));
+      eqs[i] = __ldg(a.EQ + qr_of(i / 1024) * a.ldq + (i % 1024));
   for (int r = warp; r < na; r += nw) {
-    const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
+    const float *qr = a.Q + qr_of(r) * a.ldq;
     float m = 0.f;
     for (int c = lane; c < a.da; c += 32) m = fmaxf(m, fabsf(__ldg(qr + c)));
     m = warp_max(m);
@@ -457,8 +459,8 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
       const bool pbig = warp_max(pm) > kFactorSafe;
       for (int r = 0; r < na; ++r) {
         float s0 = 0.f;
-        const float *qr = a.Q + (long long)(b * k + r) * a.ldq;
-        const float *er = a.EQ + (long long)(b * k + r) * a.ldq;
+        const float *qr = a.Q + qr_of(r) * a.ldq;
+        const float *er = a.EQ + qr_of(r) * a.ldq;
         const bool direct = pbig || qbig[r];
         for (int u = 0; u < 32; ++u) {
           const int i = lane + 32 * u;
@@ -560,7 +562,7 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
             const float4 bb = *reinterpret_cast<const float4 *>(a.bg + n);
             float4 v;
             if (n < 2 * dh) {
-              const float4 su = *reinterpret_cast<const float4 *>(a.su + gr * 2 * dh + n);
+              const float4 su = *reinterpret_cast<const float4 *>(a.su + qr_of(r) * 2 * dh + n);
               v = make_float4(cx.x + su.x, cx.y + su.y, cx.z + su.z, cx.w + su.w);
             } else {
               v = cx;
@@ -786,6 +788,7 @@ __global__ void init_beam_kernel(BeamState bs, ModelRows mr, const float *const 
     for (int i = 0; i < k; ++i) {
       bs.score[b * k + i] = 0.0;
       bs.tok[b * k + i] = 0;
+      if (bs.qrow) bs.qrow[b * k + i] = b * k + i;
     }
     if (b == 0) *bs.n_done = 0;
   }
@@ -1199,6 +1202,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       for (int i = 0; i < newna; ++i) {
         bs.score[b * k + i] = ch_v[i];
         bs.tok[b * k + i] = ch_tok[i];
+        if (bs.qrow) bs.qrow[b * k + i] = b * k + ch_par[i];
       }
       if (bs.fin_n[b] > 0 && best_new <= bs.best_fin[b]) done = 1;  // search.py:195-198
     }

@@ -38,6 +38,8 @@ struct AttnArgs {
   // (nnet.py:66-69): z -> Z, r * s -> RH split, the input half of h~ -> XH,
   // and the deep output's context + y term -> CO.
   const float *su = nullptr;   // [R][2dh] s U_{z,r} (EpiQS)
+  const int *qrow = nullptr;   // optional [R]: row of Q / EQ / su to use (the parent's, when the
+                               // previous step's deep-output GEMM computed them from s')
   const float *S = nullptr;    // state rows (pitch lds)
   int lds = 0;
   const int *tok = nullptr;    // [R] previous token
@@ -72,6 +74,7 @@ struct BeamState {
   double *best_fin;  // [B]
   int *bp_tok, *bp_par;  // [B][cap_max][k]
   int *n_done;       // [1] sentences finished so far
+  int *qrow = nullptr;  // [B*k] optional: row of the previous step each row continues (its parent)
 };
 
 constexpr int kMaxModels = 8;  // ensemble members on the device path

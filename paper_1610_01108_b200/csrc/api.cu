@@ -319,6 +319,24 @@ extern "C" int amun_model_create(int32_t device, const amun_dims *dims, const fl
   m->W_att_h = cp(T_W_ATT_H, (size_t)2 * dh * da);
   if (m->tc_ok)
     m->us_p = split_kmajor_dev(m, m->W_att_h, 2 * dh, da, 2 * dh, 2 * dh, 0, &m->Watth_hi, &m->Watth_lo);
+  if (m->tc_ok) {  // [W_att_h | C_z | C_r | C_h | W_o^c | 0]: precomp_att + HX in one GEMM
+    const int nph = da + 3 * dh + m->dep, din = de + 2 * dh;
+    std::vector<float> Wph((size_t)2 * dh * nph, 0.f);
+    for (int i = 0; i < 2 * dh; ++i) {
+      float *row = &Wph[(size_t)i * nph];
+      std::memcpy(row, t[T_W_ATT_H] + (size_t)i * da, da * sizeof(float));
+      for (int g = 0; g < 3; ++g)  // the context rows (de + i) of the decoder's input weights
+        std::memcpy(row + da + g * dh, t[T_DEC + G_WZ + g] + (size_t)(de + i) * dh, dh * sizeof(float));
+      std::memcpy(row + da + 3 * dh, t[T_W_OUT_C] + (size_t)i * de, de * sizeof(float));
+    }
+    (void)din;
+    float *dWph = nullptr;
+    AMUN_CUDA(cudaMalloc(&dWph, Wph.size() * sizeof(float)));
+    AMUN_CUDA(cudaMemcpy(dWph, Wph.data(), Wph.size() * sizeof(float), cudaMemcpyHostToDevice));
+    m->us_ph = split_kmajor_dev(m, dWph, 2 * dh, nph, 2 * dh, 2 * dh, 0, &m->Wph_hi, &m->Wph_lo);
+    AMUN_CUDA(cudaDeviceSynchronize());
+    AMUN_CUDA(cudaFree(dWph));
+  }
   m->W_init = cp(T_W_INIT, (size_t)2 * dh * dh);
   m->b_init = cp(T_B_INIT, dh);
   m->W_att_s = cp(T_W_ATT_S, (size_t)dh * da);

@@ -701,15 +701,24 @@ class AheadEncoder {
     if (jmax < 1 || jmax > T_ || !evf_[jmax - 1]) throw Error(AMUN_ERR_CUDA, "encode-ahead: bucket not tracked");
     AMUN_CUDA(cudaStreamWaitEvent(c.st, evf_[jmax - 1], 0));
     if (evb_[jmax - 1]) AMUN_CUDA(cudaStreamWaitEvent(c.st, evb_[jmax - 1], 0));
-    const SkMaps pm = make_sk_maps(out_.Hah, out_.Hal, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0,
-                                   (int)in_.store_rows, m->Watth_hi, m->Watth_lo, da, 2 * dh, m->us_p);
     const int M = (int)nrows;
-    const auto gp = ahead_grid(pm, M, std::max(32, prep_ctas_));
-    EpiStore ep{out_.P + row0 * da, da, nullptr, 0, 0};
     const int cls = c.cls;
     c.cls = AMUN_K_ENCODER;
-    c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(pm, M, gp.first, ep, c.st, 0, (int)row0, gp.second); });
-    if (out_.HX) compute_hx(c, m, out_.Hah, out_.Hal, in_.store_rows, row0, M, out_.HX, std::max(32, prep_ctas_));
+    if (out_.HX && m->Wph_hi) {  // P and HX in one GEMM (one read of the annotations)
+      const int ld = proj_ldhx(m);
+      const SkMaps pm = make_sk_maps(out_.Hah, out_.Hal, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0,
+                                     (int)in_.store_rows, m->Wph_hi, m->Wph_lo, da + ld, 2 * dh, m->us_ph);
+      const auto gp = ahead_grid(pm, M, std::max(32, prep_ctas_));
+      EpiPH ep{out_.P + row0 * da, out_.HX + row0 * ld, da, ld, 3 * dh + m->d.d_emb};
+      c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(pm, M, gp.first, ep, c.st, 0, (int)row0, gp.second); });
+    } else {
+      const SkMaps pm = make_sk_maps(out_.Hah, out_.Hal, 2 * dh, 2 * dh, nullptr, nullptr, 0, 0,
+                                     (int)in_.store_rows, m->Watth_hi, m->Watth_lo, da, 2 * dh, m->us_p);
+      const auto gp = ahead_grid(pm, M, std::max(32, prep_ctas_));
+      EpiStore ep{out_.P + row0 * da, da, nullptr, 0, 0};
+      c.run(AMUN_K_ENCODER, [&] { launch_gemm_sk(pm, M, gp.first, ep, c.st, 0, (int)row0, gp.second); });
+      if (out_.HX) compute_hx(c, m, out_.Hah, out_.Hal, in_.store_rows, row0, M, out_.HX, std::max(32, prep_ctas_));
+    }
     c.run(AMUN_K_ENCODER, [&] {
       enc_mean_kernel<<<cnt, 256, 0, c.st>>>(Hsum_, d_len_, d_e_of_i_, i0, 2 * dh, Hmean_);
       AMUN_CHECK_LAUNCH();

@@ -37,6 +37,10 @@ struct amun_model {
   // [0, d_e) deep output, [dep, ...) the Wqs block)
   __half *Wdq_hi = nullptr, *Wdq_lo = nullptr;
   float us_dq = 1.f;
+  // [W_att_h | C_z | C_r | C_h | W_o^c | 0]^T [da + 3dh + dep, 2dh]: precomp_att
+  // and the projected annotations HX of a bucket in one GEMM over the split annotations
+  __half *Wph_hi = nullptr, *Wph_lo = nullptr;
+  float us_ph = 1.f;
   __half *Wg_hi = nullptr, *Wg_lo = nullptr;    // Wg^T      [3dh, xsp]
   __half *Uhd_hi = nullptr, *Uhd_lo = nullptr;  // U_h^T     [dh, dh]
   __half *Wo_hi = nullptr, *Wo_lo = nullptr;    // Wout^T    [de, xsp]

@@ -385,6 +385,29 @@ struct EpiDQ {
   }
 };
 
+// A bucket's annotation products in one GEMM over h (split): columns
+// [0, da) precomp_att P = h W_att_h (nnet.py:126), then the projected
+// annotations HX = h [C_z | C_r | C_h | W_o^c] (row pitch ldx, nx columns used).
+struct EpiPH {
+  static constexpr bool kTile = false;
+  float *P, *HX;
+  int da, ldx, nx;
+  __device__ void operator()(int m, int n, float v, int) const {
+    if (n < da)
+      P[(long long)m * da + n] = v;
+    else if (n - da < nx)
+      HX[(long long)m * ldx + n - da] = v;
+  }
+  struct Pre {};
+  __device__ __forceinline__ Pre load4(int, int) const { return Pre{}; }
+  __device__ __forceinline__ void store4(int m, int n, float4 v, const Pre &) const {
+    if (n < da)
+      *reinterpret_cast<float4 *>(P + (long long)m * da + n) = v;
+    else if (n - da < nx)
+      *reinterpret_cast<float4 *>(HX + (long long)m * ldx + n - da) = v;
+  }
+};
+
 // Decoder GRU phase A (nnet.py:66-69): columns [0,dh) -> z, [dh,2dh) -> r
 // (stored as r*h), [2dh,3dh) -> x W_h + b_h (the input half of h~).
 struct EpiGruA {

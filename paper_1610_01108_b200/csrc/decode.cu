@@ -636,7 +636,7 @@ class AheadEncoder {
     // store: padded positions must read as zero (attention masks them, the
     // precomp GEMM reads them); P and S0 are fully written by prepare()
     const size_t ann = (size_t)in_.store_rows * 2 * dh;
-    AMUN_CUDA(cudaMemsetAsync(out_.Hann, 0, ann * sizeof(float), cf.st));
+    if (out_.Hann) AMUN_CUDA(cudaMemsetAsync(out_.Hann, 0, ann * sizeof(float), cf.st));
     AMUN_CUDA(cudaMemsetAsync(out_.Hah, 0, ann * sizeof(__half), cf.st));
     AMUN_CUDA(cudaMemsetAsync(out_.Hal, 0, ann * sizeof(__half), cf.st));
     if (Ctx::ablated() & (1u << AMUN_K_ENCODER)) {  // encoder ablated: finite inputs for the decoder
@@ -1621,7 +1621,7 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       for (int m = 0; m < n_models; ++m) {
         gencs[ci][m]->prepare(c, bk.first - chunk_first, B, bucket_row[bi], (long long)B * jmax, jmax);
         const int dh_m = ms[m]->d.d_h, da_m = ms[m]->d.d_att;
-        L.eb[m].Hann = stores[m].Hann + bucket_row[bi] * 2 * dh_m;
+        L.eb[m].Hann = stores[m].Hann ? stores[m].Hann + bucket_row[bi] * 2 * dh_m : nullptr;
         L.eb[m].P = stores[m].P + bucket_row[bi] * da_m;
         L.eb[m].HX = stores[m].HX ? stores[m].HX + bucket_row[bi] * proj_ldhx(ms[m]) : nullptr;
         s0p[m] = stores[m].S0 + (long long)(bk.first - chunk_first) * dh_m;
@@ -1953,7 +1953,8 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
       for (int pass = 0; pass < 2; ++pass) {
         cv = Carver{};
         cv.base = static_cast<char *>(S.mem);
-        S.Hann = cv.take<float>((size_t)rows * 2 * dh_m);
+        const bool proj_m = use_tcg && proj_ok(ms[m]);  // the step reads HX, never fp32 H
+        S.Hann = proj_m ? nullptr : cv.take<float>((size_t)rows * 2 * dh_m);
         S.P = cv.take<float>((size_t)rows * da_m);
         S.S0 = cv.take<float>((size_t)nc * dh_m);
         S.Hah = cv.take<__half>((size_t)rows * 2 * dh_m);

@@ -762,7 +762,7 @@ struct EpiEncFB {
   float *H;           // [n][dh]
   const float *Z;
   __half *Hh, *Hl;    // [n][dh] next phase-A operand
-  float *Hann;        // store [rows][2dh]
+  float *Hann;        // store [rows][2dh] fp32 (nullptr: only the split copy is kept)
   __half *Hah, *Hal;
   float *Hsum;        // [n][2dh]
   const int *len;            // [n]
@@ -797,7 +797,7 @@ struct EpiEncFB {
     store_split4(Hh, Hl, o, h);
     const int pos = dir ? p.L - 1 - t : t;
     const long long ao = (p.ar + pos) * 2 * dh + dir * dh + n;
-    *reinterpret_cast<float4 *>(Hann + ao) = h;
+    if (Hann) *reinterpret_cast<float4 *>(Hann + ao) = h;
     store_split4(Hah, Hal, ao, h);
     *reinterpret_cast<float4 *>(Hsum + (long long)m * 2 * dh + dir * dh + n) =
         make_float4(p.sum.x + h.x, p.sum.y + h.y, p.sum.z + h.z, p.sum.w + h.w);

@@ -150,6 +150,9 @@ constexpr int kEnergyWarps = 8;  // warps per energy CTA
 constexpr int kEnergyPos = 8;    // source positions per energy CTA (one per warp)
 constexpr float kTwoLog2e = 2.8853900817779268f;  // 2 / ln 2: e^{2x} = 2^{x kTwoLog2e}
 constexpr float kFactorSafe = 20.f;  // |p|, |q| below this: e^{2p} e^{2q} cannot overflow
+// per-sentence kernel, paired reciprocals: (1 + e^{2p} e^{2q}) <= e^44, so the
+// product of two such terms stays below the fp32 maximum (e^88.7)
+constexpr float kPairSafe = 11.f;
 
 // tanh(p + q) = 1 - 2 / (1 + e^{2p} e^{2q}): e^{2p} is computed once per
 // (position, element) and shared by the beam rows, e^{2q} once per (row,
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
     float m = 0.f;
     for (int c = lane; c < a.da; c += 32) m = fmaxf(m, fabsf(__ldg(qr + c)));
     m = warp_max(m);
-    if (lane == 0) qbig[r] = m > kFactorSafe;
+    if (lane == 0) qbig[r] = m > kPairSafe;
   }
   __syncthreads();
   int anybig = 0;
@@ -436,12 +439,22 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
         for (int u = 0; u < 8; ++u) {
           const int i = lane + 32 * (u0 + u);
           const float vi = vs[i];
+          // two rows per SFU reciprocal: 1/a = b / (ab), 1/b = a / (ab)
+          // (|p|, |q| <= kPairSafe keeps ab finite); the SFU, not the FMA
+          // pipe, bounds this loop
 #pragma unroll
-          for (int r = 0; r < KA; ++r)
-            acc[r] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], eqs[r * 1024 + i], 1.0f)), 1.0f), acc[r]);
+          for (int r = 0; r + 1 < KA; r += 2) {
+            const float a0 = fmaf(ep[u], eqs[r * 1024 + i], 1.0f), a1 = fmaf(ep[u], eqs[(r + 1) * 1024 + i], 1.0f);
+            const float inv = tc_rcp(a0 * a1);
+            acc[r] = fmaf(vi, fmaf(-2.0f, a1 * inv, 1.0f), acc[r]);
+            acc[r + 1] = fmaf(vi, fmaf(-2.0f, a0 * inv, 1.0f), acc[r + 1]);
+          }
+          if constexpr (KA % 2 == 1)
+            acc[KA - 1] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], eqs[(KA - 1) * 1024 + i], 1.0f)), 1.0f),
+                               acc[KA - 1]);
         }
       }
-      if (!(warp_max(pm) > kFactorSafe)) {
+      if (!(warp_max(pm) > kPairSafe)) {
 #pragma unroll
         for (int r = 0; r < KA; ++r) {
           const float sum = warp_sum(acc[r]);

@@ -372,8 +372,11 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
   float *vs = sm;                                    // [da]
   float *al = vs + a.da;                             // [k][jmax]
-  int *qbig = reinterpret_cast<int *>(al + (size_t)k * a.jmax);  // [k]
-  float *eqs = reinterpret_cast<float *>(qbig + ((k + 3) & ~3));  // [KA][1024] e^{2q} rows (fast path)
+  const int k4 = (k + 3) & ~3;
+  int *qrs = reinterpret_cast<int *>(al + (size_t)k * a.jmax);  // [k] row whose query (Q, EQ) and s U_zr row r uses
+  int *toks = qrs + k4;                                          // [k] row r's previous token (PROJ epilogue)
+  unsigned *wmask = reinterpret_cast<unsigned *>(toks + k4);     // [32] per-warp masks of rows with |q| > kPairSafe
+  float *eqs = reinterpret_cast<float *>(wmask + 32);            // [KA][1024] e^{2q} rows (fast path)
   // H of the sentence streamed into shared memory in chunks of kHP
   // positions by bulk copies, two buffers, issued now and consumed by the
   // context phase: the annotation reads overlap the energies instead of
@@ -399,21 +402,28 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   }
   for (int i = tid; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
   const bool fast_shape = na == KA && a.da == 1024;
-  // row whose query (Q, EQ) and s U_zr this row uses
-  auto qr_of = [&](int r) -> long long { return a.qrow ? a.qrow[b * k + r] : (long long)b * k + r; };
-  if (fast_shape)
-    for (int i = tid; i < KA * 1024; i += blockDim.x)
-      eqs[i] = __ldg(a.EQ + qr_of(i / 1024) * a.ldq + (i % 1024));
-  for (int r = warp; r < na; r += nw) {
-    const float *qr = a.Q + qr_of(r) * a.ldq;
-    float m = 0.f;
-    for (int c = lane; c < a.da; c += 32) m = fmaxf(m, fabsf(__ldg(qr + c)));
-    m = warp_max(m);
-    if (lane == 0) qbig[r] = m > kPairSafe;
-  }
+  // per-row indices staged once: the query row (the select's parent row in
+  // the query-folded step) and the previous token
+  if (tid < k) qrs[tid] = a.qrow ? a.qrow[b * k + tid] : b * k + tid;
+  else if (PROJ && tid - k < k) toks[tid - k] = a.tok[b * k + tid - k];
   __syncthreads();
-  int anybig = 0;
-  for (int r = 0; r < na; ++r) anybig |= qbig[r];
+  // e^{2q} rows into shared memory and the |q| check of every row in one
+  // pass of independent loads (column-parallel over the CTA)
+  unsigned qm = 0;
+  for (int i = tid; i < a.da; i += blockDim.x) {
+#pragma unroll 4
+    for (int r = 0; r < na; ++r) {
+      const long long qo = (long long)qrs[r] * a.ldq + i;
+      if (fabsf(__ldg(a.Q + qo)) > kPairSafe) qm |= 1u << r;
+      if (fast_shape) eqs[r * 1024 + i] = __ldg(a.EQ + qo);
+    }
+  }
+  qm = __reduce_or_sync(0xffffffffu, qm);
+  if (lane == 0) wmask[warp] = qm;
+  __syncthreads();
+  unsigned qbigm = 0;
+  for (int w = 0; w < nw; ++w) qbigm |= wmask[w];
+  const int anybig = qbigm != 0;
   // ---- energies: warp per source position (nnet.py:135-136)
   for (int j = warp; j < J; j += nw) {
     const float *pj = a.P + ((long long)b * a.jmax + j) * a.da;
@@ -472,9 +482,9 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
       const bool pbig = warp_max(pm) > kFactorSafe;
       for (int r = 0; r < na; ++r) {
         float s0 = 0.f;
-        const float *qr = a.Q + qr_of(r) * a.ldq;
-        const float *er = a.EQ + qr_of(r) * a.ldq;
-        const bool direct = pbig || qbig[r];
+        const float *qr = a.Q + (long long)qrs[r] * a.ldq;
+        const float *er = a.EQ + (long long)qrs[r] * a.ldq;
+        const bool direct = pbig || ((qbigm >> r) & 1u);
         for (int u = 0; u < 32; ++u) {
           const int i = lane + 32 * u;
           if (i < a.da)
@@ -564,28 +574,33 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
       for (int i = 0; i < kQ; ++i) {
       const int n = 4 * cq[i], dh = a.dh;
       if (live[i] && n < 3 * dh + a.de) {
+        // operands of row r + 1 are loaded (read-only path) while row r is
+        // finished and stored: one load latency for the epilogue instead of
+        // one per row (the stores would otherwise order the next loads)
+        const int reg = n < dh ? 0 : n < 2 * dh ? 1 : n < 3 * dh ? 2 : 3;  // Z | r*s | h~ input | deep output
+        const float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 bb = reg < 3 ? __ldg(reinterpret_cast<const float4 *>(a.bg + n)) : f0;
+        auto load = [&](int r, float4 &y, float4 &su, float4 &sv) {
+          const long long t = toks[r];
+          y = reg < 3 ? __ldg(reinterpret_cast<const float4 *>(a.ywg + t * 3 * dh + n))
+                      : __ldg(reinterpret_cast<const float4 *>(a.ywo + t * a.de + n - 3 * dh));
+          su = reg < 2 ? __ldg(reinterpret_cast<const float4 *>(a.su + (long long)qrs[r] * 2 * dh + n)) : f0;
+          sv = reg == 1 ? __ldg(reinterpret_cast<const float4 *>(a.S + ((long long)b * k + r) * a.lds + n - dh)) : f0;
+        };
 #pragma unroll
         for (int r = 0; r < KA; ++r) {
           if (r >= na) break;
+          float4 y, su, sv;
+          load(r, y, su, sv);
           const long long gr = (long long)b * k + r;
-          const long long t = a.tok[gr];
           const float4 cx = acc[i][r];
-          if (n < 3 * dh) {
-            const float4 y = *reinterpret_cast<const float4 *>(a.ywg + t * 3 * dh + n);
-            const float4 bb = *reinterpret_cast<const float4 *>(a.bg + n);
-            float4 v;
-            if (n < 2 * dh) {
-              const float4 su = *reinterpret_cast<const float4 *>(a.su + qr_of(r) * 2 * dh + n);
-              v = make_float4(cx.x + su.x, cx.y + su.y, cx.z + su.z, cx.w + su.w);
-            } else {
-              v = cx;
-            }
+          if (reg < 3) {
+            float4 v = reg < 2 ? make_float4(cx.x + su.x, cx.y + su.y, cx.z + su.z, cx.w + su.w) : cx;
             v = make_float4(v.x + y.x + bb.x, v.y + y.y + bb.y, v.z + y.z + bb.z, v.w + y.w + bb.w);
-            if (n < dh) {
+            if (reg == 0) {
               *reinterpret_cast<float4 *>(a.Z + gr * dh + n) =
                   make_float4(sigmoid_acc(v.x), sigmoid_acc(v.y), sigmoid_acc(v.z), sigmoid_acc(v.w));
-            } else if (n < 2 * dh) {
-              const float4 sv = *reinterpret_cast<const float4 *>(a.S + gr * a.lds + n - dh);
+            } else if (reg == 1) {
               const long long o = gr * dh + n - dh;
               store_split(a.RHh, a.RHl, o + 0, sigmoid_acc(v.x) * sv.x);
               store_split(a.RHh, a.RHl, o + 1, sigmoid_acc(v.y) * sv.y);
@@ -595,7 +610,6 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
               *reinterpret_cast<float4 *>(a.XH + gr * dh + n - 2 * dh) = v;
             }
           } else {
-            const float4 y = *reinterpret_cast<const float4 *>(a.ywo + t * a.de + n - 3 * dh);
             *reinterpret_cast<float4 *>(a.CO + gr * a.ldco + n - 3 * dh) =
                 make_float4(cx.x + y.x, cx.y + y.y, cx.z + y.z, cx.w + y.w);
           }
@@ -697,7 +711,7 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
     const char *e = getenv("AMUN_ATTN_FUSED");  // 0: two-phase kernels
     return !(e && e[0] == '0');
   }();
-  const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)((k + 3) & ~3) +
+  const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)(2 * ((k + 3) & ~3) + 32) +
                         (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0) +
                         (a.su ? 128 + sizeof(float) * 5 * 2 * (size_t)a.dh2 + 5 * sizeof(uint64_t)
                               : a.dh2 == 4 * 512 ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);
@@ -989,6 +1003,17 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
       // log-prob mean_m(logit_m - lse_m) (search.py:67-72) is
       // (sum_m logit_m - sum_m lse_m) / nm
       constexpr int kPT = 8;
+      const int n = sa.ntiles * kk;
+      const float *cv = sa.cval + (long long)r * n;
+      const int *ct = sa.ctok + (long long)r * n;
+      // tile maxima (each tile list is sorted best-first) are loaded with the
+      // first member's partials: independent loads, one round trip
+      float tmax[kPT];
+#pragma unroll
+      for (int u = 0; u < kPT; ++u) {
+        const int tt = lane + 32 * u;
+        tmax[u] = tt < sa.ntiles ? __ldg(cv + tt * kk) : -INFINITY;
+      }
       double lse = 0.0;
       for (int mi = 0; mi < sa.nm_fused; ++mi) {
         const float *pmax = sa.pmax + mi * sa.pm_stride, *psum = sa.psum + mi * sa.pm_stride;
@@ -998,8 +1023,8 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         for (int u = 0; u < kPT; ++u) {
           const int tt = lane + 32 * u;
           const bool ok = tt < sa.ntiles;
-          pm[u] = ok ? pmax[(long long)r * sa.ntiles + tt] : -INFINITY;
-          ps[u] = ok ? psum[(long long)r * sa.ntiles + tt] : 0.f;
+          pm[u] = ok ? __ldg(pmax + (long long)r * sa.ntiles + tt) : -INFINITY;
+          ps[u] = ok ? __ldg(psum + (long long)r * sa.ntiles + tt) : 0.f;
         }
         for (int tt = lane + 32 * kPT; tt < sa.ntiles; tt += 32) mx = fmaxf(mx, pmax[(long long)r * sa.ntiles + tt]);
 #pragma unroll
@@ -1016,9 +1041,6 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         s = warp_sum_d(s);
         lse += (double)mx + log(s);
       }
-      const int n = sa.ntiles * kk;
-      const float *cv = sa.cval + (long long)r * n;
-      const int *ct = sa.ctok + (long long)r * n;
       auto emit = [&](int j, const Key &bk) {
         if (lane == 0) {
           bool none = bk.tok == kNoTok;
@@ -1032,12 +1054,6 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
           // Threshold filter: every tile list is sorted best-first, so the
           // kk-th best tile maximum (thr) is a lower bound on the row's kk-th
           // best logit; only tile prefixes >= thr can hold the row's top-kk.
-          float tmax[kPT];
-#pragma unroll
-          for (int u = 0; u < kPT; ++u) {
-            const int tt = lane + 32 * u;
-            tmax[u] = tt < sa.ntiles ? cv[tt * kk] : -INFINITY;
-          }
           float lv = INFINITY;
           int lt = -1;
           for (int p = 0; p < kk; ++p) {
@@ -1075,11 +1091,19 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
 #pragma unroll 1
           for (; scan; scan &= scan - 1) {  // rolled: keeps the kernel small
             const int tt = lane + 32 * (__ffs(scan) - 1);
-            for (int j = 0; j < kk; ++j) {
-              const float x = cv[tt * kk + j];
-              const int tok = ct[tt * kk + j];
-              if (tok < 0 || x < thr) break;
-              L.push(Key{(double)x, tok, 0}, kk);
+            // the tile's whole list in one batch of loads, then the prefix
+            // >= thr inserted (was: one dependent load per candidate)
+            float xs[KMAX];
+            int ts[KMAX];
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j) {
+              xs[j] = j < kk ? __ldg(cv + tt * kk + j) : -INFINITY;
+              ts[j] = j < kk ? __ldg(ct + tt * kk + j) : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j) {
+              if (j >= kk || ts[j] < 0 || xs[j] < thr) break;
+              L.push(Key{(double)xs[j], ts[j], 0}, kk);
             }
           }
           warp_merge<KMAX>(L, kk, emit);

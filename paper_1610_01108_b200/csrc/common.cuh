@@ -68,6 +68,15 @@ inline unsigned long long *&ktime_ptr() {
 
 // Accurate transcendentals (SURVEY §7 hard part (f)): full-precision expf /
 // tanhf, never the .approx forms.
+// acc += w * h on four lanes as two packed FFMA2 (fma.rn.f32x2: the same
+// correctly rounded fma per element as four scalar fmaf, half the issue slots)
+__device__ __forceinline__ void fma4x2(float w, const float4 &h, float4 &acc) {
+  const float2 ww = make_float2(w, w);
+  const float2 lo = __ffma2_rn(ww, make_float2(h.x, h.y), make_float2(acc.x, acc.y));
+  const float2 hi = __ffma2_rn(ww, make_float2(h.z, h.w), make_float2(acc.z, acc.w));
+  acc = make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
 __device__ __forceinline__ float sigmoid_acc(float x) { return 1.0f / (1.0f + expf(-x)); }
 
 __device__ __forceinline__ float warp_max(float v) {

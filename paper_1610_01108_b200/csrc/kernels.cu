@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   int *qrs = reinterpret_cast<int *>(al + (size_t)k * a.jmax);  // [k] row whose query (Q, EQ) and s U_zr row r uses
   int *toks = qrs + k4;                                          // [k] row r's previous token (PROJ epilogue)
   unsigned *wmask = reinterpret_cast<unsigned *>(toks + k4);     // [32] per-warp masks of rows with |q| > kPairSafe
-  float *eqs = reinterpret_cast<float *>(wmask + 32);            // [KA][1024] e^{2q} rows (fast path)
+  float *eqs = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(wmask + 32) + 15) & ~uintptr_t(15));  // [KA][1024] e^{2q} (fast path)
   // H of the sentence streamed into shared memory in chunks of kHP
   // positions by bulk copies, two buffers, issued now and consumed by the
   // context phase: the annotation reads overlap the energies instead of
@@ -402,6 +402,13 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   }
   for (int i = tid; i < a.da; i += blockDim.x) vs[i] = __ldg(a.v + i);
   const bool fast_shape = na == KA && a.da == 1024;
+  // the first P chunk of this warp's first position is loaded before the
+  // prologue's dependent index loads and barriers (consumed by the energies)
+  float nx0[8];
+  if (fast_shape && warp < J) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nx0[u] = __ldg(a.P + ((long long)b * a.jmax + warp) * a.da + lane + 32 * u);
+  }
   // per-row indices staged once: the query row (the select's parent row in
   // the query-folded step) and the previous token
   if (tid < k) qrs[tid] = a.qrow ? a.qrow[b * k + tid] : b * k + tid;
@@ -415,7 +422,9 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
     for (int r = 0; r < na; ++r) {
       const long long qo = (long long)qrs[r] * a.ldq + i;
       if (fabsf(__ldg(a.Q + qo)) > kPairSafe) qm |= 1u << r;
-      if (fast_shape) eqs[r * 1024 + i] = __ldg(a.EQ + qo);
+      // rows 2p, 2p+1 interleaved as float2 pairs (one 64-bit load per
+      // pair in the energies); an odd last row after the pairs
+      if (fast_shape) eqs[r < (KA & ~1) ? ((r >> 1) * 1024 + i) * 2 + (r & 1) : (KA / 2) * 2048 + i] = __ldg(a.EQ + qo);
     }
   }
   qm = __reduce_or_sync(0xffffffffu, qm);
@@ -431,15 +440,30 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
     if (fast_shape && !anybig) {
       // factored tanh over the P row in chunks of 8 values per lane (same
       // per-lane order as one pass), |p| tracked for the safety check
-      float acc[KA];
+      float2 accp[KA / 2 + 1];  // (row 2p+1, row 2p) per pair p; the odd last row in .x of [KA / 2]
 #pragma unroll
-      for (int r = 0; r < KA; ++r) acc[r] = 0.f;
+      for (int p = 0; p <= KA / 2; ++p) accp[p] = make_float2(0.f, 0.f);
+      const float2 *eqs2 = reinterpret_cast<const float2 *>(eqs);
       float pm = 0.f;
+      // the next chunk's P values are loaded while this chunk is computed
+      // (one load latency per position instead of four)
+      float nx[8];
+      if (j == warp) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nx[u] = nx0[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nx[u] = __ldg(pj + lane + 32 * u);
+      }
 #pragma unroll 1
       for (int u0 = 0; u0 < 32; u0 += 8) {
         float ep[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) ep[u] = __ldg(pj + lane + 32 * (u0 + u));
+        for (int u = 0; u < 8; ++u) ep[u] = nx[u];
+        if (u0 + 8 < 32) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) nx[u] = __ldg(pj + lane + 32 * (u0 + 8 + u));
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           pm = fmaxf(pm, fabsf(ep[u]));
@@ -450,24 +474,27 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
           const int i = lane + 32 * (u0 + u);
           const float vi = vs[i];
           // two rows per SFU reciprocal: 1/a = b / (ab), 1/b = a / (ab)
-          // (|p|, |q| <= kPairSafe keeps ab finite); the SFU, not the FMA
-          // pipe, bounds this loop
+          // (|p|, |q| <= kPairSafe keeps ab finite), the pair's arithmetic
+          // as packed f32x2 (the same rounded fma/mul per element as the
+          // scalar form: tanh(p + q_r) = 1 - 2 / a_r)
+          const float2 epp = make_float2(ep[u], ep[u]), one2 = make_float2(1.0f, 1.0f);
 #pragma unroll
-          for (int r = 0; r + 1 < KA; r += 2) {
-            const float a0 = fmaf(ep[u], eqs[r * 1024 + i], 1.0f), a1 = fmaf(ep[u], eqs[(r + 1) * 1024 + i], 1.0f);
-            const float inv = tc_rcp(a0 * a1);
-            acc[r] = fmaf(vi, fmaf(-2.0f, a1 * inv, 1.0f), acc[r]);
-            acc[r + 1] = fmaf(vi, fmaf(-2.0f, a0 * inv, 1.0f), acc[r + 1]);
+          for (int p = 0; p < KA / 2; ++p) {
+            const float2 a2 = __ffma2_rn(epp, eqs2[p * 1024 + i], one2);  // (a_2p, a_2p+1)
+            const float inv = tc_rcp(a2.x * a2.y);
+            const float2 t = __fmul2_rn(a2, make_float2(inv, inv));  // (1 / a_2p+1, 1 / a_2p)
+            accp[p] = __ffma2_rn(make_float2(vi, vi), __ffma2_rn(make_float2(-2.0f, -2.0f), t, one2), accp[p]);
           }
           if constexpr (KA % 2 == 1)
-            acc[KA - 1] = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], eqs[(KA - 1) * 1024 + i], 1.0f)), 1.0f),
-                               acc[KA - 1]);
+            accp[KA / 2].x = fmaf(vi, fmaf(-2.0f, tc_rcp(fmaf(ep[u], eqs[(KA / 2) * 2048 + i], 1.0f)), 1.0f),
+                                  accp[KA / 2].x);
         }
       }
       if (!(warp_max(pm) > kPairSafe)) {
 #pragma unroll
         for (int r = 0; r < KA; ++r) {
-          const float sum = warp_sum(acc[r]);
+          const float2 ap = accp[r / 2];
+          const float sum = warp_sum(r == KA - 1 && KA % 2 == 1 ? ap.x : (r & 1) ? ap.x : ap.y);
           if (lane == 0) al[r * a.jmax + j] = sum;
         }
         done = true;
@@ -551,12 +578,7 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
           if (r < na) {  // positions summed in order, as the global-memory loop below
             const float w = al[r * a.jmax + j0 + jj];
 #pragma unroll
-            for (int i = 0; i < kQ; ++i) {
-              acc[i][r].x = fmaf(w, h[i].x, acc[i][r].x);
-              acc[i][r].y = fmaf(w, h[i].y, acc[i][r].y);
-              acc[i][r].z = fmaf(w, h[i].z, acc[i][r].z);
-              acc[i][r].w = fmaf(w, h[i].w, acc[i][r].w);
-            }
+            for (int i = 0; i < kQ; ++i) fma4x2(w, h[i], acc[i][r]);
           }
       }
       if (c + kNB < nch) {
@@ -711,7 +733,7 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
     const char *e = getenv("AMUN_ATTN_FUSED");  // 0: two-phase kernels
     return !(e && e[0] == '0');
   }();
-  const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)(2 * ((k + 3) & ~3) + 32) +
+  const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)(2 * ((k + 3) & ~3) + 32) + 16 +
                         (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0) +
                         (a.su ? 128 + sizeof(float) * 5 * 2 * (size_t)a.dh2 + 5 * sizeof(uint64_t)
                               : a.dh2 == 4 * 512 ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);

@@ -1666,8 +1666,12 @@ amun_result *decode_run(const std::vector<amun_model *> &ms, const int32_t *src_
     // folded query (step_rows): the bucket's first Q / EQ / s U_zr from the
     // initial rows; every later step's come from the deep-output GEMM
     for (int m = 0; m < n_models; ++m)
-      if (use_tcg && L.tsteps[m].proj && L.tsteps[m].dq_ok && L.eb[m].HX && L.lo.tc)
+      if (use_tcg && L.tsteps[m].proj && L.tsteps[m].dq_ok && L.eb[m].HX && L.lo.tc) {
         qs_prologue(c, ms[m], L.db[m], L.tsteps[m], L.R);
+        L.mr.dim[m].split = 0;  // the step reads the gathered rows in fp32 only (attention, GRU-B)
+      } else {
+        L.mr.dim[m].split = 1;
+      }
     SelectArgs &sa = L.sa;
     sa = SelectArgs{};
     sa.kk = kk;

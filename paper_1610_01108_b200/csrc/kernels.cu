@@ -1113,19 +1113,29 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
 #pragma unroll 1
           for (; scan; scan &= scan - 1) {  // rolled: keeps the kernel small
             const int tt = lane + 32 * (__ffs(scan) - 1);
-            // the tile's whole list in one batch of loads, then the prefix
-            // >= thr inserted (was: one dependent load per candidate)
-            float xs[KMAX];
-            int ts[KMAX];
+            // the tile's list in batches of independent loads (the whole
+            // list for beams <= 8, 4 at a time above: whole lists cost more
+            // than they save at beam 12), the prefix >= thr inserted (was:
+            // one dependent load per candidate)
+            constexpr int kB = KMAX <= 8 ? KMAX : 4;
+            for (int j0 = 0; j0 < kk; j0 += kB) {
+              float xs[kB];
+              int ts[kB];
 #pragma unroll
-            for (int j = 0; j < KMAX; ++j) {
-              xs[j] = j < kk ? __ldg(cv + tt * kk + j) : -INFINITY;
-              ts[j] = j < kk ? __ldg(ct + tt * kk + j) : -1;
-            }
+              for (int u = 0; u < kB; ++u) {
+                xs[u] = j0 + u < kk ? __ldg(cv + tt * kk + j0 + u) : -INFINITY;
+                ts[u] = j0 + u < kk ? __ldg(ct + tt * kk + j0 + u) : -1;
+              }
+              bool more = true;
 #pragma unroll
-            for (int j = 0; j < KMAX; ++j) {
-              if (j >= kk || ts[j] < 0 || xs[j] < thr) break;
-              L.push(Key{(double)xs[j], ts[j], 0}, kk);
+              for (int u = 0; u < kB; ++u) {
+                if (!more || ts[u] < 0 || xs[u] < thr) {
+                  more = false;
+                } else {
+                  L.push(Key{(double)xs[u], ts[u], 0}, kk);
+                }
+              }
+              if (!more) break;
             }
           }
           warp_merge<KMAX>(L, kk, emit);
@@ -1318,7 +1328,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         for (int u = 0; u < 8; ++u) {
           if (dst[u] < 0) continue;
           *reinterpret_cast<float4 *>(XS + dst[u]) = v[u];
-          if (XSh) {  // 4 halves = 8 bytes (ldxh, hpad and s_off are multiples of 4)
+          if (XSh && md.split) {  // 4 halves = 8 bytes (ldxh, hpad and s_off are multiples of 4)
             __half h4[4], l4[4];
             split_h(v[u].x, h4[0], l4[0]);
             split_h(v[u].y, h4[1], l4[1]);

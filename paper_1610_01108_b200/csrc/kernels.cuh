@@ -88,6 +88,7 @@ struct RowDims {
   // column c at c + (c >= de ? hpad : 0)
   int ldxh, hpad;
   int y = 1;  // 0: the step reads y only through per-token tables (projected context): no y gather
+  int split = 1;  // 0: nothing reads the gathered rows' fp16 splits (query folded forward): fp32 only
 };
 
 struct ModelRows {  // per-model decoder row buffers (device arrays of pointers)

@@ -358,6 +358,18 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
 // the 3 dh + de wide projected rows (1024 threads; 512 threads with two
 // quads each above beam 8, where 64 registers would spill), and the gate
 // epilogue.
+// projected-context annotation staging: kProjNB buffers of kProjHP positions
+#ifndef AMUN_PROJ_HP
+#define AMUN_PROJ_HP 4
+#endif
+#ifndef AMUN_PROJ_NB
+#define AMUN_PROJ_NB 3
+#endif
+// beams above 12 (e^{2q} rows of 16 beams: 64 KB) keep five 2-position buffers
+constexpr int proj_hp(int ka) { return ka <= 12 ? AMUN_PROJ_HP : 2; }
+constexpr int proj_nb(int ka) { return ka <= 12 ? AMUN_PROJ_NB : 5; }
+// the attn_sent_kernel instantiation a beam width runs (launch_attention's switch)
+constexpr int attn_ka(int k) { return (k <= 6 || k == 8 || k == 10 || k == 12) ? k : 16; }
 template <int KA>
 constexpr int attn_threads(bool proj) { return proj && KA <= 8 ? 1024 : 512; }
 template <int KA, bool PROJ>
@@ -381,9 +393,11 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   // positions by bulk copies, two buffers, issued now and consumed by the
   // context phase: the annotation reads overlap the energies instead of
   // stalling the context loop (one thread per 4 columns: dh2 == 4 x threads)
-  // PROJ rows are 14 KB per position: five 2-position buffers keep about
-  // ten positions in flight (the context loop is load-latency bound)
-  constexpr int kHP = PROJ ? 2 : 4, kNB = PROJ ? 5 : 2;
+  // PROJ rows are 14 KB per position: three 4-position buffers keep twelve
+  // positions in flight with one CTA barrier per 4 positions (same-box A/B:
+  // 4x3 and 6x2 ~1.3% faster than 2x5, 3x3 in between; 171 KB; beams above
+  // 12 keep 2x5, 143 KB, next to their 64 KB of e^{2q} rows)
+  constexpr int kHP = PROJ ? proj_hp(KA) : 4, kNB = PROJ ? proj_nb(KA) : 2;
   const bool hsmem = PROJ || a.dh2 == 4 * (int)blockDim.x;
   float *hbuf = reinterpret_cast<float *>(
       (reinterpret_cast<uintptr_t>(eqs + (a.da == 1024 ? k * 1024 : 0)) + 127) & ~uintptr_t(127));
@@ -735,7 +749,7 @@ int launch_attention(const AttnArgs &a, int R, cudaStream_t st) {
   }();
   const size_t smem_s = sizeof(float) * ((size_t)a.da + (size_t)k * a.jmax) + sizeof(int) * (size_t)(2 * ((k + 3) & ~3) + 32) + 16 +
                         (a.da == 1024 ? sizeof(float) * (size_t)k * 1024 : 0) +
-                        (a.su ? 128 + sizeof(float) * 5 * 2 * (size_t)a.dh2 + 5 * sizeof(uint64_t)
+                        (a.su ? 128 + sizeof(float) * proj_nb(attn_ka(k)) * proj_hp(attn_ka(k)) * (size_t)a.dh2 + proj_nb(attn_ka(k)) * sizeof(uint64_t)
                               : a.dh2 == 4 * 512 ? 128 + sizeof(float) * 2 * 4 * (size_t)a.dh2 + 2 * sizeof(uint64_t) : 0);
   // The kernel is chosen from per-call constants only (beam width, model
   // layout), never from the bucket's longest sentence: the fused and the

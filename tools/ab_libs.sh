@@ -5,6 +5,7 @@
 # rounds.  Profiling only.
 mkdir -p gpurun_out
 LIB=paper_1610_01108_b200/libamun_b200.so
+cp $LIB /tmp/ab_orig.so
 for r in 1 2; do for v in ${VARS:-A B}; do
   cp ab/lib_$v.so $LIB
   for c in ${CFGS:-cfg4 cfg2}; do
@@ -12,4 +13,4 @@ for r in 1 2; do for v in ${VARS:-A B}; do
     python -c "import json;d=json.loads(open('gpurun_out/ab_${v}_${c}_$r.json').read().strip().splitlines()[-1]);print('$v $c $r', round(d['value']), d['ms_per_step'], d['clocks']['sm_mhz'])"
   done
 done; done
-cp ab/lib_B.so $LIB
+cp /tmp/ab_orig.so $LIB

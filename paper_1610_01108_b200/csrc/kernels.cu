@@ -365,6 +365,11 @@ __global__ void __launch_bounds__(kCtxCols * kCtxGroups) attn_context_kernel(Att
 #ifndef AMUN_PROJ_NB
 #define AMUN_PROJ_NB 3
 #endif
+// P values per lane per energies chunk (the next chunk loads during this one)
+#ifndef AMUN_ENERGY_CHUNK
+#define AMUN_ENERGY_CHUNK 8
+#endif
+constexpr int kEC = AMUN_ENERGY_CHUNK;
 // beams above 12 (e^{2q} rows of 16 beams: 64 KB) keep five 2-position buffers
 constexpr int proj_hp(int ka) { return ka <= 12 ? AMUN_PROJ_HP : 2; }
 constexpr int proj_nb(int ka) { return ka <= 12 ? AMUN_PROJ_NB : 5; }
@@ -418,10 +423,10 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
   const bool fast_shape = na == KA && a.da == 1024;
   // the first P chunk of this warp's first position is loaded before the
   // prologue's dependent index loads and barriers (consumed by the energies)
-  float nx0[8];
+  float nx0[kEC];
   if (fast_shape && warp < J) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) nx0[u] = __ldg(a.P + ((long long)b * a.jmax + warp) * a.da + lane + 32 * u);
+    for (int u = 0; u < kEC; ++u) nx0[u] = __ldg(a.P + ((long long)b * a.jmax + warp) * a.da + lane + 32 * u);
   }
   // per-row indices staged once: the query row (the select's parent row in
   // the query-folded step) and the previous token
@@ -461,30 +466,30 @@ __global__ void __launch_bounds__(attn_threads<KA>(PROJ), (KA <= 8 && !PROJ) ? 2
       float pm = 0.f;
       // the next chunk's P values are loaded while this chunk is computed
       // (one load latency per position instead of four)
-      float nx[8];
+      float nx[kEC];
       if (j == warp) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) nx[u] = nx0[u];
+        for (int u = 0; u < kEC; ++u) nx[u] = nx0[u];
       } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) nx[u] = __ldg(pj + lane + 32 * u);
+        for (int u = 0; u < kEC; ++u) nx[u] = __ldg(pj + lane + 32 * u);
       }
 #pragma unroll 1
-      for (int u0 = 0; u0 < 32; u0 += 8) {
-        float ep[8];
+      for (int u0 = 0; u0 < 32; u0 += kEC) {
+        float ep[kEC];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) ep[u] = nx[u];
-        if (u0 + 8 < 32) {
+        for (int u = 0; u < kEC; ++u) ep[u] = nx[u];
+        if (u0 + kEC < 32) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) nx[u] = __ldg(pj + lane + 32 * (u0 + 8 + u));
+          for (int u = 0; u < kEC; ++u) nx[u] = __ldg(pj + lane + 32 * (u0 + kEC + u));
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kEC; ++u) {
           pm = fmaxf(pm, fabsf(ep[u]));
           ep[u] = tc_exp2(ep[u] * kTwoLog2e);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kEC; ++u) {
           const int i = lane + 32 * (u0 + u);
           const float vi = vs[i];
           // two rows per SFU reciprocal: 1/a = b / (ab), 1/b = a / (ab)

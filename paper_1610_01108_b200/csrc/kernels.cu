@@ -1027,6 +1027,15 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   const int b = blockIdx.x;
   if (bs.done[b]) return;
   const int t = bs.steps[b];  // this sentence's step index (graph-replay safe: no host-side t)
+  // the update phase's per-sentence scalars, read now (their latency overlaps
+  // the row phase instead of serialising thread 0's update)
+  int fin_n0 = 0, cap0 = 0;
+  double best_fin0 = 0.0;
+  if (threadIdx.x == 0) {
+    fin_n0 = bs.fin_n[b];
+    best_fin0 = bs.best_fin[b];
+    cap0 = bs.cap[b];
+  }
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int na = bs.n_act[b];
   const int kk = sa.kk;
@@ -1261,12 +1270,12 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     const int rowbase = (b * bs.cap_max + t) * k;
     for (int j = 0; j < nch; ++j) {
       if (ch_tok[j] == 0) {  // EOS_ID -> finished list (unbounded in the reference)
-        int idx = bs.fin_n[b]++;
+        const int idx = fin_n0++;
         long long fo = (long long)b * bs.fin_cap + idx;
         bs.fin_score[fo] = ch_v[j];
         bs.fin_t[fo] = t;
         bs.fin_par[fo] = ch_par[j];
-        if (ch_v[j] > bs.best_fin[b]) bs.best_fin[b] = ch_v[j];
+        if (ch_v[j] > best_fin0) best_fin0 = ch_v[j];
         fin_par[nfin] = ch_par[j];
         fin_idx[nfin] = idx;
         ++nfin;
@@ -1281,6 +1290,10 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         ch_par[slot] = ch_par[j];
       }
     }
+    if (nfin > 0) {
+      bs.fin_n[b] = fin_n0;
+      bs.best_fin[b] = best_fin0;
+    }
     bs.steps[b] = t + 1;
     int done = 0;
     if (newna == 0) {
@@ -1292,9 +1305,9 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         bs.tok[b * k + i] = ch_tok[i];
         if (bs.qrow) bs.qrow[b * k + i] = b * k + ch_par[i];
       }
-      if (bs.fin_n[b] > 0 && best_new <= bs.best_fin[b]) done = 1;  // search.py:195-198
+      if (fin_n0 > 0 && best_new <= best_fin0) done = 1;  // search.py:195-198
     }
-    if (t + 1 >= bs.cap[b]) done = 1;
+    if (t + 1 >= cap0) done = 1;
     if (done) {
       bs.done[b] = 1;
       atomicAdd(bs.n_done, 1);

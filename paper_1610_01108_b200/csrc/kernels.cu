@@ -1020,6 +1020,8 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   // phase-1 row candidates [k][kk] (log-prob, token), consumed by phase 2
   double *c_lp = reinterpret_cast<double *>(smraw + (((size_t)k * (sizeof(double) + 4 * sizeof(int)) + 15) & ~size_t(15)));
   int *c_tok = reinterpret_cast<int *>(c_lp + (size_t)k * sa.kk);
+  // the beam's scores, staged during the row phase for the sentence top-k
+  double *s_sc = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(c_tok + (size_t)k * sa.kk) + 7) & ~uintptr_t(7));
   __shared__ int s_nch, s_newna, s_nfin;
 
   const CtaClock kclk(sa.kt);
@@ -1039,6 +1041,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   const int na = bs.n_act[b];
   const int kk = sa.kk;
+  for (int i = threadIdx.x; i < na; i += blockDim.x) s_sc[i] = bs.score[b * k + i];
   const int n_models = mr.n_models;
 
   // ---- phase 1: per active row, log-sum-exp and top-kk candidates
@@ -1217,7 +1220,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
     Key me{-INFINITY, -1, -1};
     if (lane < n) {
       const int par = lane / kk;
-      me = Key{bs.score[b * k + par] + c_lp[lane], c_tok[lane], par};
+      me = Key{s_sc[par] + c_lp[lane], c_tok[lane], par};
     }
     const bool valid = lane < n && me.tok >= 0;
     int rank = 0, nvalid = 0;
@@ -1246,7 +1249,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs sa, BeamState bs
         n, k,
         [&](int e) {
           int par = e / kk;
-          return Key{bs.score[b * k + par] + clp[e], ctk[e], par};
+          return Key{s_sc[par] + clp[e], ctk[e], par};
         },
         [&](int j, const Key &bk) {
           if (bk.tok == kNoTok) return;
@@ -1422,7 +1425,7 @@ static void launch_select_t(const SelectArgs &sa, const BeamState &bs, const Mod
 void launch_select(const SelectArgs &sa, const BeamState &bs, const ModelRows &mr, cudaStream_t st) {
   if (mr.n_models > kMaxModels) throw Error(4, "at most 8 ensemble members are supported on the device path");
   size_t smem = (((size_t)bs.k * (sizeof(double) + 4 * sizeof(int)) + 15) & ~size_t(15)) +
-                (size_t)bs.k * sa.kk * (sizeof(double) + sizeof(int));
+                (size_t)bs.k * sa.kk * (sizeof(double) + sizeof(int)) + 8 + (size_t)bs.k * sizeof(double);
   const int need = std::max(bs.k, sa.kk);  // list sizes used in phases 1 and 2
   if (sa.fused) {
     if (need <= 1) launch_select_t<1, true>(sa, bs, mr, smem, st);
